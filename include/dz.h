@@ -1,0 +1,195 @@
+/*
+ * dz.h -- C ABI of libdz: block-causal chunk attention for DreamZero-style
+ * chunk-wise autoregressive video/action diffusion on NVIDIA B200 (sm_100a).
+ *
+ * The operation (arXiv 2602.15922, PAPER.md):
+ *   * A chunk is K latent frames of view-concatenated video tokens plus the
+ *     chunk's action tokens (l.94 "concatenate all views into a single frame",
+ *     l.99 "each chunk has a fixed number of latent frames K").
+ *   * During one denoising step the current noisy chunk attends
+ *     bidirectionally to itself and causally to the KV cache of clean previous
+ *     chunks (Fig. 10 / l.505; Alg. 2 l.584-585, u_theta(...; KV, ..., update=False)).
+ *   * Ground-truth injection appends the clean chunk's keys/values to the cache
+ *     (Alg. 2 l.569-570 and l.601-602, update=True); predicted latents are
+ *     never cached (l.603).
+ *   * Q and K first get per-head RMSNorm and 3D (frame, height, width) RoPE
+ *     (BASELINE.json north_star).  Conventions (readings A1-A9):
+ *     x' = RoPE(x / sqrt(mean(x^2) + eps) * g); RoPE rotates interleaved pairs
+ *     (2i, 2i+1) inside axis slices [t | h | w] of widths rope_dims, by angle
+ *     p_axis * theta^(-2i / d_axis).
+ *
+ * Tensor conventions (all device memory, caller-owned, contiguous):
+ *   * activations q_raw, k_raw, v_raw, out: bf16 [batch][n_local][heads][head_dim]
+ *     (token-major, what a QKV projection emits); n_local = n / world_size.
+ *   * positions: int32 [n_local][3] = (t, h, w) of this rank's tokens, global
+ *     coordinates (the same positions for every batch element).
+ *   * gains: fp32 [heads * head_dim] (q_gain, k_gain).
+ *   * cache storage: one caller-owned device buffer of dz_cache_bytes() bytes;
+ *     K' is kept post-norm/post-RoPE in fp16, V as given in bf16, token-major
+ *     per rank: [batch][slots][heads/world_size][head_dim].
+ *
+ * Streams and concurrency: every kernel and NCCL call is enqueued on the given
+ * stream (a cudaStream_t passed as void*); no call synchronises the host.
+ * Inputs must stay untouched until the stream passes the call.  A context is
+ * single-owner: calls on one context must be serialised by the caller;
+ * different contexts may be used concurrently.
+ *
+ * Errors: argument/state validation happens before anything is enqueued and
+ * leaves the context unchanged.  A CUDA or NCCL enqueue error returns
+ * DZ_ECUDA / DZ_ENCCL and poisons the context (later calls return DZ_ESTATE
+ * until dz_destroy).  Device faults surface at the caller's next sync.  The
+ * library never throws and never aborts.
+ */
+#ifndef DZ_H_
+#define DZ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DZ_API __attribute__((visibility("default")))
+#else
+#define DZ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dz_ctx dz_ctx; /* opaque; one per (layer, batch group) */
+
+typedef enum {
+  DZ_OK = 0,
+  DZ_EINVAL = -1,    /* null pointer, bad flag, misaligned pointer            */
+  DZ_ESHAPE = -2,    /* unsupported shape (head_dim, rope split, n % world)  */
+  DZ_ECAPACITY = -3, /* cache or staging capacity exceeded                   */
+  DZ_ESTATE = -4,    /* chunk ordering violated, nothing staged, poisoned    */
+  DZ_ECUDA = -5,     /* CUDA error while enqueuing (see dz_last_error)       */
+  DZ_ENCCL = -6,     /* NCCL error while enqueuing                           */
+  DZ_ERANGE = -7     /* sqrt(head_dim)*max|gain| would overflow fp16 Q'/K'    */
+} dz_status;
+
+enum { DZ_CLEAN = 0, DZ_NOISY = 1 }; /* dz_span.kind (Fig. 10: C chunks vs Z/Y chunks) */
+
+enum {
+  DZ_FLAG_NONE = 0,
+  DZ_FLAG_WRITE_LSE = 1 /* keep a per-row log-sum-exp of the last attend (dz_copy_lse) */
+};
+
+typedef struct {
+  int32_t batch;                 /* B: independent sequences (e.g. CFG cond/uncond) */
+  int32_t heads;                 /* global heads H (Wan-14B: 40)                            */
+  int32_t head_dim;              /* D in {64, 128}                                          */
+  int32_t rope_dims[3];          /* (d_t, d_h, d_w), each even, sum == head_dim              */
+  float rope_theta;              /* 0 => 10000                                              */
+  float rms_eps;                 /* 0 => 1e-6                                               */
+  float softmax_scale;           /* 0 => 1/sqrt(head_dim)                                   */
+  int64_t cache_capacity_tokens; /* committed tokens per batch element (global sequence)    */
+  int32_t max_chunk_tokens;      /* largest chunk n (global), staged after the committed part */
+  int32_t window_slack_tokens;   /* extra slots so dz_evict_front rarely compacts; 0 = none */
+  const float* q_gain;           /* device fp32 [heads*head_dim]; must outlive the ctx      */
+  const float* k_gain;           /* device fp32 [heads*head_dim]; must outlive the ctx      */
+  float max_abs_gain;            /* host-side bound on |gain| (checked: DZ_ERANGE)           */
+  void* cache_storage;           /* device buffer of >= dz_cache_bytes(cfg) bytes, 256-B aligned */
+  size_t cache_bytes;
+  void* nccl_comm;               /* ncclComm_t when world_size > 1, else NULL               */
+  int32_t world_size;            /* Ulysses sequence-parallel ranks (heads % world_size == 0) */
+  int32_t rank;
+  int32_t flags;                 /* DZ_FLAG_*                                               */
+} dz_config;
+
+/* One chunk of the sequence (Fig. 10): id, kind and its global token count. */
+typedef struct {
+  int32_t chunk_id;        /* chunk index; committed ids must increase                  */
+  int32_t kind;            /* DZ_CLEAN or DZ_NOISY                                       */
+  int32_t n_tokens;        /* global tokens of the chunk; n_tokens % world_size == 0     */
+  const int32_t* pos_thw;  /* device int32 [n_tokens/world_size][3], this rank's tokens  */
+} dz_span;
+
+/* Bytes of cache storage the caller must provide for cfg:
+ *   2 tensors (K' fp16, V bf16) x batch x (capacity + max_chunk + slack) x
+ *   (heads / world_size) x head_dim x 2 B, rounded up to 256 B. 0 if cfg is invalid. */
+DZ_API size_t dz_cache_bytes(const dz_config* cfg);
+
+/* Validates cfg, computes the RoPE frequencies (fp64, host), allocates the
+ * context's own device workspace (Q' and, under SP, the all-to-all buffers).
+ * On success *out owns that workspace until dz_destroy. */
+DZ_API dz_status dz_create(const dz_config* cfg, dz_ctx** out);
+
+/* Cache append of a clean chunk (Alg. 2 l.601-602, update=True): K' =
+ * RoPE(RMSNorm(k_raw)) and V are written to slots [valid, valid + n) and
+ * committed.  Requires chunk->kind == DZ_CLEAN, chunk_id greater than the last
+ * committed id (else DZ_ESTATE) and valid + n <= capacity (else DZ_ECAPACITY).
+ * k_raw, v_raw: bf16 [batch][n_local][heads][head_dim]. */
+DZ_API dz_status dz_append_kv(dz_ctx* ctx, const void* k_raw, const void* v_raw, const dz_span* chunk, void* stream);
+
+/* One denoising step of the current chunk (Alg. 2 l.584-585, update=False):
+ * out = softmax(Q' K'^T * scale) V over keys = committed chunks (all have id <
+ * chunk_id) plus the chunk itself (bidirectional, Fig. 10).  Q' and the chunk's
+ * K'/V are computed here (K1 prologue) and staged after the committed slots;
+ * the committed cache is never modified.  chunk_id must exceed every committed
+ * id (else DZ_ESTATE); n <= max_chunk_tokens (else DZ_ECAPACITY).
+ * out: bf16 [batch][n_local][heads][head_dim]. */
+DZ_API dz_status dz_attend_chunk(dz_ctx* ctx, const void* q_raw, const void* k_raw, const void* v_raw,
+                          const dz_span* chunk, void* out, void* stream);
+
+/* Commit the chunk staged by the last dz_attend_chunk (which must have had
+ * kind DZ_CLEAN and this chunk_id): the model-side "attend the clean chunk,
+ * then update the cache" form of Alg. 2 l.601-602.  Moves no data.  DZ_ESTATE
+ * if nothing matching is staged; DZ_ECAPACITY if the cache is full. */
+DZ_API dz_status dz_commit_staged(dz_ctx* ctx, int32_t chunk_id, void* stream);
+
+/* Drop the n_chunks oldest committed chunks (sliding context window, PAPER.md
+ * l.510 "maximum context length is 8 latent frames").  RoPE is relative, so the
+ * remaining keys need no re-rotation.  Usually bookkeeping only; compacts the
+ * storage with a device copy on `stream` when the window reaches its end. */
+DZ_API dz_status dz_evict_front(dz_ctx* ctx, int32_t n_chunks, void* stream);
+
+/* Committed state: tokens per batch element, number of chunks, last chunk id (-1 if none). */
+DZ_API dz_status dz_cache_state(const dz_ctx* ctx, int64_t* valid_tokens, int32_t* n_chunks, int32_t* last_chunk_id);
+
+/* Device pointers to the K' (fp16) and V (bf16) slot 0 of batch element b, and
+ * the element stride between slots (= heads/world_size * head_dim); committed
+ * tokens are slots [0, valid).  For tests and checkpoint dumps. */
+DZ_API dz_status dz_cache_view(const dz_ctx* ctx, int32_t b, void** k_slot0, void** v_slot0, int64_t* slot_stride);
+
+/* Copy the fp32 log-sum-exp rows [batch][heads/world_size][n] of the last
+ * attend (needs DZ_FLAG_WRITE_LSE) into a caller device buffer on stream. */
+DZ_API dz_status dz_copy_lse(dz_ctx* ctx, float* dst, size_t dst_elems, void* stream);
+
+/* Tile map of the last attend as seen by the attention kernel's planner for
+ * one (batch, head) unit: host uint8 [n_q_tiles][n_kv_tiles], 0 SKIP, 1
+ * PARTIAL, 2 FULL (same encoding as the oracle's classifier). */
+DZ_API dz_status dz_get_tile_map(const dz_ctx* ctx, uint8_t* host, size_t cap, int32_t* n_q_tiles, int32_t* n_kv_tiles,
+                          int32_t* bm, int32_t* bn);
+
+/* Releases the context's host state and device workspace (not the caller's
+ * buffers).  Safe on NULL. */
+DZ_API dz_status dz_destroy(dz_ctx* ctx);
+
+DZ_API const char* dz_status_string(dz_status s);
+DZ_API const char* dz_last_error(const dz_ctx* ctx);
+
+/* NCCL plumbing for Ulysses sequence parallelism (one process per GPU).
+ * dz_nccl_unique_id fills 128 bytes on rank 0 (broadcast them with the host's
+ * own process group); dz_nccl_comm_init creates a communicator on the current
+ * device; dz_nccl_comm_destroy frees it. */
+DZ_API dz_status dz_nccl_unique_id(void* id128);
+DZ_API dz_status dz_nccl_comm_init(int32_t world_size, const void* id128, int32_t rank, void** comm);
+DZ_API dz_status dz_nccl_comm_destroy(void* comm);
+
+/* Hang diagnosis: every mbarrier wait in the attention kernel is bounded (5 s).
+ * A wait that times out records {1, block, warp, barrier smem address, parity,
+ * SM id, barrier-block base, 0} and makes all later waits return, so the kernel
+ * finishes with garbage output instead of hanging the GPU.  Copies that record
+ * (zeros if no timeout) to host8[8]; reset != 0 clears it.  Synchronous. */
+DZ_API dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset);
+
+/* Number of attention work units (batch x heads/world_size x query-tile pairs)
+ * for an n-token chunk; the persistent grid is min(units, SM count). */
+DZ_API int32_t dz_attention_units(const dz_ctx* ctx, int32_t n_tokens);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DZ_H_ */

@@ -1,0 +1,301 @@
+"""paper_2602_15922_b200 -- B200-native block-causal chunk attention (DreamZero, arXiv 2602.15922).
+
+A thin ctypes binding over ``libdz.so`` (C ABI: ``include/dz.h``).  Every step
+of the hot path -- the fused RMSNorm + 3D RoPE prologue, the tcgen05 flash
+attention over the KV cache, the cache append and the Ulysses exchange -- runs
+inside the library.  This module only marshals arguments: it checks dtypes,
+shapes and devices, passes ``data_ptr()`` values and the current torch CUDA
+stream, and owns the device buffers (PyTorch is used for memory, streams and
+process groups only).  There is no CPU fallback: if ``libdz.so`` is missing or
+was built for another architecture, importing :func:`lib` raises.
+
+Paper mapping: ``ChunkKVCache.append`` is the update=True cache
+write of Alg. 2 (l.569-570, l.601-602); ``ChunkKVCache.attend`` is one
+denoising step's self-attention, update=False (l.584-585), under the Fig. 10
+mask (l.502-507).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+__all__ = ["DzError", "lib", "ChunkKVCache", "CLEAN", "NOISY", "FLAG_WRITE_LSE", "nccl_unique_id",
+           "nccl_comm_init", "nccl_comm_destroy", "status_string"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdz.so")
+
+CLEAN, NOISY = 0, 1
+FLAG_WRITE_LSE = 1
+
+STATUS = {0: "DZ_OK", -1: "DZ_EINVAL", -2: "DZ_ESHAPE", -3: "DZ_ECAPACITY", -4: "DZ_ESTATE",
+          -5: "DZ_ECUDA", -6: "DZ_ENCCL", -7: "DZ_ERANGE"}
+
+
+class DzError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class DzConfig(ctypes.Structure):
+    _fields_ = [
+        ("batch", ctypes.c_int32), ("heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+        ("rope_dims", ctypes.c_int32 * 3),
+        ("rope_theta", ctypes.c_float), ("rms_eps", ctypes.c_float), ("softmax_scale", ctypes.c_float),
+        ("cache_capacity_tokens", ctypes.c_int64), ("max_chunk_tokens", ctypes.c_int32),
+        ("window_slack_tokens", ctypes.c_int32),
+        ("q_gain", ctypes.c_void_p), ("k_gain", ctypes.c_void_p), ("max_abs_gain", ctypes.c_float),
+        ("cache_storage", ctypes.c_void_p), ("cache_bytes", ctypes.c_size_t),
+        ("nccl_comm", ctypes.c_void_p), ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+    ]
+
+
+class DzSpan(ctypes.Structure):
+    _fields_ = [("chunk_id", ctypes.c_int32), ("kind", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
+                ("pos_thw", ctypes.c_void_p)]
+
+
+# every entry point declared in include/dz.h: (name, restype, argtypes)
+P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+SIGNATURES = [
+    ("dz_cache_bytes", SZ, [ctypes.POINTER(DzConfig)]),
+    ("dz_create", I32, [ctypes.POINTER(DzConfig), ctypes.POINTER(P)]),
+    ("dz_append_kv", I32, [P, P, P, ctypes.POINTER(DzSpan), P]),
+    ("dz_attend_chunk", I32, [P, P, P, P, ctypes.POINTER(DzSpan), P, P]),
+    ("dz_commit_staged", I32, [P, I32, P]),
+    ("dz_evict_front", I32, [P, I32, P]),
+    ("dz_cache_state", I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+    ("dz_cache_view", I32, [P, I32, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(I64)]),
+    ("dz_copy_lse", I32, [P, P, SZ, P]),
+    ("dz_get_tile_map", I32, [P, P, SZ, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32),
+                              ctypes.POINTER(I32)]),
+    ("dz_destroy", I32, [P]),
+    ("dz_status_string", ctypes.c_char_p, [I32]),
+    ("dz_last_error", ctypes.c_char_p, [P]),
+    ("dz_nccl_unique_id", I32, [P]),
+    ("dz_nccl_comm_init", I32, [I32, P, I32, ctypes.POINTER(P)]),
+    ("dz_nccl_comm_destroy", I32, [P]),
+    ("dz_attention_units", I32, [P, I32]),
+    ("dz_debug_watchdog", I32, [P, I32]),
+]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdz.so (built by ``python -m paper_2602_15922_b200.build``); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not found: build it with `python -m paper_2602_15922_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def status_string(s: int) -> str:
+    return lib().dz_status_string(s).decode()
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _need(t: torch.Tensor, name: str, dtype: torch.dtype, shape: Sequence[int], device: torch.device):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def watchdog(reset: bool = True):
+    """The attention kernel's hang record: (fired, block, warp, bar addr, parity, smid, bars base, 0)."""
+    buf = (ctypes.c_uint32 * 8)()
+    s = lib().dz_debug_watchdog(ctypes.cast(buf, P), int(reset))
+    if s:
+        raise DzError(s, "dz_debug_watchdog")
+    return list(buf)
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    s = lib().dz_nccl_unique_id(ctypes.cast(buf, P))
+    if s:
+        raise DzError(s, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def nccl_comm_init(world_size: int, uid: bytes, rank: int) -> int:
+    buf = ctypes.create_string_buffer(uid, 128)
+    comm = P()
+    s = lib().dz_nccl_comm_init(world_size, ctypes.cast(buf, P), rank, ctypes.byref(comm))
+    if s:
+        raise DzError(s, "ncclCommInitRank failed")
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int):
+    lib().dz_nccl_comm_destroy(comm)
+
+
+class ChunkKVCache:
+    """One layer's KV cache of clean chunks plus the chunk-attention step.
+
+    Shapes: activations bf16 ``[batch, n_local, heads, head_dim]``; positions
+    int32 ``[n_local, 3]`` (t, h, w); gains fp32 ``[heads, head_dim]``.
+    ``world_size > 1`` shards the sequence Ulysses-style over ranks (needs an
+    NCCL communicator from :func:`nccl_comm_init`).
+    """
+
+    def __init__(self, batch: int, heads: int, head_dim: int, capacity: int, max_chunk: int,
+                 rope_dims: Sequence[int], q_gain: torch.Tensor, k_gain: torch.Tensor,
+                 rope_theta: float = 10000.0, rms_eps: float = 1e-6, softmax_scale: float = 0.0,
+                 window_slack: int = 0, world_size: int = 1, rank: int = 0, nccl_comm: int = 0,
+                 flags: int = 0, device: Optional[torch.device] = None):
+        L = lib()
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.type != "cuda":
+            raise ValueError(f"ChunkKVCache needs a CUDA device, got {dev} (there is no CPU path)")
+        self.device = dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
+        self.batch, self.heads, self.head_dim = batch, heads, head_dim
+        self.world_size, self.rank = world_size, rank
+        self.heads_local = heads // world_size
+        _need(q_gain, "q_gain", torch.float32, (heads, head_dim), self.device)
+        _need(k_gain, "k_gain", torch.float32, (heads, head_dim), self.device)
+        self.q_gain, self.k_gain = q_gain, k_gain
+        cfg = DzConfig()
+        cfg.batch, cfg.heads, cfg.head_dim = batch, heads, head_dim
+        for i in range(3):
+            cfg.rope_dims[i] = int(rope_dims[i])
+        cfg.rope_theta, cfg.rms_eps, cfg.softmax_scale = rope_theta, rms_eps, softmax_scale
+        cfg.cache_capacity_tokens, cfg.max_chunk_tokens = capacity, max_chunk
+        cfg.window_slack_tokens = window_slack
+        cfg.q_gain, cfg.k_gain = q_gain.data_ptr(), k_gain.data_ptr()
+        cfg.max_abs_gain = float(max(q_gain.abs().max().item(), k_gain.abs().max().item(), 1e-30))
+        cfg.nccl_comm = nccl_comm or None
+        cfg.world_size, cfg.rank, cfg.flags = world_size, rank, flags
+        nbytes = L.dz_cache_bytes(ctypes.byref(cfg))
+        if nbytes == 0:
+            raise DzError(-2, "invalid configuration")
+        self.storage = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        cfg.cache_storage, cfg.cache_bytes = self.storage.data_ptr(), nbytes
+        self._cfg = cfg
+        ctx = P()
+        s = L.dz_create(ctypes.byref(cfg), ctypes.byref(ctx))
+        if s:
+            raise DzError(s, "dz_create")
+        self._ctx = ctx
+
+    # -- helpers -----------------------------------------------------------
+    def _check(self, s: int, what: str):
+        if s:
+            raise DzError(s, f"{what}: {lib().dz_last_error(self._ctx).decode()}")
+
+    def _span(self, chunk_id: int, kind: int, n_local: int, pos: torch.Tensor) -> DzSpan:
+        _need(pos, "pos", torch.int32, (n_local, 3), self.device)
+        return DzSpan(chunk_id, kind, n_local * self.world_size, pos.data_ptr())
+
+    def _act(self, t: torch.Tensor, name: str, n_local: int):
+        _need(t, name, torch.bfloat16, (self.batch, n_local, self.heads, self.head_dim), self.device)
+
+    # -- the hot path --------------------------------------------------------
+    def append(self, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, chunk_id: int,
+               stream: Optional[torch.cuda.Stream] = None):
+        """Cache append of a clean chunk (Alg. 2 update=True): K' = RoPE(RMSNorm(k)), V = v."""
+        n_local = k.shape[1]
+        self._act(k, "k", n_local)
+        self._act(v, "v", n_local)
+        span = self._span(chunk_id, CLEAN, n_local, pos)
+        self._check(lib().dz_append_kv(self._ctx, k.data_ptr(), v.data_ptr(), ctypes.byref(span),
+                                       _stream_ptr(stream)), "dz_append_kv")
+
+    def attend(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, chunk_id: int,
+               kind: int = NOISY, out: Optional[torch.Tensor] = None,
+               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """One denoising step's self-attention of chunk ``chunk_id`` over the cache and itself."""
+        n_local = q.shape[1]
+        for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+            self._act(t, nm, n_local)
+        if out is None:
+            out = torch.empty_like(q)
+        else:
+            self._act(out, "out", n_local)
+        span = self._span(chunk_id, kind, n_local, pos)
+        self._check(lib().dz_attend_chunk(self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), ctypes.byref(span),
+                                          out.data_ptr(), _stream_ptr(stream)), "dz_attend_chunk")
+        return out
+
+    def commit_staged(self, chunk_id: int, stream: Optional[torch.cuda.Stream] = None):
+        self._check(lib().dz_commit_staged(self._ctx, chunk_id, _stream_ptr(stream)), "dz_commit_staged")
+
+    def evict_front(self, n_chunks: int, stream: Optional[torch.cuda.Stream] = None):
+        self._check(lib().dz_evict_front(self._ctx, n_chunks, _stream_ptr(stream)), "dz_evict_front")
+
+    # -- introspection ---------------------------------------------------------
+    def state(self) -> Tuple[int, int, int]:
+        v, n, last = I64(), I32(), I32()
+        self._check(lib().dz_cache_state(self._ctx, ctypes.byref(v), ctypes.byref(n), ctypes.byref(last)),
+                    "dz_cache_state")
+        return v.value, n.value, last.value
+
+    def cache_view(self, b: int = 0, tokens: Optional[int] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+        """(K' fp16, V bf16) views [tokens, heads_local, head_dim] of batch element b, committed slots first."""
+        k0, v0, stride = P(), P(), I64()
+        self._check(lib().dz_cache_view(self._ctx, b, ctypes.byref(k0), ctypes.byref(v0), ctypes.byref(stride)),
+                    "dz_cache_view")
+        if tokens is None:
+            tokens = self.state()[0]
+        base = self.storage.data_ptr()
+        nb = tokens * stride.value * 2
+
+        def view(ptr, dt):
+            off = ptr - base
+            return self.storage[off:off + nb].view(dt).view(tokens, self.heads_local, self.head_dim)
+        return view(k0.value, torch.float16), view(v0.value, torch.bfloat16)
+
+    def tile_map(self) -> np.ndarray:
+        nq, nk, bm, bn = I32(), I32(), I32(), I32()
+        self._check(lib().dz_get_tile_map(self._ctx, None, 0, ctypes.byref(nq), ctypes.byref(nk),
+                                          ctypes.byref(bm), ctypes.byref(bn)), "dz_get_tile_map")
+        buf = np.zeros((nq.value, nk.value), dtype=np.uint8)
+        self._check(lib().dz_get_tile_map(self._ctx, buf.ctypes.data, buf.size, ctypes.byref(nq),
+                                          ctypes.byref(nk), ctypes.byref(bm), ctypes.byref(bn)),
+                    "dz_get_tile_map")
+        return buf
+
+    def lse(self, n: int, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        out = torch.empty(self.batch, self.heads_local, n, dtype=torch.float32, device=self.device)
+        self._check(lib().dz_copy_lse(self._ctx, out.data_ptr(), out.numel(), _stream_ptr(stream)), "dz_copy_lse")
+        return out
+
+    def attention_units(self, n_tokens: int) -> int:
+        return int(lib().dz_attention_units(self._ctx, n_tokens))
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().dz_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,580 @@
+// dz.cpp -- the C ABI (include/dz.h): validation, cache bookkeeping, tensor
+// maps, Ulysses exchange plan and NCCL calls, kernel launches.
+//
+// Cache bookkeeping follows Alg. 2 of PAPER.md (l.558-607): committed clean
+// chunks occupy slots [start, start + valid) of a token-major buffer; the
+// chunk being denoised is staged right after them so that one contiguous KV
+// range [start, start + valid + n) is what the attention kernel reads.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/dz.h"
+#include "kernels.h"
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {  // byte offsets inside the caller's storage
+  int64_t slots = 0;
+  size_t k_off = 0, v_off = 0, q_off = 0, lse_off = 0, sq_off = 0, sk_off = 0, sv_off = 0, ol_off = 0,
+         or_off = 0, map_off = 0, total = 0;
+};
+
+bool basic_cfg_ok(const dz_config* c) {
+  if (!c) return false;
+  if (c->batch <= 0 || c->heads <= 0) return false;
+  if (c->head_dim != 64 && c->head_dim != 128) return false;
+  if (c->world_size <= 0 || c->rank < 0 || c->rank >= c->world_size) return false;
+  if (c->heads % c->world_size) return false;
+  if (c->max_chunk_tokens <= 0 || c->max_chunk_tokens % c->world_size) return false;
+  if (c->cache_capacity_tokens < 0 || c->window_slack_tokens < 0) return false;
+  int s = 0;
+  for (int a = 0; a < 3; ++a) {
+    if (c->rope_dims[a] < 0 || c->rope_dims[a] % 2) return false;
+    s += c->rope_dims[a];
+  }
+  return s == c->head_dim;
+}
+
+Layout make_layout(const dz_config* c) {
+  Layout L;
+  const int64_t B = c->batch, Hl = c->heads / c->world_size, D = c->head_dim, N = c->world_size;
+  const int64_t mc = c->max_chunk_tokens;
+  L.slots = c->cache_capacity_tokens + mc + c->window_slack_tokens;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align_up(bytes);
+    return o;
+  };
+  L.k_off = take((size_t)B * L.slots * Hl * D * 2);
+  L.v_off = take((size_t)B * L.slots * Hl * D * 2);
+  L.q_off = take((size_t)B * mc * Hl * D * 2);                       // Q' fp16
+  L.lse_off = take((c->flags & DZ_FLAG_WRITE_LSE) ? (size_t)B * Hl * mc * 4 : 0);
+  L.map_off = take(4096 + (size_t)((mc + 127) / 128) * ((c->cache_capacity_tokens + mc + 127) / 128));
+  if (N > 1) {
+    const size_t sb = (size_t)B * (mc / N) * c->heads * D * 2;       // [N][B][n_loc][Hl][D]
+    L.sq_off = take(sb);
+    L.sk_off = take(sb);
+    L.sv_off = take(sb);
+    L.ol_off = take((size_t)B * mc * Hl * D * 2);                    // O local [B][n][Hl][D]
+    L.or_off = take(sb);                                              // O recv [N][B][n_loc][Hl][D]
+  }
+  L.total = off;
+  return L;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 4D token-major tensor [B][tokens][H][D] (16-bit elements) as TMA dims (D, H, tokens, B),
+// box (64, 1, 128, 1), 128-byte swizzle, out-of-bounds elements read as zero.
+bool make_tmap(CUtensorMap* m, const void* base, bool bf16, int64_t D, int64_t H, int64_t tokens, int64_t B,
+               int64_t batch_stride_elems) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)tokens, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)(D * 2), (cuuint64_t)(H * D * 2), (cuuint64_t)(batch_stride_elems * 2)};
+  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+struct dz_ctx {
+  dz_config cfg{};
+  Layout L;
+  int B = 0, H = 0, Hl = 0, D = 0, N = 1, rank = 0;
+  float theta = 1e4f, eps = 1e-6f, scale = 0.f;
+  int num_sms = 148;
+  // committed state
+  int64_t start = 0, valid = 0;
+  std::deque<std::pair<int32_t, int64_t>> chunks;  // (id, tokens)
+  int32_t last_id = -1;
+  // staged chunk (written by the last attend)
+  bool staged = false;
+  int32_t staged_id = 0, staged_kind = 0;
+  int64_t staged_n = 0;
+  // last attend geometry (tile map / lse)
+  int32_t last_nq = 0, last_nkv_tiles = 0, last_nq_tiles = 0;
+  bool have_map = false;
+  // device pointers into the caller's storage
+  char* base = nullptr;
+  dz::PrologueArgs pro;  // RoPE frequencies, axes, gains
+  ncclComm_t comm = nullptr;
+  bool poisoned = false;
+  std::string err;
+
+  void* kslot(int b, int64_t slot) const {
+    return base + L.k_off + ((size_t)b * L.slots + slot) * Hl * D * 2;
+  }
+  void* vslot(int b, int64_t slot) const {
+    return base + L.v_off + ((size_t)b * L.slots + slot) * Hl * D * 2;
+  }
+};
+
+namespace {
+
+dz_status fail(dz_ctx* c, dz_status s, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+    if (s == DZ_ECUDA || s == DZ_ENCCL) c->poisoned = true;
+  }
+  return s;
+}
+
+dz_status cuda_check(dz_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return DZ_OK;
+  return fail(c, DZ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+dz_status nccl_check(dz_ctx* c, ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return DZ_OK;
+  return fail(c, DZ_ENCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Ulysses exchange plan: for tensor X of rank r, the block that
+// goes to peer p for batch element b, and where the block from peer p lands.
+struct Xfer {
+  const void* send;
+  void* recv;
+  size_t bytes;
+};
+
+// pre-attention: seq shard [n_loc, H] -> head shard [n, Hl]; which: 0 q, 1 k, 2 v
+Xfer pre_xfer(const dz_ctx* c, int which, int p, int b, int64_t n) {
+  const int64_t n_loc = n / c->N;
+  const size_t blk = (size_t)n_loc * c->Hl * c->D * 2;
+  const size_t so = (which == 0 ? c->L.sq_off : which == 1 ? c->L.sk_off : c->L.sv_off);
+  Xfer x;
+  x.send = c->base + so + ((size_t)p * c->B + b) * blk;
+  x.bytes = blk;
+  const int64_t slot = c->start + c->valid + (int64_t)p * n_loc;
+  if (which == 0)
+    x.recv = c->base + c->L.q_off + ((size_t)b * n + (size_t)p * n_loc) * c->Hl * c->D * 2;
+  else
+    x.recv = which == 1 ? c->kslot(b, slot) : c->vslot(b, slot);
+  return x;
+}
+
+// post-attention: O head shard [n, Hl] -> seq shard [n_loc, H] (receive side packed [N][B][n_loc][Hl][D])
+Xfer post_xfer(const dz_ctx* c, int p, int b, int64_t n) {
+  const int64_t n_loc = n / c->N;
+  const size_t blk = (size_t)n_loc * c->Hl * c->D * 2;
+  Xfer x;
+  x.send = c->base + c->L.ol_off + ((size_t)b * n + (size_t)p * n_loc) * c->Hl * c->D * 2;
+  x.recv = c->base + c->L.or_off + ((size_t)p * c->B + b) * blk;
+  x.bytes = blk;
+  return x;
+}
+
+dz_status check_ready(dz_ctx* c) {
+  if (!c) return DZ_EINVAL;
+  if (c->poisoned) return fail(c, DZ_ESTATE, "context poisoned by an earlier CUDA/NCCL error: %s", c->err.c_str());
+  return DZ_OK;
+}
+
+dz_status check_span(dz_ctx* c, const dz_span* s) {
+  if (!s || !s->pos_thw) return fail(c, DZ_EINVAL, "null span or positions");
+  if (s->kind != DZ_CLEAN && s->kind != DZ_NOISY) return fail(c, DZ_EINVAL, "bad span kind %d", s->kind);
+  if (s->n_tokens <= 0 || s->n_tokens % c->N) return fail(c, DZ_ESHAPE, "n_tokens %d not a positive multiple of world_size %d", s->n_tokens, c->N);
+  if (s->n_tokens > c->cfg.max_chunk_tokens)
+    return fail(c, DZ_ECAPACITY, "chunk of %d tokens exceeds max_chunk_tokens %d", s->n_tokens, c->cfg.max_chunk_tokens);
+  if (s->chunk_id <= c->last_id)
+    return fail(c, DZ_ESTATE, "chunk id %d must exceed the last committed id %d", s->chunk_id, c->last_id);
+  return DZ_OK;
+}
+
+// Keep [start, start + valid + max_chunk) inside the slot range: compact the
+// committed window down to slot 0 when it would run past the end.
+dz_status ensure_staging_room(dz_ctx* c, cudaStream_t st) {
+  if (c->start + c->valid + c->cfg.max_chunk_tokens <= c->L.slots) return DZ_OK;
+  const size_t row = (size_t)c->Hl * c->D * 2;
+  const int64_t s0 = c->start;
+  for (int b = 0; b < c->B; ++b) {
+    for (int kv = 0; kv < 2; ++kv) {
+      // forward copy in pieces of s0 slots: each piece's source lies above its destination
+      for (int64_t done = 0; done < c->valid; done += s0) {
+        const int64_t len = std::min<int64_t>(s0, c->valid - done);
+        void* dst = kv == 0 ? c->kslot(b, done) : c->vslot(b, done);
+        const void* src = kv == 0 ? c->kslot(b, s0 + done) : c->vslot(b, s0 + done);
+        dz_status r = cuda_check(c, cudaMemcpyAsync(dst, src, len * row, cudaMemcpyDeviceToDevice, st), "compact");
+        if (r) return r;
+      }
+    }
+  }
+  c->start = 0;
+  return DZ_OK;
+}
+
+void fill_prologue_common(dz_ctx* c, dz::PrologueArgs& a, const dz_span* s, int64_t n_loc) {
+  a = c->pro;
+  a.B = c->B;
+  a.n = (int32_t)n_loc;
+  a.H = c->H;
+  a.D = c->D;
+  a.x_bstride = n_loc * c->H * c->D;
+  a.pos = s->pos_thw;
+}
+
+// K1 prologue for the current chunk: Q' and the chunk's K'/V, written either
+// straight into the staging slot (N == 1) or into the all-to-all send layout.
+dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, const dz_span* s, cudaStream_t st) {
+  const int64_t n = s->n_tokens, n_loc = n / c->N;
+  dz::PrologueArgs a;
+  fill_prologue_common(c, a, s, n_loc);
+  a.x[0] = q;
+  a.x[1] = k;
+  a.x[2] = v;
+  if (c->N == 1) {
+    a.heads_per_dest = c->H;
+    a.y[0] = {c->base + c->L.q_off, n * c->H * c->D, (int64_t)c->H * c->D, 0};
+    const int64_t slot = c->start + c->valid;
+    a.y[1] = {c->kslot(0, slot), c->L.slots * c->H * c->D, (int64_t)c->H * c->D, 0};
+    a.y[2] = {c->vslot(0, slot), c->L.slots * c->H * c->D, (int64_t)c->H * c->D, 0};
+  } else {
+    a.heads_per_dest = c->Hl;
+    const int64_t tst = (int64_t)c->Hl * c->D, bst = n_loc * tst, dst = (int64_t)c->B * bst;
+    a.y[0] = {c->base + c->L.sq_off, bst, tst, dst};
+    a.y[1] = {c->base + c->L.sk_off, bst, tst, dst};
+    a.y[2] = {c->base + c->L.sv_off, bst, tst, dst};
+  }
+  return cuda_check(c, dz::launch_prologue(a, st), "prologue launch");
+}
+
+dz_status exchange_pre(dz_ctx* c, bool with_q, int64_t n, cudaStream_t st) {
+  dz_status r = nccl_check(c, ncclGroupStart(), "ncclGroupStart");
+  if (r) return r;
+  for (int which = with_q ? 0 : 1; which < 3; ++which)
+    for (int p = 0; p < c->N; ++p)
+      for (int b = 0; b < c->B; ++b) {
+        // what this rank sends to p, and what it receives from p
+        const Xfer x = pre_xfer(c, which, p, b, n);
+        r = nccl_check(c, ncclSend(x.send, x.bytes, ncclUint8, p, c->comm, st), "ncclSend");
+        if (!r) r = nccl_check(c, ncclRecv(x.recv, x.bytes, ncclUint8, p, c->comm, st), "ncclRecv");
+        if (r) {
+          ncclGroupEnd();
+          return r;
+        }
+      }
+  return nccl_check(c, ncclGroupEnd(), "ncclGroupEnd");
+}
+
+dz_status exchange_post(dz_ctx* c, int64_t n, cudaStream_t st) {
+  dz_status r = nccl_check(c, ncclGroupStart(), "ncclGroupStart");
+  if (r) return r;
+  for (int p = 0; p < c->N; ++p)
+    for (int b = 0; b < c->B; ++b) {
+      const Xfer x = post_xfer(c, p, b, n);
+      r = nccl_check(c, ncclSend(x.send, x.bytes, ncclUint8, p, c->comm, st), "ncclSend");
+      if (!r) r = nccl_check(c, ncclRecv(x.recv, x.bytes, ncclUint8, p, c->comm, st), "ncclRecv");
+      if (r) {
+        ncclGroupEnd();
+        return r;
+      }
+    }
+  return nccl_check(c, ncclGroupEnd(), "ncclGroupEnd");
+}
+
+// K2 over local heads and the full sequence: committed slots + the staged chunk.
+dz_status run_attention(dz_ctx* c, int64_t n, void* out_local, int64_t o_bstride, int64_t o_tstride,
+                        cudaStream_t st) {
+  dz::AttnArgs a;
+  const int64_t kv_len = c->valid + n;
+  const int64_t bs = c->L.slots * c->Hl * c->D;
+  if (!make_tmap(&a.tm_q, c->base + c->L.q_off, false, c->D, c->Hl, n, c->B, n * c->Hl * c->D) ||
+      !make_tmap(&a.tm_k, c->kslot(0, c->start), false, c->D, c->Hl, kv_len, c->B, bs) ||
+      !make_tmap(&a.tm_v, c->vslot(0, c->start), true, c->D, c->Hl, kv_len, c->B, bs))
+    return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled failed");
+  a.out = out_local;
+  a.o_bstride = o_bstride;
+  a.o_tstride = o_tstride;
+  a.lse = (c->cfg.flags & DZ_FLAG_WRITE_LSE) ? reinterpret_cast<float*>(c->base + c->L.lse_off) : nullptr;
+  a.B = c->B;
+  a.H = c->Hl;
+  a.D = c->D;
+  a.nq = (int32_t)n;
+  a.kv_len = (int32_t)kv_len;
+  a.scale_log2 = c->scale * 1.4426950408889634f;
+  const int units = dz::attention_units(c->B, c->Hl, (int32_t)n);
+  a.grid = std::min(units, c->num_sms);
+  const int nqt = (int)((n + 127) / 128), nkt = (int)((kv_len + 127) / 128);
+  const size_t map_cap = 4096 + (size_t)((c->cfg.max_chunk_tokens + 127) / 128) *
+                                    ((c->cfg.cache_capacity_tokens + c->cfg.max_chunk_tokens + 127) / 128);
+  if ((size_t)nqt * nkt <= map_cap) {
+    a.tile_map = reinterpret_cast<uint8_t*>(c->base + c->L.map_off);
+    c->last_nq_tiles = nqt;
+    c->last_nkv_tiles = nkt;
+    c->have_map = true;
+  }
+  c->last_nq = (int32_t)n;
+  return cuda_check(c, dz::launch_attention(a, st), "attention launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dz_cache_bytes(const dz_config* cfg) {
+  if (!basic_cfg_ok(cfg)) return 0;
+  return make_layout(cfg).total;
+}
+
+dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
+  if (!out) return DZ_EINVAL;
+  *out = nullptr;
+  if (!cfg) return DZ_EINVAL;
+  if (cfg->head_dim != 64 && cfg->head_dim != 128) return DZ_ESHAPE;
+  if (!basic_cfg_ok(cfg)) return DZ_ESHAPE;
+  if (!cfg->q_gain || !cfg->k_gain || !cfg->cache_storage) return DZ_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(cfg->cache_storage) & (kAlign - 1)) || !aligned16(cfg->q_gain) ||
+      !aligned16(cfg->k_gain))
+    return DZ_EINVAL;
+  // fp16 Q'/K' (reading A13): |x'_i| <= sqrt(D) * |g_i| after RMSNorm
+  if (!(cfg->max_abs_gain > 0.f) || std::sqrt((double)cfg->head_dim) * cfg->max_abs_gain >= 6.0e4) return DZ_ERANGE;
+  if (cfg->world_size > 1 && !cfg->nccl_comm) return DZ_EINVAL;
+  Layout L = make_layout(cfg);
+  if (cfg->cache_bytes < L.total) return DZ_ECAPACITY;
+
+  dz_ctx* c = new (std::nothrow) dz_ctx();
+  if (!c) return DZ_ECUDA;
+  c->cfg = *cfg;
+  c->L = L;
+  c->B = cfg->batch;
+  c->H = cfg->heads;
+  c->N = cfg->world_size;
+  c->rank = cfg->rank;
+  c->Hl = cfg->heads / cfg->world_size;
+  c->D = cfg->head_dim;
+  c->theta = cfg->rope_theta > 0.f ? cfg->rope_theta : 1e4f;
+  c->eps = cfg->rms_eps > 0.f ? cfg->rms_eps : 1e-6f;
+  c->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : 1.0f / std::sqrt((float)cfg->head_dim);
+  c->base = static_cast<char*>(cfg->cache_storage);
+  c->comm = static_cast<ncclComm_t>(cfg->nccl_comm);
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  // RoPE frequencies per pair j (fp64): axis slice [t | h | w], omega = theta^(-2i/d_a)
+  int j = 0;
+  for (int ax = 0; ax < 3; ++ax)
+    for (int i = 0; i < cfg->rope_dims[ax] / 2; ++i, ++j) {
+      c->pro.omega[j] = std::pow((double)c->theta, -2.0 * i / cfg->rope_dims[ax]);
+      c->pro.axis[j] = (int8_t)ax;
+    }
+  c->pro.gain[0] = cfg->q_gain;
+  c->pro.gain[1] = cfg->k_gain;
+  c->pro.eps = c->eps;
+  *out = c;
+  return DZ_OK;
+}
+
+dz_status dz_append_kv(dz_ctx* c, const void* k_raw, const void* v_raw, const dz_span* s, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if (!k_raw || !v_raw || !aligned16(k_raw) || !aligned16(v_raw)) return fail(c, DZ_EINVAL, "null/misaligned k or v");
+  if ((r = check_span(c, s))) return r;
+  if (s->kind != DZ_CLEAN) return fail(c, DZ_ESTATE, "only clean chunks enter the cache (Alg. 2 l.603)");
+  if (c->valid + s->n_tokens > c->cfg.cache_capacity_tokens)
+    return fail(c, DZ_ECAPACITY, "cache full: %lld + %d > %lld", (long long)c->valid, s->n_tokens,
+                (long long)c->cfg.cache_capacity_tokens);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((r = run_prologue(c, nullptr, k_raw, v_raw, s, st))) return r;
+  if (c->N > 1 && (r = exchange_pre(c, false, s->n_tokens, st))) return r;
+  c->valid += s->n_tokens;
+  c->chunks.emplace_back(s->chunk_id, (int64_t)s->n_tokens);
+  c->last_id = s->chunk_id;
+  c->staged = false;
+  return ensure_staging_room(c, st);
+}
+
+dz_status dz_attend_chunk(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const dz_span* s,
+                          void* out, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if (!q_raw || !k_raw || !v_raw || !out) return fail(c, DZ_EINVAL, "null q/k/v/out");
+  if (!aligned16(q_raw) || !aligned16(k_raw) || !aligned16(v_raw) || !aligned16(out))
+    return fail(c, DZ_EINVAL, "q/k/v/out must be 16-byte aligned");
+  if ((r = check_span(c, s))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = s->n_tokens;
+  c->staged = false;
+  if ((r = run_prologue(c, q_raw, k_raw, v_raw, s, st))) return r;
+  if (c->N == 1) {
+    if ((r = run_attention(c, n, out, n * c->H * c->D, (int64_t)c->H * c->D, st))) return r;
+  } else {
+    if ((r = exchange_pre(c, true, n, st))) return r;
+    if ((r = run_attention(c, n, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, st))) return r;
+    if ((r = exchange_post(c, n, st))) return r;
+    if ((r = cuda_check(c, dz::launch_sp_unpack(c->base + c->L.or_off, out, c->N, c->B, (int32_t)(n / c->N), c->Hl,
+                                                c->D, st),
+                        "unpack launch")))
+      return r;
+  }
+  c->staged = true;
+  c->staged_id = s->chunk_id;
+  c->staged_kind = s->kind;
+  c->staged_n = n;
+  return DZ_OK;
+}
+
+dz_status dz_commit_staged(dz_ctx* c, int32_t chunk_id, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if (!c->staged || c->staged_id != chunk_id || c->staged_kind != DZ_CLEAN)
+    return fail(c, DZ_ESTATE, "no clean chunk %d staged by the last attend", chunk_id);
+  if (c->valid + c->staged_n > c->cfg.cache_capacity_tokens)
+    return fail(c, DZ_ECAPACITY, "cache full");
+  c->valid += c->staged_n;
+  c->chunks.emplace_back(chunk_id, c->staged_n);
+  c->last_id = chunk_id;
+  c->staged = false;
+  return ensure_staging_room(c, static_cast<cudaStream_t>(stream));
+}
+
+dz_status dz_evict_front(dz_ctx* c, int32_t n_chunks, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if (n_chunks < 0 || (size_t)n_chunks > c->chunks.size())
+    return fail(c, DZ_EINVAL, "cannot evict %d of %zu chunks", n_chunks, c->chunks.size());
+  for (int i = 0; i < n_chunks; ++i) {
+    c->start += c->chunks.front().second;
+    c->valid -= c->chunks.front().second;
+    c->chunks.pop_front();
+  }
+  if (c->valid == 0) c->start = 0;
+  c->staged = false;
+  return ensure_staging_room(c, static_cast<cudaStream_t>(stream));
+}
+
+dz_status dz_cache_state(const dz_ctx* c, int64_t* valid, int32_t* n_chunks, int32_t* last_id) {
+  if (!c) return DZ_EINVAL;
+  if (valid) *valid = c->valid;
+  if (n_chunks) *n_chunks = (int32_t)c->chunks.size();
+  if (last_id) *last_id = c->last_id;
+  return DZ_OK;
+}
+
+dz_status dz_cache_view(const dz_ctx* c, int32_t b, void** k0, void** v0, int64_t* stride) {
+  if (!c || b < 0 || b >= c->B) return DZ_EINVAL;
+  if (k0) *k0 = c->kslot(b, c->start);
+  if (v0) *v0 = c->vslot(b, c->start);
+  if (stride) *stride = (int64_t)c->Hl * c->D;
+  return DZ_OK;
+}
+
+dz_status dz_copy_lse(dz_ctx* c, float* dst, size_t elems, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if (!(c->cfg.flags & DZ_FLAG_WRITE_LSE)) return fail(c, DZ_ESTATE, "created without DZ_FLAG_WRITE_LSE");
+  const size_t need = (size_t)c->B * c->Hl * c->last_nq;
+  if (!dst || elems < need) return fail(c, DZ_EINVAL, "lse buffer too small (%zu < %zu)", elems, need);
+  return cuda_check(c, cudaMemcpyAsync(dst, c->base + c->L.lse_off, need * 4, cudaMemcpyDeviceToDevice,
+                                       static_cast<cudaStream_t>(stream)),
+                    "lse copy");
+}
+
+dz_status dz_get_tile_map(const dz_ctx* c, uint8_t* host, size_t cap, int32_t* nq, int32_t* nk, int32_t* bm,
+                          int32_t* bn) {
+  if (!c) return DZ_EINVAL;
+  if (!c->have_map) return DZ_ESTATE;
+  const size_t need = (size_t)c->last_nq_tiles * c->last_nkv_tiles;
+  if (nq) *nq = c->last_nq_tiles;
+  if (nk) *nk = c->last_nkv_tiles;
+  if (bm) *bm = 128;
+  if (bn) *bn = 128;
+  if (!host) return DZ_OK;
+  if (cap < need) return DZ_EINVAL;
+  // synchronous device read of the kernel-written debug map (tests only)
+  if (cudaMemcpy(host, c->base + c->L.map_off, need, cudaMemcpyDeviceToHost) != cudaSuccess) return DZ_ECUDA;
+  return DZ_OK;
+}
+
+dz_status dz_destroy(dz_ctx* c) {
+  delete c;
+  return DZ_OK;
+}
+
+const char* dz_status_string(dz_status s) {
+  switch (s) {
+    case DZ_OK: return "DZ_OK";
+    case DZ_EINVAL: return "DZ_EINVAL: invalid argument";
+    case DZ_ESHAPE: return "DZ_ESHAPE: unsupported shape";
+    case DZ_ECAPACITY: return "DZ_ECAPACITY: capacity exceeded";
+    case DZ_ESTATE: return "DZ_ESTATE: invalid cache state or ordering";
+    case DZ_ECUDA: return "DZ_ECUDA: CUDA error";
+    case DZ_ENCCL: return "DZ_ENCCL: NCCL error";
+    case DZ_ERANGE: return "DZ_ERANGE: gains overflow fp16";
+  }
+  return "unknown dz_status";
+}
+
+const char* dz_last_error(const dz_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+dz_status dz_nccl_unique_id(void* id128) {
+  if (!id128) return DZ_EINVAL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  return ncclGetUniqueId(static_cast<ncclUniqueId*>(id128)) == ncclSuccess ? DZ_OK : DZ_ENCCL;
+}
+
+dz_status dz_nccl_comm_init(int32_t world_size, const void* id128, int32_t rank, void** comm) {
+  if (!id128 || !comm || world_size <= 0 || rank < 0 || rank >= world_size) return DZ_EINVAL;
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t c = nullptr;
+  if (ncclCommInitRank(&c, world_size, id, rank) != ncclSuccess) return DZ_ENCCL;
+  *comm = c;
+  return DZ_OK;
+}
+
+dz_status dz_nccl_comm_destroy(void* comm) {
+  if (!comm) return DZ_OK;
+  return ncclCommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? DZ_OK : DZ_ENCCL;
+}
+
+dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset) {
+  if (!host8) return DZ_EINVAL;
+  if (dz::read_watchdog(host8) != cudaSuccess) return DZ_ECUDA;
+  if (reset && dz::reset_watchdog() != cudaSuccess) return DZ_ECUDA;
+  return DZ_OK;
+}
+
+int32_t dz_attention_units(const dz_ctx* c, int32_t n) {
+  if (!c || n <= 0) return 0;
+  return dz::attention_units(c->B, c->Hl, n);
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// kernels.h -- internal launcher interface between the C-ABI layer (dz.cpp)
+// and the sm_100a kernels (*.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace dz {
+
+constexpr int kMaxHeadDim = 128;
+
+// ---- K1 / K4: fused per-head RMSNorm + 3D RoPE (+ V copy) -----------------
+// One output tensor slot.  Address of output row (b, t, h):
+//   base + b*bstride + (h / heads_per_dest)*dstride + t*tstride + (h % heads_per_dest)*D
+struct OutSlot {
+  void* base = nullptr;
+  int64_t bstride = 0, tstride = 0, dstride = 0;
+};
+
+struct PrologueArgs {
+  const void* x[3] = {nullptr, nullptr, nullptr};  // raw bf16 q, k, v: [B][n][H][D]
+  int64_t x_bstride = 0;                           // elements between batch elements
+  const int32_t* pos = nullptr;                    // [n][3] (t, h, w)
+  const float* gain[2] = {nullptr, nullptr};       // q, k gains [H*D]
+  OutSlot y[3];                                    // q' fp16, k' fp16, v bf16
+  int32_t B = 0, n = 0, H = 0, D = 0, heads_per_dest = 0;
+  float eps = 1e-6f;
+  double omega[kMaxHeadDim / 2];                   // per pair j: theta^(-2i/d_a), fp64 (host)
+  int8_t axis[kMaxHeadDim / 2];                    // per pair j: 0 t, 1 h, 2 w
+};
+cudaError_t launch_prologue(const PrologueArgs& a, cudaStream_t s);
+
+// ---- K2: block-causal flash attention (tcgen05 + TMEM + TMA) --------------
+struct AttnArgs {
+  CUtensorMap tm_q;   // Q' fp16, dims (D, H, nq, B), box (64, 1, 128, 1), SW128
+  CUtensorMap tm_k;   // K' fp16 cache, dims (D, H, kv_len, B)
+  CUtensorMap tm_v;   // V  bf16 cache, dims (D, H, kv_len, B)
+  void* out = nullptr;            // bf16, row (b, s, h) at out + b*o_bstride + s*o_tstride + h*D
+  int64_t o_bstride = 0, o_tstride = 0;
+  float* lse = nullptr;           // optional fp32 [B][H][nq] natural-log LSE
+  uint8_t* tile_map = nullptr;    // optional debug [n_q_tiles][n_kv_tiles] for (b, h) = (0, 0)
+  int32_t B = 0, H = 0, D = 0, nq = 0, kv_len = 0;
+  float scale_log2 = 0.f;         // softmax_scale * log2(e)
+  int32_t grid = 0;               // persistent CTAs (<= #SMs)
+};
+cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);
+int attention_units(int32_t B, int32_t H, int32_t nq);
+cudaError_t read_watchdog(uint32_t* host8);   // {fired, block, warp, bar addr, parity, smid, bars base, 0}
+cudaError_t reset_watchdog();  // work units (b, h, q-tile pair)
+
+// ---- K5: Ulysses receive unpack [N][B][n_loc][Hl][D] -> [B][n_loc][H][D] ---
+cudaError_t launch_sp_unpack(const void* recv, void* out, int32_t N, int32_t B, int32_t n_loc, int32_t Hl,
+                             int32_t D, cudaStream_t s);
+
+}  // namespace dz

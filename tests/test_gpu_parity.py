@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Tolerances from BASELINE.json north_star: max |err| <=
+2e-2 and relative Frobenius <= 5e-3 on bf16 inputs; bit-exact for integer /
+mask / tile decisions and for V (a copy)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from helpers import GpuRun, assert_parity, errors
+
+pytestmark = pytest.mark.gpu
+
+
+def _small(name="C1", **kw):
+    return synth.scaled(synth.workload(name), **kw)
+
+
+# ---------------------------------------------------------------- append --
+@pytest.mark.parametrize("wname", ["C0", "C1"])
+def test_append_parity(wname):
+    w = synth.workload(wname)
+    run = GpuRun(w)
+    run.fill()
+    torch.cuda.synchronize()
+    valid, nch, last = run.cache.state()
+    assert (valid, nch, last) == (w.cache_tokens, w.cached_chunks, w.cached_chunks - 1)
+    kc, vc = run.cache.cache_view(0)
+    s = run.streams[0]
+    want_k = np.concatenate([oracle.prologue(k, run.gk, p, w.rope_dims) for k, p in zip(s.cache_k, s.cache_pos)])
+    want_v = torch.cat(s.cache_v)
+    assert torch.equal(vc.cpu(), want_v), "V must be copied bit-exactly"
+    got = kc.cpu().double().numpy()
+    # K' within 1 ulp of fp16 of the oracle's exact value, plus the fp32
+    # rounding of the rotation u*c - w*s (cancellation: relative to the pair norm)
+    ulp = np.spacing(np.abs(want_k).astype(np.float16)).astype(np.float64)
+    pair = np.repeat(np.hypot(want_k[..., 0::2], want_k[..., 1::2]), 2, axis=-1)
+    bound = ulp + 2.0 ** -20 * pair
+    assert np.all(np.abs(got - want_k) <= bound), float((np.abs(got - want_k) / bound).max())
+    assert np.mean(np.abs(got - want_k) <= 0.5 * ulp + 2.0 ** -20 * pair) > 0.99
+
+
+# ---------------------------------------------------------------- attend --
+def test_attend_parity_c0():
+    w = synth.workload("C0")
+    run = GpuRun(w)
+    run.fill()
+    out = run.attend().cpu().double().numpy()[0]
+    assert_parity(out, run.oracle_out(), "C0")
+
+
+def test_attend_parity_c1_all_heads():
+    w = synth.workload("C1")
+    run = GpuRun(w)
+    run.fill()
+    out = run.attend().cpu().double().numpy()[0]
+    m, r = assert_parity(out, run.oracle_out(), "C1")
+    print(f"C1 max|err|={m:.3e} rel_fro={r:.3e}")
+
+
+@pytest.mark.parametrize("D,rd", [(128, (44, 42, 42)), (64, (16, 24, 24))])
+@pytest.mark.parametrize("n,cached", [(1, 0), (64, 0), (130, 1), (200, 2), (256, 3), (383, 2), (1344, 1)])
+def test_attend_parity_ragged(D, rd, n, cached):
+    # chunk sizes spanning several tiles with ragged tails; cache of `cached` chunks
+    w = synth.Workload(f"R{n}", 7, batch=1, heads=3, head_dim=D, rope_dims=rd, frames=1, grid_h=1, grid_w=n,
+                       views=1, actions=0, cached_chunks=cached)
+    run = GpuRun(w)
+    run.fill()
+    out = run.attend().cpu().double().numpy()[0]
+    assert_parity(out, run.oracle_out(), f"D{D} n{n} c{cached}")
+
+
+def test_empty_cache_first_chunk():
+    w = _small(cached_chunks=0)
+    run = GpuRun(w, capacity=w.chunk_tokens)
+    out = run.attend().cpu().double().numpy()[0]
+    assert_parity(out, run.oracle_out(heads=(0, 40)), "empty cache")
+
+
+def test_determinism_and_cache_unchanged():
+    w = synth.workload("C1")
+    run = GpuRun(w)
+    run.fill()
+    k0, v0 = [t.clone() for t in run.cache.cache_view(0)]
+    a = run.attend()
+    b = run.attend()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b), "same call twice must be bitwise identical"
+    k1, v1 = run.cache.cache_view(0)
+    assert torch.equal(k0, k1) and torch.equal(v0, v1), "attend must not modify committed chunks"
+
+
+def test_tile_map_matches_oracle_classifier():
+    w = synth.workload("C1")
+    run = GpuRun(w)
+    run.fill()
+    run.attend()
+    torch.cuda.synchronize()
+    got = run.cache.tile_map()
+    C, n = w.cached_chunks, w.chunk_tokens
+    kt = oracle.chunk_tags(list(range(C)) + [C], [oracle.CLEAN] * C + [oracle.NOISY], [n] * (C + 1))
+    qt = (np.full(n, C, np.int32), np.full(n, oracle.NOISY, np.int32), np.full(n, C, np.int32))
+    want = oracle.tile_map(qt, kt, 128, 128)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want), oracle.tile_map_str(got) + " vs " + oracle.tile_map_str(want)
+
+
+def test_masked_beyond_valid_is_bitwise_invariant():
+    # slots past the visible range hold garbage (finite or NaN): the output must not change
+    w = _small(heads=4, cached_chunks=2)
+    run = GpuRun(w, slack=4 * w.chunk_tokens)
+    run.fill()
+    ref = run.attend().clone()
+    n_total = (w.cached_chunks + 1) * w.chunk_tokens
+    for fill in (float("nan"), 1e4, -3.0):
+        k, v = run.cache.cache_view(0, tokens=n_total + 3 * w.chunk_tokens)
+        k[n_total:] = fill
+        v[n_total:] = fill
+        out = run.attend()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), f"fill={fill}"
+
+
+def test_cfg_batch_steps_c3():
+    # C3: batch 2 (cond/uncond caches drawn independently), 4 denoise steps over one cache
+    w = synth.workload("C3")
+    run = GpuRun(w)
+    run.fill()
+    k0 = [t.clone() for t in run.cache.cache_view(0)] + [t.clone() for t in run.cache.cache_view(1)]
+    outs = []
+    for st in range(w.steps):
+        outs.append(run.attend(step=st).clone())
+    torch.cuda.synchronize()
+    k1 = list(run.cache.cache_view(0)) + list(run.cache.cache_view(1))
+    assert all(torch.equal(a, b) for a, b in zip(k0, k1)), "committed cache changed across denoise steps"
+    assert torch.equal(run.attend(step=0), outs[0]), "replaying step 0 must reproduce it bitwise"
+    for b in (0, 1):
+        for st in (0, 3):
+            for h in (0, 39):
+                got = outs[st][b, :, h:h + 1].cpu().double().numpy()
+                assert_parity(got, run.oracle_out(b=b, step=st, heads=(h, h + 1)), f"C3 b{b} step{st} h{h}")
+
+
+def test_long_cache_outliers_c2():
+    w = synth.workload("C2")
+    run = GpuRun(w)
+    run.fill()
+    out = run.attend().cpu().double().numpy()[0]
+    for h in (0, 39):
+        assert_parity(out[:, h:h + 1], run.oracle_out(heads=(h, h + 1)), f"C2 head {h}")
+
+
+def test_sp_shape_c4_single_gpu_sampled_rows():
+    # full C4 size on one GPU (32 cached chunks of 2688 tokens); oracle on heads {0, 39}, sampled queries
+    w = synth.workload("C4")
+    run = GpuRun(w)
+    run.fill()
+    out = run.attend().cpu().double().numpy()[0]
+    rows = np.arange(0, w.chunk_tokens, 37)
+    rows = np.unique(np.concatenate([rows, [w.chunk_tokens - 1, 2639, 2640]]))
+    for h in (0, 39):
+        want = run.oracle_out(heads=(h, h + 1), rows=rows)
+        assert_parity(out[rows, h:h + 1], want, f"C4 head {h}")
+
+
+def test_gt_injection_attend_then_commit():
+    # Alg. 2 l.601-602 as a model runs it: attend the clean chunk, then commit its staged K'/V
+    w = _small(heads=4, cached_chunks=2)
+    run = GpuRun(w, capacity=3 * w.chunk_tokens)
+    run.fill()
+    C = w.cached_chunks
+    s = run.streams[0]
+    pos = s.cur_pos.to(run.dev)
+    q, k, v = (run.stack(x, 0) for x in ("cur_q", "cur_k", "cur_v"))
+    run.cache.attend(q, k, v, pos, C, kind=0)
+    run.cache.commit_staged(C)
+    torch.cuda.synchronize()
+    assert run.cache.state() == (3 * w.chunk_tokens, 3, C)
+    kc, vc = run.cache.cache_view(0)
+    want_k = oracle.prologue(s.cur_k[0], run.gk, s.cur_pos, w.rope_dims)
+    got = kc[C * w.chunk_tokens:].cpu().double().numpy()
+    assert errors(got, want_k)[0] < 1e-2
+    assert torch.equal(vc[C * w.chunk_tokens:].cpu(), s.cur_v[0])
+
+
+def test_sliding_window_evict_equals_fresh_cache():
+    # evicting the oldest chunk (P:510 context budget) == a cache built without it
+    w = _small(heads=4, cached_chunks=3)
+    run = GpuRun(w, slack=w.chunk_tokens)
+    run.fill()
+    run.cache.evict_front(1)
+    a = run.attend(chunk_id=w.cached_chunks).cpu()
+    fresh = GpuRun(w)
+    for c in range(1, w.cached_chunks):
+        fresh.cache.append(fresh.stack("cache_k", c), fresh.stack("cache_v", c),
+                           fresh.streams[0].cache_pos[c].to(fresh.dev), c)
+    b = fresh.attend().cpu()
+    assert torch.equal(a, b)
