@@ -73,7 +73,8 @@ enum { DZ_CLEAN = 0, DZ_NOISY = 1 }; /* dz_span.kind (Fig. 10: C chunks vs Z/Y c
 
 enum {
   DZ_FLAG_NONE = 0,
-  DZ_FLAG_WRITE_LSE = 1 /* keep a per-row log-sum-exp of the last attend (dz_copy_lse) */
+  DZ_FLAG_WRITE_LSE = 1, /* keep a per-row log-sum-exp of the last attend (dz_copy_lse) */
+  DZ_FLAG_PROFILE = 2    /* record CUDA events around every kernel/exchange (dz_profile_last) */
 };
 
 typedef struct {
@@ -162,6 +163,13 @@ DZ_API dz_status dz_copy_lse(dz_ctx* ctx, float* dst, size_t dst_elems, void* st
  * PARTIAL, 2 FULL (same encoding as the oracle's classifier). */
 DZ_API dz_status dz_get_tile_map(const dz_ctx* ctx, uint8_t* host, size_t cap, int32_t* n_q_tiles, int32_t* n_kv_tiles,
                           int32_t* bm, int32_t* bn);
+
+/* Device times in ms of the last calls (needs DZ_FLAG_PROFILE), measured with
+ * CUDA events on the caller's stream: ms[0] attend prologue (K1), ms[1]
+ * pre-attention all-to-all, ms[2] attention (K2), ms[3] post all-to-all +
+ * unpack, ms[4] attend total, ms[5] last append (K4 + exchange).  Waits for the
+ * recorded events (host sync).  Entries not yet recorded are 0. */
+DZ_API dz_status dz_profile_last(dz_ctx* ctx, float* ms6);
 
 /* Releases the context's host state and device workspace (not the caller's
  * buffers).  Safe on NULL. */

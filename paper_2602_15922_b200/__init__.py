@@ -31,6 +31,7 @@ LIB_PATH = os.path.join(_HERE, "libdz.so")
 
 CLEAN, NOISY = 0, 1
 FLAG_WRITE_LSE = 1
+FLAG_PROFILE = 2
 
 STATUS = {0: "DZ_OK", -1: "DZ_EINVAL", -2: "DZ_ESHAPE", -3: "DZ_ECAPACITY", -4: "DZ_ESTATE",
           -5: "DZ_ECUDA", -6: "DZ_ENCCL", -7: "DZ_ERANGE"}
@@ -83,6 +84,7 @@ SIGNATURES = [
     ("dz_nccl_comm_destroy", I32, [P]),
     ("dz_attention_units", I32, [P, I32]),
     ("dz_debug_watchdog", I32, [P, I32]),
+    ("dz_profile_last", I32, [P, P]),
 ]
 
 _lib = None
@@ -285,6 +287,13 @@ class ChunkKVCache:
         out = torch.empty(self.batch, self.heads_local, n, dtype=torch.float32, device=self.device)
         self._check(lib().dz_copy_lse(self._ctx, out.data_ptr(), out.numel(), _stream_ptr(stream)), "dz_copy_lse")
         return out
+
+    def profile_last(self) -> dict:
+        """Device ms of the last attend/append phases (needs FLAG_PROFILE); host-syncs."""
+        buf = (ctypes.c_float * 6)()
+        self._check(lib().dz_profile_last(self._ctx, ctypes.cast(buf, P)), "dz_profile_last")
+        keys = ("prologue", "exchange_pre", "attention", "exchange_post", "attend_total", "append")
+        return dict(zip(keys, list(buf)))
 
     def attention_units(self, n_tokens: int) -> int:
         return int(lib().dz_attention_units(self._ctx, n_tokens))

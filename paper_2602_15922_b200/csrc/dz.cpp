@@ -131,6 +131,9 @@ struct dz_ctx {
   dz::PrologueArgs pro;  // RoPE frequencies, axes, gains
   ncclComm_t comm = nullptr;
   bool poisoned = false;
+  // DZ_FLAG_PROFILE: events e[0..4] around the attend phases, a[0..1] around the append
+  cudaEvent_t ev[5] = {}, ev_app[2] = {};
+  bool have_attend_ev = false, have_append_ev = false;
   std::string err;
 
   void* kslot(int b, int64_t slot) const {
@@ -398,6 +401,12 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   c->pro.gain[0] = cfg->q_gain;
   c->pro.gain[1] = cfg->k_gain;
   c->pro.eps = c->eps;
+  if (cfg->flags & DZ_FLAG_PROFILE) {
+    for (auto& e : c->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) e = nullptr;
+    for (auto& e : c->ev_app)
+      if (cudaEventCreate(&e) != cudaSuccess) e = nullptr;
+  }
   *out = c;
   return DZ_OK;
 }
@@ -412,8 +421,12 @@ dz_status dz_append_kv(dz_ctx* c, const void* k_raw, const void* v_raw, const dz
     return fail(c, DZ_ECAPACITY, "cache full: %lld + %d > %lld", (long long)c->valid, s->n_tokens,
                 (long long)c->cfg.cache_capacity_tokens);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool prof = c->ev_app[0] != nullptr;
+  if (prof) cudaEventRecord(c->ev_app[0], st);
   if ((r = run_prologue(c, nullptr, k_raw, v_raw, s, st))) return r;
   if (c->N > 1 && (r = exchange_pre(c, false, s->n_tokens, st))) return r;
+  if (prof) cudaEventRecord(c->ev_app[1], st);
+  c->have_append_ev = prof;
   c->valid += s->n_tokens;
   c->chunks.emplace_back(s->chunk_id, (int64_t)s->n_tokens);
   c->last_id = s->chunk_id;
@@ -432,18 +445,28 @@ dz_status dz_attend_chunk(dz_ctx* c, const void* q_raw, const void* k_raw, const
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t n = s->n_tokens;
   c->staged = false;
+  const bool prof = c->ev[0] != nullptr;
+  auto mark = [&](int i) { if (prof) cudaEventRecord(c->ev[i], st); };
+  mark(0);
   if ((r = run_prologue(c, q_raw, k_raw, v_raw, s, st))) return r;
+  mark(1);
   if (c->N == 1) {
+    mark(2);
     if ((r = run_attention(c, n, out, n * c->H * c->D, (int64_t)c->H * c->D, st))) return r;
+    mark(3);
   } else {
     if ((r = exchange_pre(c, true, n, st))) return r;
+    mark(2);
     if ((r = run_attention(c, n, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, st))) return r;
+    mark(3);
     if ((r = exchange_post(c, n, st))) return r;
     if ((r = cuda_check(c, dz::launch_sp_unpack(c->base + c->L.or_off, out, c->N, c->B, (int32_t)(n / c->N), c->Hl,
                                                 c->D, st),
                         "unpack launch")))
       return r;
   }
+  mark(4);
+  c->have_attend_ev = prof;
   c->staged = true;
   c->staged_id = s->chunk_id;
   c->staged_kind = s->kind;
@@ -523,7 +546,32 @@ dz_status dz_get_tile_map(const dz_ctx* c, uint8_t* host, size_t cap, int32_t* n
   return DZ_OK;
 }
 
+dz_status dz_profile_last(dz_ctx* c, float* ms) {
+  if (!c || !ms) return DZ_EINVAL;
+  if (!c->ev[0]) return fail(c, DZ_ESTATE, "created without DZ_FLAG_PROFILE");
+  for (int i = 0; i < 6; ++i) ms[i] = 0.f;
+  auto el = [&](cudaEvent_t a, cudaEvent_t b, float* o) {
+    if (cudaEventSynchronize(b) != cudaSuccess) return false;
+    return cudaEventElapsedTime(o, a, b) == cudaSuccess;
+  };
+  bool ok = true;
+  if (c->have_attend_ev) {
+    ok &= el(c->ev[0], c->ev[1], &ms[0]);
+    ok &= el(c->ev[1], c->ev[2], &ms[1]);
+    ok &= el(c->ev[2], c->ev[3], &ms[2]);
+    ok &= el(c->ev[3], c->ev[4], &ms[3]);
+    ok &= el(c->ev[0], c->ev[4], &ms[4]);
+  }
+  if (c->have_append_ev) ok &= el(c->ev_app[0], c->ev_app[1], &ms[5]);
+  return ok ? DZ_OK : fail(c, DZ_ECUDA, "cudaEventElapsedTime failed");
+}
+
 dz_status dz_destroy(dz_ctx* c) {
+  if (!c) return DZ_OK;
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev_app)
+    if (e) cudaEventDestroy(e);
   delete c;
   return DZ_OK;
 }
