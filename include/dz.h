@@ -74,7 +74,9 @@ enum { DZ_CLEAN = 0, DZ_NOISY = 1 }; /* dz_span.kind (Fig. 10: C chunks vs Z/Y c
 enum {
   DZ_FLAG_NONE = 0,
   DZ_FLAG_WRITE_LSE = 1, /* keep a per-row log-sum-exp of the last attend (dz_copy_lse) */
-  DZ_FLAG_PROFILE = 2    /* record CUDA events around every kernel/exchange (dz_profile_last) */
+  DZ_FLAG_PROFILE = 2,   /* record CUDA events around every kernel/exchange (dz_profile_last) */
+  DZ_FLAG_ONLINE_SOFTMAX = 4 /* always track the running row max, even when the QK-norm bound
+                                D*max|g|^2*scale would allow a fixed softmax base (see dz_create) */
 };
 
 typedef struct {
@@ -112,9 +114,15 @@ typedef struct {
  *   (heads / world_size) x head_dim x 2 B, rounded up to 256 B. 0 if cfg is invalid. */
 DZ_API size_t dz_cache_bytes(const dz_config* cfg);
 
-/* Validates cfg, computes the RoPE frequencies (fp64, host), allocates the
- * context's own device workspace (Q' and, under SP, the all-to-all buffers).
- * On success *out owns that workspace until dz_destroy. */
+/* Validates cfg and computes the RoPE frequencies (fp64, host).  The device
+ * workspace (Q', the all-to-all buffers under SP, debug maps) lives inside the
+ * caller's cache_storage (dz_cache_bytes counts it); the context allocates no
+ * device memory.  Also derives the QK-norm logit bound
+ *   |<q',k'>| * scale * log2(e) <= head_dim * max_abs_gain^2 * scale * log2(e)
+ * (RMSNorm makes ||x'|| <= sqrt(head_dim) * max|g|); when it is <= 40 the
+ * attention uses it as a fixed softmax base instead of a running row max
+ * (DZ_FLAG_ONLINE_SOFTMAX disables this).  *out is owned by the caller until
+ * dz_destroy. */
 DZ_API dz_status dz_create(const dz_config* cfg, dz_ctx** out);
 
 /* Cache append of a clean chunk (Alg. 2 l.601-602, update=True): K' =
@@ -192,6 +200,12 @@ DZ_API dz_status dz_nccl_comm_destroy(void* comm);
  * finishes with garbage output instead of hanging the GPU.  Copies that record
  * (zeros if no timeout) to host8[8]; reset != 0 clears it.  Synchronous. */
 DZ_API dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset);
+
+/* Pipeline diagnostics: enable != 0 makes later attention launches record a
+ * clock() trace of CTA 0's first work unit (MMA waits/issues, softmax S-ready /
+ * P-done per KV step, up to 256 steps; layout documented in attention.cu).
+ * host != NULL copies up to n words of the last trace.  Synchronous. */
+DZ_API dz_status dz_debug_trace(int32_t enable, uint32_t* host, size_t n);
 
 /* Number of attention work units (batch x heads/world_size x query-tile pairs)
  * for an n-token chunk; the persistent grid is min(units, SM count). */

@@ -32,6 +32,7 @@ LIB_PATH = os.path.join(_HERE, "libdz.so")
 CLEAN, NOISY = 0, 1
 FLAG_WRITE_LSE = 1
 FLAG_PROFILE = 2
+FLAG_ONLINE_SOFTMAX = 4
 
 STATUS = {0: "DZ_OK", -1: "DZ_EINVAL", -2: "DZ_ESHAPE", -3: "DZ_ECAPACITY", -4: "DZ_ESTATE",
           -5: "DZ_ECUDA", -6: "DZ_ENCCL", -7: "DZ_ERANGE"}
@@ -85,6 +86,7 @@ SIGNATURES = [
     ("dz_attention_units", I32, [P, I32]),
     ("dz_debug_watchdog", I32, [P, I32]),
     ("dz_profile_last", I32, [P, P]),
+    ("dz_debug_trace", I32, [I32, P, SZ]),
 ]
 
 _lib = None
@@ -135,6 +137,15 @@ def watchdog(reset: bool = True):
     if s:
         raise DzError(s, "dz_debug_watchdog")
     return list(buf)
+
+
+def debug_trace(enable: bool, read: bool = False) -> Optional[np.ndarray]:
+    """Toggle / read the attention kernel's cycle trace (uint32 [8192]); see dz.h."""
+    buf = np.zeros(8192, dtype=np.uint32) if read else None
+    s = lib().dz_debug_trace(int(enable), buf.ctypes.data if read else None, 8192 if read else 0)
+    if s:
+        raise DzError(s, "dz_debug_trace")
+    return buf
 
 
 def nccl_unique_id() -> bytes:

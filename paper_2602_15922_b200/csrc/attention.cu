@@ -1,4 +1,4 @@
-// attention.cu -- K2: block-causal chunk attention on tcgen05 tensor cores.
+// attention.cu -- K2: block-causal chunk attention on tcgen05 tensor cores, CTA pairs.
 //
 // Computes, for every (b, h, query s) of the current chunk,
 //     O_s = sum_j softmax_j(<q'_s, k'_j> * scale) v_j
@@ -7,20 +7,46 @@
 // committed key and every own-chunk key is visible, so the only masked pairs
 // are out-of-bounds columns of the last KV tile.
 //
-// Structure (one persistent CTA per SM, 12 warps):
-//   warp 0       TMA producer: Q tile pair once per unit, then K_j, V_j into a
-//                ring of 32 KB stages (cp.async.bulk.tensor, SW128).
-//   warp 1       MMA issuer (one thread): S_t = Q_t K_j^T (SS, f16 x f16 -> f32
-//                in TMEM), O_t += P_t V_j (TS, P bf16 from TMEM, V bf16 smem).
-//   warp 2       TMEM allocator (512 columns: S0 S1 O0 O1).
-//   warps 4..7   softmax for Q tile 0, warps 8..11 for Q tile 1: one thread per
-//                query row (TMEM lane), register-resident online softmax with
-//                lazy rescaling (only when the running max grows by > 2^8),
-//                P written back over S in TMEM, epilogue O / l -> bf16 -> HBM.
-// Two Q tiles of the same head share every K/V stage; while one tile's
-// softmax runs, the tensor core works on the other tile (ping-pong).
+// Work unit: a cluster of two CTAs (one SM each, same TPC) owns (batch, head,
+// two consecutive 128-row query tiles); CTA r keeps q-tile 2g + r in shared
+// memory.  Per KV step of 256 keys the leader CTA issues two cta_group::2
+// tcgen05.mma groups (M = 256 rows: 128 per CTA):
+//   S = Q K_j^T      SS, f16 x f16 -> f32, N = 256 keys; each CTA supplies its
+//                    128 query rows and 128 of the step's keys
+//   O += P V_j       TS, P bf16 from TMEM, K = 256 keys, N = D; each CTA
+//                    supplies D/2 of V's columns
+// so each byte of K and V in shared memory is read by one SM, and the shared
+// memory traffic per SM stays under 100 B/clk (the port is 128 B/clk; a 1-CTA
+// M=128 N=128 SS MMA alone saturates it).
+//
+// TMEM per CTA (512 columns): S [0,256) fp32, P [256,384) bf16 pairs, O
+// [384,512).  The pipeline (issue order QK(j) PV(j-1) QK(j+1) PV(j) ...):
+//   * S is released ("S free") as soon as the softmax has copied it into
+//     registers, so QK(j+1) is gated only by that copy, never by the softmax's
+//     exponentials;
+//   * P has its own buffer, so PV(j) runs behind QK(j+1) and overlaps the
+//     softmax of step j+1.
+// Each handshake (commit -> mbarrier -> wake, ~400 clk on this part, measured
+// with tools/handoff_bench.cu) is paid once per 1024 clk of QK work; with
+// 128-key steps and two query tiles per CTA the same handshakes cost ~35% of
+// the tensor pipe (measured: 2750 clk per 2048 clk of MMA work).
+//
+// Warps per CTA (12; schedulers favour high warp ids, so the single-thread
+// roles sit on top):
+//   11     QK issuer (leader CTA)
+//   9      PV issuer (leader CTA)
+//   10     TMA producer (both CTAs; bytes counted on the leader's barriers)
+//   8      TMEM allocator (cta_group::2)
+//   0..7   softmax + epilogue: warp w owns TMEM lanes 32*(w%4).. (query rows)
+//          and S columns 128*(w/4)..+128 (keys), O columns (w/4)*D/2..+D/2.
+//          Fixed softmax base from the QK-norm bound (or a running max with
+//          lazy rescaling, exchanged between the two warps of a row, when the
+//          bound is large); exp2 on MUFU with 3 of every 8 pairs on an
+//          FMA-pipe polynomial.
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -28,72 +54,126 @@
 namespace dz {
 namespace {
 
-constexpr int BM = 128;        // query rows per tile (MMA M)
-constexpr int BN = 128;        // keys per KV tile (MMA N of QK^T, K of PV)
-constexpr int kThreads = 384;  // 12 warps
+constexpr int BM = 128;           // query rows per CTA (MMA M = 256 per pair)
+constexpr int BN = 256;           // keys per KV step
+constexpr int kThreads = 384;     // 12 warps
 constexpr float kRescaleLog2 = 8.0f;
+constexpr int kPolyPairs = 2;     // of every 8 exp2 pairs, this many go to the FMA-pipe polynomial
+constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
+constexpr int kWarpMma = 11, kWarpTma = 10, kWarpPv = 9, kWarpTmem = 8;
+constexpr uint32_t kRegsLight = 88, kRegsSoftmax = 208;  // setmaxnreg: 128*88 + 256*208 = 384*168 (launch)
+
+// Cycle trace of cluster 0's first unit (diagnostics, dz_debug_trace), per CTA
+// rank r at [r * 16 * kTraceSteps]: per step j [8j+0,1] QK wait/issue,
+// [8j+2,3] PV wait/issue (of step j), [8j+4,5] softmax S-ready / P-done
+// (warp 0), [8j+6] S loaded, [8j+7] exp done.
+constexpr int kTraceSteps = 256;
+__device__ uint32_t g_dz_trace[kTraceSteps * 32];
+__device__ int g_dz_trace_on;
 
 template <int D>
 struct Cfg {
-  static constexpr int kBoxes = D / 64;                   // 64-element (128 B) SW128 boxes per row
-  static constexpr int kTileBytes = BM * D * 2;           // Q / K / V tile (fp16 / bf16)
-  static constexpr int kStages = D == 128 ? 4 : 8;
+  static constexpr int kQBoxes = D / 64;                  // 64-column SW128 boxes per Q / K row
+  static constexpr int kQTileBytes = BM * D * 2;          // one CTA's query tile (fp16)
+  static constexpr int kStageBytes = 256 * D;             // K half (128 keys x D) or V half (256 keys x D/2)
+  static constexpr int kStages = D == 128 ? 6 : 12;
   static constexpr int kQOff = 0;
-  static constexpr int kKVOff = 2 * kTileBytes;
-  static constexpr int kBarOff = kKVOff + kStages * kTileBytes;
-  static constexpr int kSmem = kBarOff + 256 + 1024;      // + barriers + 1 KB alignment slack
-  static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, BM, BN);  // f16 x f16, K-major both
-  static constexpr uint32_t kIdescPV = ptx::idesc_f16(1, 1, 0, 1, BM, D);   // bf16 P (TMEM) x bf16 V (MN-major)
+  static constexpr int kKVOff = kQTileBytes;
+  static constexpr int kRedOff = kKVOff + kStages * kStageBytes;  // row max / row sum exchange [2][BM]
+  static constexpr int kBarOff = kRedOff + 2 * BM * 4;
+  static constexpr int kSmem = kBarOff + 256 + 1024;              // + barriers + alignment slack
+  static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, 2 * BM, BN / 2);  // f16 x f16, K-major, per half
+  static constexpr uint32_t kIdescPV = ptx::idesc_f16(1, 1, 0, 1, 2 * BM, D);   // P (TMEM) x V (MN-major)
+  static constexpr int kVRowBytes = D;                      // V half row: D/2 bf16
 };
 
 struct Bars {
-  uint64_t q_full, q_empty;
-  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
-  uint64_t kv_full[8], kv_empty[8];
+  uint64_t q_full, q_empty, s_full[2], s_free[2], p_full, p_empty, o_full, o_empty;
+  uint64_t kv_full[12], kv_empty[12];
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void decode_unit(int u, int n_qpairs, int H, int& b, int& h, int& qp) {
-  qp = u % n_qpairs;
-  const int bh = u / n_qpairs;
+// p = 2^(x + nb) for 32 pairs of scores (already in log2 units): kPolyPairs of
+// every 8 pairs through the FMA-pipe polynomial, the rest through MUFU.EX2;
+// row-sum partials in acc, bf16 pairs in pk.  kOffset: add the softmax base nb
+// (online mode); kClamp: x may be -inf / below -126 (masked tile, online mode).
+template <bool kOffset, bool kClamp>
+__device__ __forceinline__ void exp_half(const float* s, uint64_t nb2, uint32_t (&pk)[32], uint64_t (&acc)[4]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    uint64_t x = ptx::f2_pack(s[2 * i], s[2 * i + 1]);
+    if (kOffset) x = ptx::f2_add(x, nb2);
+    uint64_t p;
+    if ((i % 8) >= 8 - kPolyPairs) {
+      p = ptx::f2_exp2_poly<kClamp>(x);
+    } else {
+      float x0, x1;
+      ptx::f2_unpack(x, x0, x1);
+      p = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+    }
+    acc[i % 4] = ptx::f2_add(acc[i % 4], p);
+    float p0, p1;
+    ptx::f2_unpack(p, p0, p1);
+    pk[i] = ptx::pack_bf16x2(p0, p1);
+  }
+}
+
+__device__ __forceinline__ void decode_unit(int u, int n_groups, int H, int& b, int& h, int& g) {
+  g = u % n_groups;
+  const int bh = u / n_groups;
   h = bh % H;
   b = bh / H;
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ out, int64_t o_bstride,
                     int64_t o_tstride, float* __restrict__ lse, uint8_t* __restrict__ tile_map, int B, int H,
-                    int nq, int kv_len, float scale_log2) {
+                    int nq, int kv_len, float scale_log2, float m_static, int dbg) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
-  // SW128 operands need 1024-byte aligned tiles.
   const uint32_t raw = ptx::smem_u32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t base = (raw + 1023u) & ~1023u;           // SW128 tiles need 1024-byte alignment
   uint8_t* smem = smem_raw + (base - raw);
   Bars* bars = reinterpret_cast<Bars*>(smem + C::kBarOff);
+  float* red = reinterpret_cast<float*>(smem + C::kRedOff);
   const uint32_t sQ = base + C::kQOff;
   const uint32_t sKV = base + C::kKVOff;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
   const int n_qtiles = (nq + BM - 1) / BM;
-  const int n_qpairs = (n_qtiles + 1) / 2;
-  const int n_units = B * H * n_qpairs;
-  const int nkv = (kv_len + BN - 1) / BN;
+  const int n_groups = (n_qtiles + 1) / 2;                 // 2 query tiles per cluster unit
+  const int n_units = B * H * n_groups;
+  const int nkv = (kv_len + BN - 1) / BN;                  // 256-key steps
+  const int nkv128 = (kv_len + 127) / 128;                 // 128-key tiles (tile-map granularity)
+  const int cid = (int)ptx::cluster_id_x(), ncl = (int)ptx::nclusters_x();
+  const bool trace_on = g_dz_trace_on != 0 && cid == 0;
+  uint32_t* const trace = g_dz_trace + rank * kTraceSteps * 16;
+  constexpr uint16_t kBoth = 0x3;
 
   auto bar = [&](uint64_t& b) { return ptx::smem_u32(&b); };
+  auto lbar = [&](uint64_t& b) { return ptx::mapa(ptx::smem_u32(&b), 0); };  // leader's copy
+  // ring slot of the i-th K/V load (TMA order K0 V0 K1 V1 ...)
+  auto slot = [&](uint32_t i, uint32_t& st, uint32_t& ph) {
+    st = i % C::kStages;
+    ph = (i / C::kStages) & 1;
+  };
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpTma && lane == 0) {
     ptx::mbar_init(bar(bars->q_full), 1);
     ptx::mbar_init(bar(bars->q_empty), 1);
-    for (int t = 0; t < 2; ++t) {
-      ptx::mbar_init(bar(bars->s_full[t]), 1);
-      ptx::mbar_init(bar(bars->p_full[t]), 4);
-      ptx::mbar_init(bar(bars->o_full[t]), 1);
-      ptx::mbar_init(bar(bars->o_empty[t]), 4);
+    for (int hh = 0; hh < 2; ++hh) {
+      ptx::mbar_init(bar(bars->s_full[hh]), 1);
+      ptx::mbar_init(bar(bars->s_free[hh]), 8);  // 4 softmax warps of that key half x 2 CTAs
     }
+    ptx::mbar_init(bar(bars->p_full), 16);
+    ptx::mbar_init(bar(bars->p_empty), 1);
+    ptx::mbar_init(bar(bars->o_full), 1);
+    ptx::mbar_init(bar(bars->o_empty), 16);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(bar(bars->kv_full[s]), 1);
       ptx::mbar_init(bar(bars->kv_empty[s]), 1);
@@ -103,229 +183,284 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
   }
-  if (warp == 2) ptx::tmem_alloc<512>(ptx::smem_u32(&bars->tmem_base));
+  if (warp == kWarpTmem) ptx::tmem_alloc_2cta<512>(ptx::smem_u32(&bars->tmem_base));
   if (blockIdx.x == 0 && threadIdx.x == 0) ptx::g_dz_watchdog[6] = ptx::smem_u32(bars);
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();  // both CTAs' barriers initialised and TMEM allocated before any remote traffic
   ptx::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  if (warp == 0) {
+  if (warp >= 8) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsLight));
+  if (warp == kWarpTma) {
     // ------------------------------------------------------ TMA producer --
     const uint64_t pol_q = ptx::l2_policy_evict_first();
     const uint64_t pol_kv = ptx::l2_policy_evict_last();
-    uint32_t stage = 0, phase = 0, q_phase = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int b, h, qp;
-      decode_unit(u, n_qpairs, H, b, h, qp);
+    uint32_t ld = 0, q_phase = 0;
+    for (int u = cid; u < n_units; u += ncl) {
+      int b, h, g;
+      decode_unit(u, n_groups, H, b, h, g);
       ptx::mbar_wait(bar(bars->q_empty), q_phase ^ 1);
       q_phase ^= 1;
+      const int qt = 2 * g + (int)rank;
       if (lane == 0) {
-        // the second tile of the last pair may lie wholly past nq: do not load it
-        // (its rows are computed on stale data and never stored).
-        const int tiles = (2 * qp + 1 < n_qtiles) ? 2 : 1;
-        ptx::mbar_arrive_expect_tx(bar(bars->q_full), tiles * C::kTileBytes);
-        for (int t = 0; t < tiles; ++t)
-          for (int x = 0; x < C::kBoxes; ++x)
-            ptx::tma_load_4d(sQ + t * C::kTileBytes + x * BM * 128, &tm_q, bar(bars->q_full), x * 64, h,
-                             (2 * qp + t) * BM, b, pol_q);
+        if (leader) ptx::mbar_arrive_expect_tx(bar(bars->q_full), min(2, n_qtiles - 2 * g) * C::kQTileBytes);
+        if (qt < n_qtiles)  // a tile wholly past nq is not loaded (its rows are never stored)
+          for (int x = 0; x < C::kQBoxes; ++x)
+            ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * 64, h, qt * BM, b, pol_q);
       }
       for (int j = 0; j < nkv; ++j) {
-        for (int kv = 0; kv < 2; ++kv) {  // K_j then V_j
-          ptx::mbar_wait(bar(bars->kv_empty[stage]), phase ^ 1);
-          if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(bar(bars->kv_full[stage]), C::kTileBytes);
-            for (int x = 0; x < C::kBoxes; ++x)
-              ptx::tma_load_4d(sKV + stage * C::kTileBytes + x * BN * 128, kv == 0 ? &tm_k : &tm_v,
-                               bar(bars->kv_full[stage]), x * 64, h, j * BN, b, pol_kv);
+        for (int kv = 0; kv < 2; ++kv, ++ld) {  // K_j half (128 keys x D), then V_j half (256 keys x D/2)
+          uint32_t st, ph;
+          slot(ld, st, ph);
+          ptx::mbar_wait(bar(bars->kv_empty[st]), ph ^ 1);
+          if (lane == 0 && (dbg & 1)) {  // diagnostics: no K/V traffic, MMAs read stale smem
+            if (leader) ptx::mbar_arrive(bar(bars->kv_full[st]));
+          } else if (lane == 0) {
+            if (leader) ptx::mbar_arrive_expect_tx(bar(bars->kv_full[st]), 2 * C::kStageBytes);
+            const uint32_t dst = sKV + st * C::kStageBytes;
+            if (kv == 0) {
+              // S half hh (keys 128hh..128hh+127 of the step) takes 64 keys from each CTA:
+              // this CTA loads keys 128hh + 64*rank .. +63 into [hh][dim box] of 64 x 128 B
+              for (int hh = 0; hh < 2; ++hh)
+                for (int x = 0; x < C::kQBoxes; ++x)
+                  ptx::tma_load_4d_2cta(dst + (hh * C::kQBoxes + x) * 64 * 128, &tm_k, lbar(bars->kv_full[st]),
+                                        x * 64, h, j * BN + 128 * hh + 64 * (int)rank, b, pol_kv);
+            } else {
+              ptx::tma_load_4d_2cta(dst, &tm_v, lbar(bars->kv_full[st]), (int)rank * (D / 2), h, j * BN, b, pol_kv);
+            }
           }
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
       __syncwarp();
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------- MMA issuer --
-    uint32_t stage = 0, phase = 0, q_phase = 0;
-    uint32_t p_phase[2] = {0, 0}, oe_phase[2] = {0, 0};
-    const uint32_t tS[2] = {tmem + 0, tmem + 128};
-    const uint32_t tO[2] = {tmem + 256, tmem + 384};
-    auto qk = [&](int t, uint32_t kst) {
-      const uint32_t qa = sQ + t * C::kTileBytes, ka = sKV + kst * C::kTileBytes;
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t off = (kk / 4) * (BM * 128) + (kk % 4) * 32;
-        ptx::mma_ss(tS[t], ptx::sdesc_sw128(qa + off, 16, 1024), ptx::sdesc_sw128(ka + off, 16, 1024),
-                    C::kIdescQK, kk > 0);
-      }
-    };
-    auto pv = [&](int t, uint32_t vst, bool acc) {
-      const uint32_t va = sKV + vst * C::kTileBytes;
-#pragma unroll
-      for (int kk = 0; kk < BN / 16; ++kk)
-        ptx::mma_ts(tO[t], tS[t] + kk * 8, ptx::sdesc_sw128(va + kk * 16 * 128, BN * 128, 1024), C::kIdescPV,
-                    (acc || kk > 0) ? 1u : 0u);
-    };
-    auto next = [&](uint32_t& st) {
-      st = stage;
-      if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-    };
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      ptx::mbar_wait(bar(bars->q_full), q_phase);
-      q_phase ^= 1;
-      uint32_t k_st, v_st;
-      ptx::mbar_wait(bar(bars->kv_full[stage]), phase);
-      next(k_st);
-      ptx::tc_fence_after();
-      if (lane == 0) {
-        for (int t = 0; t < 2; ++t) {
-          qk(t, k_st);
-          ptx::tc_commit(bar(bars->s_full[t]));
+  } else if ((warp == kWarpMma || warp == kWarpPv) && leader) {
+    // ------------------------------------------------------ MMA issuers --
+    // Two single-thread issuers walk the flattened steps g of this cluster's
+    // units: warp 11 issues QK(g), warp 9 issues PV(g-1).  tcgen05.mma issue
+    // blocks at the tensor pipe's rate (the queue is shallow), so an issuer that
+    // waits on a barrier starves the pipe; with two issuers, one keeps it fed
+    // while the other waits.  QK and PV touch disjoint TMEM (S vs P/O) and
+    // release their own K / V stages, so their streams need no mutual order.
+    const bool do_qk = warp == kWarpMma;
+    uint32_t q_phase = 0, sf_phase = 0, pf_phase = 0, oe_phase = 0;
+    const int my_units = cid < n_units ? (n_units - cid + ncl - 1) / ncl : 0;
+    const int G = my_units * nkv;
+    for (int gs = 0; gs <= G; ++gs) {
+      const int j = gs % nkv;
+      const bool tr = trace_on && gs < kTraceSteps && gs < nkv && lane == 0;
+      if (do_qk && gs < G) {
+        if (j == 0) {  // first step of a new unit: its Q tiles
+          ptx::mbar_wait(bar(bars->q_full), q_phase);
+          q_phase ^= 1;
         }
-        ptx::tc_commit(bar(bars->kv_empty[k_st]));
-        if (nkv == 1) ptx::tc_commit(bar(bars->q_empty));
-      }
-      __syncwarp();
-      for (int j = 1; j < nkv; ++j) {
-        ptx::mbar_wait(bar(bars->kv_full[stage]), phase);  // V_{j-1}
-        next(v_st);
-        ptx::mbar_wait(bar(bars->kv_full[stage]), phase);  // K_j
-        next(k_st);
-        for (int t = 0; t < 2; ++t) {
-          ptx::mbar_wait(bar(bars->p_full[t]), p_phase[t]);
-          p_phase[t] ^= 1;
-          if (j == 1) {
-            ptx::mbar_wait(bar(bars->o_empty[t]), oe_phase[t] ^ 1);
-            oe_phase[t] ^= 1;
+        uint32_t k_st, k_ph;
+        slot(2 * gs, k_st, k_ph);
+        ptx::mbar_wait(bar(bars->kv_full[k_st]), k_ph);
+        // S in two halves of 128 keys (N = 128 each): the half-hh softmax warps release
+        // their half as soon as they hold it, so each QK half waits only for the copy
+        // of the same half of the previous step
+        for (int hh = 0; hh < 2; ++hh) {
+          if (tr && hh == 0) trace[j * 8 + 0] = (uint32_t)clock();
+          if (gs > 0) {
+            ptx::mbar_wait(bar(bars->s_free[hh]), sf_phase);
+            if (hh == 1) sf_phase ^= 1;
           }
+          if (tr && hh == 0) trace[j * 8 + 1] = (uint32_t)clock();
           ptx::tc_fence_after();
           if (lane == 0) {
-            pv(t, v_st, j > 1);
-            qk(t, k_st);
-            ptx::tc_commit(bar(bars->s_full[t]));
+            const uint32_t ka = sKV + k_st * C::kStageBytes + hh * C::kQBoxes * 64 * 128;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t qoff = (kk / 4) * (128 * 128) + (kk % 4) * 32;  // Q: 128 rows per box
+              const uint32_t koff = (kk / 4) * (64 * 128) + (kk % 4) * 32;   // K half: 64 rows per box
+              ptx::mma_ss_2cta(tmem + kColS + hh * 128, ptx::sdesc_sw128(sQ + qoff, 16, 1024),
+                               ptx::sdesc_sw128(ka + koff, 16, 1024), C::kIdescQK, kk > 0);
+              if (tr && j == 9) trace[kTraceSteps * 8 + hh * 8 + kk] = (uint32_t)clock();
+            }
+            ptx::tc_commit_2cta(bar(bars->s_full[hh]), kBoth);
+            if (hh == 1) {
+              ptx::tc_commit_2cta(bar(bars->kv_empty[k_st]), kBoth);
+              if (j == nkv - 1) ptx::tc_commit_2cta(bar(bars->q_empty), kBoth);
+            }
           }
           __syncwarp();
         }
-        if (lane == 0) {
-          ptx::tc_commit(bar(bars->kv_empty[v_st]));
-          ptx::tc_commit(bar(bars->kv_empty[k_st]));
-          if (j == nkv - 1) ptx::tc_commit(bar(bars->q_empty));
-        }
-        __syncwarp();
       }
-      ptx::mbar_wait(bar(bars->kv_full[stage]), phase);  // V_{nkv-1}
-      next(v_st);
-      for (int t = 0; t < 2; ++t) {
-        ptx::mbar_wait(bar(bars->p_full[t]), p_phase[t]);
-        p_phase[t] ^= 1;
-        if (nkv == 1) {
-          ptx::mbar_wait(bar(bars->o_empty[t]), oe_phase[t] ^ 1);
-          oe_phase[t] ^= 1;
+      if (!do_qk && gs > 0) {
+        const int jp = (gs - 1) % nkv;
+        const bool trp = trace_on && gs - 1 < nkv && lane == 0;
+        uint32_t v_st, v_ph;
+        slot(2 * (gs - 1) + 1, v_st, v_ph);
+        ptx::mbar_wait(bar(bars->kv_full[v_st]), v_ph);
+        if (trp) trace[jp * 8 + 2] = (uint32_t)clock();
+        ptx::mbar_wait(bar(bars->p_full), pf_phase);
+        pf_phase ^= 1;
+        if (jp == 0) {  // the previous unit's epilogue has read O
+          ptx::mbar_wait(bar(bars->o_empty), oe_phase ^ 1);
+          oe_phase ^= 1;
         }
+        if (trp) trace[jp * 8 + 3] = (uint32_t)clock();
         ptx::tc_fence_after();
         if (lane == 0) {
-          pv(t, v_st, nkv > 1);
-          ptx::tc_commit(bar(bars->o_full[t]));
+          const uint32_t va = sKV + v_st * C::kStageBytes;
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            const uint64_t bd = D == 128 ? ptx::sdesc_sw128(va + kk * 16 * C::kVRowBytes, 16, 1024)
+                                         : ptx::sdesc_sw64(va + kk * 16 * C::kVRowBytes, 16, 512);
+            ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + kk * 8, bd, C::kIdescPV, (jp > 0 || kk > 0) ? 1u : 0u);
+            if (trp && jp == 9) trace[kTraceSteps * 8 + 16 + kk] = (uint32_t)clock();
+          }
+          ptx::tc_commit_2cta(bar(bars->p_empty), kBoth);              // P may be overwritten
+          if (jp == nkv - 1) ptx::tc_commit_2cta(bar(bars->o_full), kBoth);
+          ptx::tc_commit_2cta(bar(bars->kv_empty[v_st]), kBoth);
         }
         __syncwarp();
       }
-      if (lane == 0) ptx::tc_commit(bar(bars->kv_empty[v_st]));
-      __syncwarp();
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
     // ---------------------------------------------- softmax + epilogue --
-    const int t = (warp - 4) / 4;
-    const int quad = warp % 4;
+    const int quad = warp % 4;                  // TMEM lane quadrant (query rows)
+    const int hc = warp / 4;                    // key half of S / column half of O
     const int row = quad * 32 + lane;
     const uint32_t lane_bits = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_bits + t * 128;
-    const uint32_t tO = tmem + lane_bits + 256 + t * 128;
-    uint32_t s_phase = 0, of_phase = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int b, h, qp;
-      decode_unit(u, n_qpairs, H, b, h, qp);
-      float m_used = -INFINITY;  // running max in log2 units of scaled scores
-      float l = 0.f;
+    const uint32_t tS = tmem + lane_bits + kColS + hc * 128;
+    const uint32_t tP = tmem + lane_bits + kColP + hc * 64;
+    const uint32_t tO = tmem + lane_bits + kColO + hc * (D / 2);
+    const uint32_t pair_bar = 1 + quad;         // named barrier: the two warps of these rows
+    uint32_t s_phase = 0, pe_phase = 0, of_phase = 0;
+    for (int u = cid; u < n_units; u += ncl) {
+      int b, h, g;
+      decode_unit(u, n_groups, H, b, h, g);
+      const int qt = 2 * g + (int)rank;
+      float m_used = m_static > 0.f ? 0.f : -INFINITY;  // softmax base, log2 units (fixed base: 0)
+      float l = 0.f;                                          // partial row sum over this warp's keys
       for (int j = 0; j < nkv; ++j) {
-        ptx::mbar_wait(bar(bars->s_full[t]), s_phase);
+        ptx::mbar_wait(bar(bars->s_full[hc]), s_phase);
         s_phase ^= 1;
+        const bool tr = trace_on && u == cid && j < kTraceSteps && row == 0 && hc == 0;
+        if (tr) trace[j * 8 + 4] = (uint32_t)clock();
         ptx::tc_fence_after();
-        float s[BN];
+        float s[128];
         {
-          uint32_t r[32];
+          uint32_t r[128];
+          if (dbg & 2) {  // diagnostics: no TMEM loads of S
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c) {
-            ptx::tmem_ld32(tS + c * 32, r);
+            for (int i = 0; i < 128; ++i) r[i] = __float_as_uint((float)((i * 7 + row) & 15) * 0.01f);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[c * 32]));
             ptx::tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
           }
-        }
-        const int kv_valid = kv_len - j * BN;
-        if (tile_map != nullptr && u < n_qpairs && row == 0) {
-          // debug: the kernel's own per-tile decision for unit (b=0, h=0):
-          // 2 FULL (no column masked, all rows in bounds), 1 PARTIAL (masked).
-          const int qt = 2 * qp + t;
-          if (qt < n_qtiles) tile_map[qt * nkv + j] = (kv_valid >= BN && nq - qt * BM >= BM) ? 2 : 1;
-        }
-        if (kv_valid < BN) {
 #pragma unroll
-          for (int i = 0; i < BN; ++i)
+          for (int i = 0; i < 128; ++i) s[i] = __uint_as_float(r[i]);
+        }
+        // S is in registers: the next QK may overwrite it now
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->s_free[hc]));
+        if (tr) trace[j * 8 + 6] = (uint32_t)clock();
+        const int kt = 2 * j + hc;                  // this warp's 128-key tile
+        const int kv_valid = kv_len - kt * 128;     // valid keys among its 128 columns
+        if (tile_map != nullptr && u < n_groups && row == 0 && qt < n_qtiles && kt < nkv128)
+          // debug: the kernel's own per-tile decision for (b, h) = (0, 0): 2 FULL, 1 PARTIAL
+          tile_map[qt * nkv128 + kt] = (kv_valid >= 128 && nq - qt * BM >= BM) ? 2 : 1;
+        if (kv_valid < 128) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
             if (i >= kv_valid) s[i] = -INFINITY;
         }
-        float mx = s[0];
+        const bool online = m_static <= 0.f;
+        if (online) {
+          // Online softmax with lazy rescaling: a row moves its base only when its max
+          // grew by more than 2^8; both warps of a row take the same decision from the
+          // exchanged maxima.  O may be rescaled only when no PV into it is in flight:
+          // wait for PV(j-1) (p_empty) first.  tcgen05.ld/st are warp-collective, so
+          // the decision is warp-uniform.
+          float mx = s[0];
 #pragma unroll
-        for (int i = 1; i < BN; ++i) mx = fmaxf(mx, s[i]);
-        const float mx_s = mx * scale_log2;
-        // Lazy rescale: a row moves its softmax base only when its max grew by
-        // more than 2^8.  The decision is made per row, but the TMEM traffic it
-        // needs (tcgen05.ld/st are warp-collective) is issued by the whole warp.
-        const bool grow = mx_s > m_used + kRescaleLog2;
-        const bool rescale = grow && j > 0 && m_used != -INFINITY;
-        if (__any_sync(0xffffffffu, rescale)) {
-          // O_t is quiescent here: PV_t(j-1) completed before S_t(j) was committed.
-          const float alpha = rescale ? ptx::ex2(m_used - mx_s) : 1.f;
-          l *= alpha;
-          uint32_t r[32];
+          for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+          red[hc * BM + row] = mx;
+          ptx::named_bar_sync(pair_bar, 64);
+          mx = fmaxf(mx, red[(hc ^ 1) * BM + row]);
+          ptx::named_bar_sync(pair_bar, 64);  // both read before the next exchange
+          const bool grow = mx > m_used + kRescaleLog2;
+          const bool rescale = grow && j > 0 && m_used != -INFINITY;
+          if (__any_sync(0xffffffffu, rescale)) {
+            ptx::mbar_wait(bar(bars->p_empty), pe_phase ^ 1);  // PV(j-1) done
+            ptx::tc_fence_after();
+            const float alpha = rescale ? ptx::ex2(m_used - mx) : 1.f;
+            l *= alpha;
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            ptx::tmem_ld32(tO + c * 32, r);
-            ptx::tmem_wait_ld();
+            for (int c = 0; c < D / 64; ++c) {
+              uint32_t r[32];
+              ptx::tmem_ld32(tO + c * 32, r);
+              ptx::tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            ptx::tmem_st32(tO + c * 32, r);
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+              ptx::tmem_st32(tO + c * 32, r);
+            }
+            ptx::tmem_wait_st();
           }
-          ptx::tmem_wait_st();
+          if (grow) m_used = mx;
         }
-        if (grow) m_used = mx_s;
-        const float nbase = (m_used == -INFINITY) ? 0.f : -m_used;
+        // Scores are in log2 units (Q' was pre-scaled by scale*log2e).  Fixed base (QK-norm
+        // bound, m_static <= 40): p = 2^s directly, every p in [2^-40, 2^40], so neither an
+        // offset nor a clamp is needed; online base: p = 2^(s - m).
+        const float nbase = (!online || m_used == -INFINITY) ? 0.f : -m_used;
+        const uint64_t nb2 = ptx::f2_pack(nbase, nbase);
+        const bool plain = !online && kv_valid >= 128;
         __syncwarp();
+        uint64_t acc[4] = {0, 0, 0, 0};
+        // two halves of 64 keys: exponentials of half h, then its P store (the first store
+        // waits until PV(j-1) has read P), so only 32 packed registers are live at a time
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t pk[16];
+        for (int half = 0; half < 2; ++half) {
+          uint32_t pk[32];
+          if (dbg & 4) {  // diagnostics: no exponentials (P = packed S)
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float p0 = ptx::ex2(fmaf(s[c * 32 + 2 * i], scale_log2, nbase));
-            const float p1 = ptx::ex2(fmaf(s[c * 32 + 2 * i + 1], scale_log2, nbase));
-            l += p0 + p1;
-            pk[i] = ptx::pack_bf16x2(p0, p1);
+            for (int i = 0; i < 32; ++i) pk[i] = ptx::pack_bf16x2(s[64 * half + 2 * i], s[64 * half + 2 * i + 1]);
+          } else if (plain) {
+            exp_half<false, false>(s + 64 * half, nb2, pk, acc);
+          } else {
+            exp_half<true, true>(s + 64 * half, nb2, pk, acc);
           }
-          ptx::tmem_st16(tS + c * 16, pk);
+          if (half == 0) {
+            if (tr) trace[j * 8 + 7] = (uint32_t)clock();
+            // P may be overwritten once PV(j-1) has read it
+            ptx::mbar_wait(bar(bars->p_empty), pe_phase ^ 1);
+            pe_phase ^= 1;
+            ptx::tc_fence_after();
+          }
+          ptx::tmem_st32(tP + 32 * half, pk);
+        }
+        {
+          const uint64_t a = ptx::f2_add(ptx::f2_add(acc[0], acc[1]), ptx::f2_add(acc[2], acc[3]));
+          float a0, a1;
+          ptx::f2_unpack(a, a0, a1);
+          l += a0 + a1;
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(bar(bars->p_full[t]));
+        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->p_full));
+        if (tr) trace[j * 8 + 5] = (uint32_t)clock();
       }
-      // epilogue: O_t / l -> bf16 -> HBM
-      ptx::mbar_wait(bar(bars->o_full[t]), of_phase);
+      // epilogue: total row sum over both key halves, O / l -> bf16 -> HBM (this warp's D/2 columns)
+      red[hc * BM + row] = l;
+      ptx::named_bar_sync(pair_bar, 64);
+      const float lt = l + red[(hc ^ 1) * BM + row];
+      ptx::named_bar_sync(pair_bar, 64);  // the buffer is reused by the next exchange
+      ptx::mbar_wait(bar(bars->o_full), of_phase);
       of_phase ^= 1;
       ptx::tc_fence_after();
-      const int s_idx = (2 * qp + t) * BM + row;
-      const float inv_l = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* orow = out + b * o_bstride + (int64_t)s_idx * o_tstride + (int64_t)h * D;
+      const int s_idx = qt * BM + row;
+      const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
+      __nv_bfloat16* orow = out + b * o_bstride + (int64_t)s_idx * o_tstride + (int64_t)h * D + hc * (D / 2);
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 64; ++c) {
         uint32_t r[32];
         __syncwarp();  // reconverge after the row-dependent store below
         ptx::tmem_ld32(tO + c * 32, r);
@@ -340,19 +475,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::st_global_v4(orow + c * 32 + v * 8, pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
         }
       }
-      if (lse != nullptr && s_idx < nq)
+      if (lse != nullptr && hc == 0 && s_idx < nq)
         lse[((int64_t)b * H + h) * nq + s_idx] =
-            (l > 0.f) ? (m_used + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+            (lt > 0.f) ? (m_used + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar(bars->o_empty[t]));
+      if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));
     }
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();  // no remote arrives / multicast commits may target an exited CTA
   ptx::tc_fence_after();
-  if (warp == 2) ptx::tmem_dealloc<512>(tmem);
+  if (warp == kWarpTmem) ptx::tmem_dealloc_2cta<512>(tmem);
 }
 
 template <int D>
@@ -362,8 +497,8 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return e;
   k<<<a.grid, kThreads, C::kSmem, s>>>(a.tm_q, a.tm_k, a.tm_v, static_cast<__nv_bfloat16*>(a.out), a.o_bstride,
-                                       a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq, a.kv_len,
-                                       a.scale_log2);
+                                       a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq, a.kv_len, a.scale_log2,
+                                       a.m_static, a.debug_flags);
   return cudaGetLastError();
 }
 
@@ -372,6 +507,12 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
 cudaError_t read_watchdog(uint32_t* host8) {
   return cudaMemcpyFromSymbol(host8, ptx::g_dz_watchdog, sizeof(uint32_t) * 8);
 }
+cudaError_t trace_control(int enable, uint32_t* host, size_t n) {
+  cudaError_t e = cudaMemcpyToSymbol(g_dz_trace_on, &enable, sizeof(int));
+  if (e != cudaSuccess || host == nullptr) return e;
+  const size_t bytes = std::min(n, (size_t)kTraceSteps * 32) * sizeof(uint32_t);
+  return cudaMemcpyFromSymbol(host, g_dz_trace, bytes);
+}
 cudaError_t reset_watchdog() {
   static const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   return cudaMemcpyToSymbol(ptx::g_dz_watchdog, zero, sizeof zero);
@@ -379,7 +520,7 @@ cudaError_t reset_watchdog() {
 
 int attention_units(int32_t B, int32_t H, int32_t nq) {
   const int n_qtiles = (nq + BM - 1) / BM;
-  return B * H * ((n_qtiles + 1) / 2);
+  return B * H * ((n_qtiles + 1) / 2);  // cluster units (pairs of CTAs, one query tile each)
 }
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s) {

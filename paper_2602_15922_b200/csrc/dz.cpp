@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <deque>
 #include <mutex>
 #include <new>
@@ -92,18 +93,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 4D token-major tensor [B][tokens][H][D] (16-bit elements) as TMA dims (D, H, tokens, B),
-// box (64, 1, 128, 1), 128-byte swizzle, out-of-bounds elements read as zero.
+// box (box_d, 1, box_t, 1); swizzle = box_d * 2 bytes (128 or 64); out-of-bounds elements read as zero.
 bool make_tmap(CUtensorMap* m, const void* base, bool bf16, int64_t D, int64_t H, int64_t tokens, int64_t B,
-               int64_t batch_stride_elems) {
+               int64_t batch_stride_elems, uint32_t box_d, uint32_t box_t) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)tokens, (cuuint64_t)B};
   cuuint64_t strides[3] = {(cuuint64_t)(D * 2), (cuuint64_t)(H * D * 2), (cuuint64_t)(batch_stride_elems * 2)};
-  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t box[4] = {box_d, 1, box_t, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUtensorMapSwizzle sw = box_d * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
-                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -114,6 +116,7 @@ struct dz_ctx {
   Layout L;
   int B = 0, H = 0, Hl = 0, D = 0, N = 1, rank = 0;
   float theta = 1e4f, eps = 1e-6f, scale = 0.f;
+  float m_static = 0.f;  // QK-norm logit bound used as a fixed softmax base (0: online max)
   int num_sms = 148;
   // committed state
   int64_t start = 0, valid = 0;
@@ -261,6 +264,7 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
   const int64_t n = s->n_tokens, n_loc = n / c->N;
   dz::PrologueArgs a;
   fill_prologue_common(c, a, s, n_loc);
+  a.q_scale = c->scale * 1.4426950408889634f;  // scores leave the QK MMA in log2 units
   a.x[0] = q;
   a.x[1] = k;
   a.x[2] = v;
@@ -320,9 +324,11 @@ dz_status run_attention(dz_ctx* c, int64_t n, void* out_local, int64_t o_bstride
   dz::AttnArgs a;
   const int64_t kv_len = c->valid + n;
   const int64_t bs = c->L.slots * c->Hl * c->D;
-  if (!make_tmap(&a.tm_q, c->base + c->L.q_off, false, c->D, c->Hl, n, c->B, n * c->Hl * c->D) ||
-      !make_tmap(&a.tm_k, c->kslot(0, c->start), false, c->D, c->Hl, kv_len, c->B, bs) ||
-      !make_tmap(&a.tm_v, c->vslot(0, c->start), true, c->D, c->Hl, kv_len, c->B, bs))
+  // Q: 128-row tiles per CTA; K: each CTA of a pair loads 2 x 64 of a step's 256 keys;
+  // V: each CTA loads D/2 of the columns of all 256 keys (see attention.cu).
+  if (!make_tmap(&a.tm_q, c->base + c->L.q_off, false, c->D, c->Hl, n, c->B, n * c->Hl * c->D, 64, 128) ||
+      !make_tmap(&a.tm_k, c->kslot(0, c->start), false, c->D, c->Hl, kv_len, c->B, bs, 64, 64) ||
+      !make_tmap(&a.tm_v, c->vslot(0, c->start), true, c->D, c->Hl, kv_len, c->B, bs, (uint32_t)c->D / 2, 256))
     return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled failed");
   a.out = out_local;
   a.o_bstride = o_bstride;
@@ -334,8 +340,10 @@ dz_status run_attention(dz_ctx* c, int64_t n, void* out_local, int64_t o_bstride
   a.nq = (int32_t)n;
   a.kv_len = (int32_t)kv_len;
   a.scale_log2 = c->scale * 1.4426950408889634f;
-  const int units = dz::attention_units(c->B, c->Hl, (int32_t)n);
-  a.grid = std::min(units, c->num_sms);
+  a.m_static = c->m_static;
+  if (const char* e = getenv("DZ_DEBUG_KERNEL")) a.debug_flags = atoi(e);  // diagnostics: results are garbage
+  const int units = dz::attention_units(c->B, c->Hl, (int32_t)n);  // CTA-pair units
+  a.grid = 2 * std::min(units, c->num_sms / 2);                      // persistent: one CTA pair per TPC
   const int nqt = (int)((n + 127) / 128), nkt = (int)((kv_len + 127) / 128);
   const size_t map_cap = 4096 + (size_t)((c->cfg.max_chunk_tokens + 127) / 128) *
                                     ((c->cfg.cache_capacity_tokens + c->cfg.max_chunk_tokens + 127) / 128);
@@ -401,6 +409,15 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   c->pro.gain[0] = cfg->q_gain;
   c->pro.gain[1] = cfg->k_gain;
   c->pro.eps = c->eps;
+  // RMSNorm gives ||q'|| <= sqrt(D) max|g|, ||k'|| <= sqrt(D) max|g| (RoPE keeps norms), so
+  // |score| * log2e <= D * max|g|^2 * scale * log2e (+0.5% for the fp16 rounding of Q'/K').
+  // When that bound is small the kernel uses it as a fixed softmax base: every 2^(x - m)
+  // stays within (2^-80, 1], far from fp32/bf16 underflow, and no running max is needed.
+  {
+    const double bound = (double)cfg->head_dim * cfg->max_abs_gain * cfg->max_abs_gain * c->scale *
+                         1.4426950408889634 * 1.005;
+    c->m_static = (!(cfg->flags & DZ_FLAG_ONLINE_SOFTMAX) && bound <= 40.0) ? (float)std::max(bound, 1.0) : 0.f;  // > 0 selects the fixed base
+  }
   if (cfg->flags & DZ_FLAG_PROFILE) {
     for (auto& e : c->ev)
       if (cudaEventCreate(&e) != cudaSuccess) e = nullptr;
@@ -618,6 +635,10 @@ dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset) {
   if (dz::read_watchdog(host8) != cudaSuccess) return DZ_ECUDA;
   if (reset && dz::reset_watchdog() != cudaSuccess) return DZ_ECUDA;
   return DZ_OK;
+}
+
+dz_status dz_debug_trace(int32_t enable, uint32_t* host, size_t n) {
+  return dz::trace_control(enable, host, n) == cudaSuccess ? DZ_OK : DZ_ECUDA;
 }
 
 int32_t dz_attention_units(const dz_ctx* c, int32_t n) {

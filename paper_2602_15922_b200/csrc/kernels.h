@@ -26,6 +26,7 @@ struct PrologueArgs {
   OutSlot y[3];                                    // q' fp16, k' fp16, v bf16
   int32_t B = 0, n = 0, H = 0, D = 0, heads_per_dest = 0;
   float eps = 1e-6f;
+  float q_scale = 1.f;                             // extra factor on Q' (softmax_scale * log2e)
   double omega[kMaxHeadDim / 2];                   // per pair j: theta^(-2i/d_a), fp64 (host)
   int8_t axis[kMaxHeadDim / 2];                    // per pair j: 0 t, 1 h, 2 w
 };
@@ -41,13 +42,16 @@ struct AttnArgs {
   float* lse = nullptr;           // optional fp32 [B][H][nq] natural-log LSE
   uint8_t* tile_map = nullptr;    // optional debug [n_q_tiles][n_kv_tiles] for (b, h) = (0, 0)
   int32_t B = 0, H = 0, D = 0, nq = 0, kv_len = 0;
-  float scale_log2 = 0.f;         // softmax_scale * log2(e)
+  float scale_log2 = 0.f;         // unused by the kernel: Q' is pre-scaled by softmax_scale * log2(e)
+  float m_static = 0.f;           // > 0: fixed softmax base (log2 units) bounding every logit; 0: online max
+  int32_t debug_flags = 0;        // diagnostics only (DZ_DEBUG_KERNEL env): 1 no K/V TMA, 2 no S loads
   int32_t grid = 0;               // persistent CTAs (<= #SMs)
 };
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);
 int attention_units(int32_t B, int32_t H, int32_t nq);
 cudaError_t read_watchdog(uint32_t* host8);   // {fired, block, warp, bar addr, parity, smid, bars base, 0}
-cudaError_t reset_watchdog();  // work units (b, h, q-tile pair)
+cudaError_t reset_watchdog();
+cudaError_t trace_control(int enable, uint32_t* host, size_t n);  // K2 cycle trace (CTA 0, first unit)  // work units (b, h, q-tile pair)
 
 // ---- K5: Ulysses receive unpack [N][B][n_loc][Hl][D] -> [B][n_loc][H][D] ---
 cudaError_t launch_sp_unpack(const void* recv, void* out, int32_t N, int32_t B, int32_t n_loc, int32_t Hl,

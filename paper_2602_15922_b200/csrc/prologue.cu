@@ -5,7 +5,9 @@
 // per (token, head) row of D elements (BJ:5 "per-head RMSNorm on Q/K and 3D
 // (frame, height, width) RoPE"; readings A1-A9 in DESIGN.md: interleaved pairs
 // (2i, 2i+1) inside the axis slices [t | h | w], omega_i = theta^(-2i/d_a)).
-// fp32 math; Q' and K' stored fp16 (reading A13), V stays bf16.
+// fp32 math; Q' and K' stored fp16 (reading A13), V stays bf16.  Q' is stored
+// multiplied by softmax_scale * log2(e), so the attention kernel's scores come
+// out of the tensor core already in log2 units (one FMA per score saved).
 //
 // Layout: one CTA per (token, batch element).  The token's D/2 rotation
 // angles are computed once in fp64 (sincos of p_a * omega_j) into shared
@@ -106,7 +108,8 @@ __global__ void __launch_bounds__(kThreads) prologue_kernel(const PrologueArgs a
         const float u = f[2 * i] * inv * gg[2 * i];
         const float w = f[2 * i + 1] * inv * gg[2 * i + 1];
         const float2 c = cs[li * 4 + i];
-        pk[i] = pack_half2(u * c.x - w * c.y, u * c.y + w * c.x);
+        const float sc = which == 0 ? a.q_scale : 1.f;  // Q' leaves pre-scaled by softmax_scale*log2(e)
+        pk[i] = pack_half2((u * c.x - w * c.y) * sc, (u * c.y + w * c.x) * sc);
       }
       reinterpret_cast<uint4*>(o.base)[off / 8 + li] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }

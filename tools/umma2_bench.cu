@@ -1,0 +1,154 @@
+// umma2_bench.cu -- cta_group::2 tcgen05.mma throughput (M=256 across a CTA pair).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2602_15922_b200/csrc tools/umma2_bench.cu -o tools/umma2_bench
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+
+using namespace dz;
+
+template <int MODE, bool RANDOM, bool TMEM_TRAFFIC, int COMMIT_EVERY = 0, int FENCE = 0, int ALU = 0>  // 0: SS N=128 (QK-like), 1: TS N=128 (PV-like), 2: TS+SS 8+8
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long long* cycles, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  __shared__ uint64_t bar, dummy[4], idle;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x / 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x) {
+    uint32_t x = RANDOM ? (i * 2654435761u + 12345u) : 0u;
+    // random fp16/bf16 values of magnitude ~[0.5, 2): sign and mantissa bits random, exponent fixed
+    const uint32_t m = RANDOM ? ((x & 0x83FF83FFu) | 0x3C003C00u) : 0u;
+    reinterpret_cast<uint4*>(smem_raw + (base - raw))[i] = make_uint4(m, m ^ 0x01230123u, m ^ 0x80008000u, m);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(ptx::smem_u32(&bar), 1);
+    for (int i = 0; i < 4; ++i) ptx::mbar_init(ptx::smem_u32(&dummy[i]), 1);
+    ptx::mbar_init(ptx::smem_u32(&idle), 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0) ptx::tmem_alloc_2cta<512>(ptx::smem_u32(&tbase));
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (rank == 0 && threadIdx.x == 0) {
+    constexpr uint32_t idesc_ss = ptx::idesc_f16(0, 0, 0, 0, 256, 128);
+    constexpr uint32_t idesc_ts = ptx::idesc_f16(1, 1, 0, 1, 256, 128);
+    const uint32_t a = base, b = base + 32768;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      if (FENCE & 1) ptx::tc_fence_after();
+      if (FENCE & 2) ptx::mbar_wait(ptx::smem_u32(&idle), 1);  // already-complete phase
+      if (MODE == 1 || MODE == 2) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_ts_2cta(tmem + 256, tmem + kk * 8, ptx::sdesc_sw128(b + kk * 2048, 16, 1024), idesc_ts, 1);
+      }
+      if (MODE == 0 || MODE == 2) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t qoff = (kk / 4) * 16384 + (kk % 4) * 32, koff = (kk / 4) * 8192 + (kk % 4) * 32;
+          ptx::mma_ss_2cta(tmem + 128, ptx::sdesc_sw128(a + qoff, 16, 1024), ptx::sdesc_sw128(b + koff, 16, 1024),
+                           idesc_ss, 1);
+        }
+      }
+      if (COMMIT_EVERY > 0 && (it % COMMIT_EVERY) == 0) ptx::tc_commit_2cta(ptx::smem_u32(&dummy[it & 3]), 0x3);
+    }
+    ptx::tc_commit_2cta(ptx::smem_u32(&bar), 0x3);
+    ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+    long long t1 = clock64();
+    cycles[blockIdx.x / 2] = t1 - t0;
+    *(volatile uint32_t*)&tbase = 0xFFFFFFFFu;  // stop local TMEM traffic
+  }
+  if (rank == 1 && threadIdx.x == 0) {
+    ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+    *(volatile uint32_t*)&tbase = 0xFFFFFFFFu;
+  }
+  if (ALU && warp >= 4) {  // 8 warps of softmax-like MUFU/FMA/F2FP math (issue-slot pressure)
+    float a[16];
+    for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+    uint32_t acc = 0;
+    for (int k = 0; *(volatile uint32_t*)&tbase != 0xFFFFFFFFu; ++k) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        const uint64_t x = ptx::f2_fma(ptx::f2_pack(a[i], a[i + 1]), ptx::f2_pack(0.5f, 0.5f), ptx::f2_pack(-1.f, -1.f));
+        float x0, x1;
+        ptx::f2_unpack(x, x0, x1);
+        if (ALU == 2 && (i & 2)) {
+          const uint64_t p = ptx::f2_exp2_poly(x);
+          ptx::f2_unpack(p, x0, x1);
+        } else {
+          x0 = ptx::ex2(x0);
+          x1 = ptx::ex2(x1);
+        }
+        acc += ptx::pack_bf16x2(x0, x1);
+        a[i] = x0 * 0.999f;
+        a[i + 1] = x1 * 0.999f;
+      }
+    }
+    if (acc == 0x12345) cycles[100] = acc;
+  }
+  if (TMEM_TRAFFIC && warp >= 4) {  // 8 warps: softmax-like S loads and P stores
+    const uint32_t lanes = (uint32_t)((warp % 4) * 32) << 16;
+    uint32_t r[32];
+    for (int k = 0; *(volatile uint32_t*)&tbase != 0xFFFFFFFFu; ++k) {
+      ptx::tmem_ld32(tmem + lanes + (k & 3) * 32, r);
+      ptx::tmem_wait_ld();
+      ptx::tmem_st32(tmem + lanes + 128 + ((warp / 4 - 1) * 64) + (k & 1) * 32, r);
+      ptx::tmem_wait_st();
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 0) ptx::tmem_dealloc_2cta<512>(tmem);  // tmem captured before tbase was overwritten
+}
+
+template <int MODE, bool RANDOM, bool TT, int CE = 0, int FE = 0, int AL = 0>
+void run(const char* name, double instr_per_iter) {
+  long long* d;
+  cudaMalloc(&d, 74 * sizeof(long long));
+  const int iters = 4096;
+  auto k = bench<MODE, RANDOM, TT, CE, FE, AL>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<148, 384, 100 * 1024>>>(d, 16);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k<<<148, 384, 100 * 1024>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  long long h[74];
+  cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 74; ++i) avg += h[i];
+  avg /= 74;
+  const double instrs = iters * instr_per_iter;
+  const double flop = 74.0 * instrs * 2.0 * 256 * 128 * 16;
+  printf("%-30s cyc/instr %7.2f (ideal 64)  %8.1f TFLOP/s  err=%s\n", name, avg / instrs, flop / (ms * 1e-3) / 1e12,
+         cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
+int main() {
+  run<0, false, false>("2CTA SS M256 N128 zeros", 8);
+  run<0, true, false>("2CTA SS M256 N128 random", 8);
+  run<1, true, false>("2CTA TS M256 N128 random", 8);
+  run<2, false, false>("2CTA TS+SS zeros", 16);
+  run<2, true, false>("2CTA TS+SS random", 16);
+  run<2, true, true>("2CTA TS+SS random+TMEM ld/st", 16);
+  run<0, true, false, 1>("2CTA SS + commit per 8 MMAs", 8);
+  run<2, true, false, 1>("2CTA TS+SS + commit per 16", 16);
+  run<2, true, false, 1, 1>("... + fence::after per 16", 16);
+  run<2, true, false, 1, 2>("... + mbar try_wait per 16", 16);
+  run<2, true, false, 1, 3>("... + both per 16", 16);
+  run<2, true, false, 1, 0, 1>("TS+SS + 8 warps MUFU math", 16);
+  run<2, true, false, 1, 0, 2>("TS+SS + 8 warps MUFU+poly math", 16);
+  return 0;
+}
