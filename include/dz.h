@@ -142,6 +142,27 @@ DZ_API dz_status dz_append_kv(dz_ctx* ctx, const void* k_raw, const void* v_raw,
 DZ_API dz_status dz_attend_chunk(dz_ctx* ctx, const void* q_raw, const void* k_raw, const void* v_raw,
                           const dz_span* chunk, void* out, void* stream);
 
+/* General Fig. 10 form (PAPER.md l.505 caption): the new
+ * tokens are n_spans consecutive spans (the token ranges of q_raw/k_raw/v_raw
+ * in order), each with its own chunk id and kind; spans[i].pos_thw is ignored
+ * and pos_thw holds the positions of all new tokens of this rank, int32
+ * [n_local_total][3].  Queries are the new tokens; keys are the committed
+ * chunks followed by the new tokens.  A NOISY query of chunk k sees the CLEAN
+ * keys of chunks < k and every key of its own span; a CLEAN query of chunk j
+ * sees the CLEAN keys of chunks <= j; committed chunks are CLEAN and, because
+ * every span id must exceed the last committed id (else DZ_ESTATE), visible to
+ * every query.  Examples: the training layout [C0 .. C_{M-1}; Z1 .. Z_M] of
+ * Fig. 10(a) with an empty cache; attend_chunk is the one-span case.
+ * Key tiles of 256 keys whose (query group of 256 rows, key tile) pairs are
+ * all invisible are skipped (never loaded, never multiplied); partially
+ * visible tiles are masked per element.  1 <= n_spans <= 64; the total token
+ * count must be <= max_chunk_tokens (else DZ_ECAPACITY) and a multiple of
+ * world_size.  Nothing is staged for dz_commit_staged.
+ * out: bf16 [batch][n_local_total][heads][head_dim]. */
+DZ_API dz_status dz_attend_spans(dz_ctx* ctx, const void* q_raw, const void* k_raw, const void* v_raw,
+                                 const int32_t* pos_thw, const dz_span* spans, int32_t n_spans, void* out,
+                                 void* stream);
+
 /* Commit the chunk staged by the last dz_attend_chunk (which must have had
  * kind DZ_CLEAN and this chunk_id): the model-side "attend the clean chunk,
  * then update the cache" form of Alg. 2 l.601-602.  Moves no data.  DZ_ESTATE
@@ -166,9 +187,11 @@ DZ_API dz_status dz_cache_view(const dz_ctx* ctx, int32_t b, void** k_slot0, voi
  * attend (needs DZ_FLAG_WRITE_LSE) into a caller device buffer on stream. */
 DZ_API dz_status dz_copy_lse(dz_ctx* ctx, float* dst, size_t dst_elems, void* stream);
 
-/* Tile map of the last attend as seen by the attention kernel's planner for
- * one (batch, head) unit: host uint8 [n_q_tiles][n_kv_tiles], 0 SKIP, 1
- * PARTIAL, 2 FULL (same encoding as the oracle's classifier). */
+/* Tile map of the last attend as decided by the attention kernel for (batch,
+ * head) = (0, 0): host uint8 [n_q_tiles][n_kv_tiles] with tiles of *bm = 256
+ * query rows (one CTA pair) x *bn = 256 keys (one KV step); 0 SKIP (not
+ * computed), 1 PARTIAL (masked per element), 2 FULL (unmasked) -- the
+ * encoding of the oracle's classifier.  Synchronous device read (tests). */
 DZ_API dz_status dz_get_tile_map(const dz_ctx* ctx, uint8_t* host, size_t cap, int32_t* n_q_tiles, int32_t* n_kv_tiles,
                           int32_t* bm, int32_t* bn);
 

@@ -70,6 +70,7 @@ SIGNATURES = [
     ("dz_create", I32, [ctypes.POINTER(DzConfig), ctypes.POINTER(P)]),
     ("dz_append_kv", I32, [P, P, P, ctypes.POINTER(DzSpan), P]),
     ("dz_attend_chunk", I32, [P, P, P, P, ctypes.POINTER(DzSpan), P, P]),
+    ("dz_attend_spans", I32, [P, P, P, P, P, ctypes.POINTER(DzSpan), I32, P, P]),
     ("dz_commit_staged", I32, [P, I32, P]),
     ("dz_evict_front", I32, [P, I32, P]),
     ("dz_cache_state", I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32)]),
@@ -254,6 +255,24 @@ class ChunkKVCache:
         span = self._span(chunk_id, kind, n_local, pos)
         self._check(lib().dz_attend_chunk(self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), ctypes.byref(span),
                                           out.data_ptr(), _stream_ptr(stream)), "dz_attend_chunk")
+        return out
+
+    def attend_spans(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor,
+                     spans: Sequence[Tuple[int, int, int]], out: Optional[torch.Tensor] = None,
+                     stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Fig. 10 general form: the new tokens are consecutive spans ``(chunk_id, kind, n_tokens)``
+        (global token counts); queries = new tokens, keys = committed chunks + new tokens."""
+        n_local = q.shape[1]
+        for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+            self._act(t, nm, n_local)
+        _need(pos, "pos", torch.int32, (n_local, 3), self.device)
+        if out is None:
+            out = torch.empty_like(q)
+        else:
+            self._act(out, "out", n_local)
+        arr = (DzSpan * len(spans))(*[DzSpan(int(c), int(kd), int(n), None) for c, kd, n in spans])
+        self._check(lib().dz_attend_spans(self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), pos.data_ptr(), arr,
+                                          len(spans), out.data_ptr(), _stream_ptr(stream)), "dz_attend_spans")
         return out
 
     def commit_staged(self, chunk_id: int, stream: Optional[torch.cuda.Stream] = None):

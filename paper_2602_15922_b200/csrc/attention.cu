@@ -118,6 +118,72 @@ __device__ __forceinline__ void exp_half(const float* s, uint64_t nb2, uint32_t 
   }
 }
 
+// ------------------------------------------------ Fig. 10 visibility (spans) --
+// Every role of the kernel (TMA producer, both MMA issuers, softmax warps)
+// evaluates the same pure functions below, so they agree on which steps run
+// without exchanging anything.
+constexpr uint8_t kSkip = 0, kPartial = 1, kFull = 2;  // oracle tile_map encoding
+
+__device__ __forceinline__ bool span_vis(const SpanTable& st, int qs, int ks) {
+  return qs == ks || st.kc[ks] < st.qth[qs];
+}
+// first span whose range ends after token x (x < start[n])
+__device__ __forceinline__ int span_at(const SpanTable& st, int x) {
+  int i = 0;
+  while (i + 1 < st.n && st.start[i + 1] <= x) ++i;
+  return i;
+}
+// Class of the (256-row query group g, 256-key step j) tile: SKIP if no
+// (query, key) pair in it is visible, FULL if all are visible and in bounds,
+// else PARTIAL.  Visibility is constant over a (query span, key span) pair, so
+// the tile's class follows from the spans overlapping its row and key ranges.
+__device__ uint8_t step_class(const SpanTable& st, int g, int j, int nq, int kv_len) {
+  const int r0 = g * kTileQ, r1 = min(r0 + kTileQ, nq);
+  const int k0 = j * kTileK, k1 = min(k0 + kTileK, kv_len);
+  bool any = k0 < st.valid;  // committed keys are visible to every query
+  bool all = (r1 - r0 == kTileQ) && (k1 - k0 == kTileK);
+  if (st.n == 1) return (any || k1 > st.valid) ? (all ? kFull : kPartial) : kSkip;
+  if (k1 > st.valid) {
+    const int ka = max(k0, st.valid) - st.valid, kb = k1 - st.valid;
+    const int ks0 = span_at(st, ka);
+    for (int qs = span_at(st, r0); qs < st.n && st.start[qs] < r1; ++qs)
+      for (int ks = ks0; ks < st.n && st.start[ks] < kb; ++ks) {
+        const bool v = span_vis(st, qs, ks);
+        any |= v;
+        all &= v;
+      }
+  }
+  return !any ? kSkip : (all ? kFull : kPartial);
+}
+// set bits [lo, hi) of a 128-bit mask
+__device__ __forceinline__ void set_bits(uint32_t (&m)[4], int lo, int hi) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int a = min(max(lo - 32 * w, 0), 32), b = min(max(hi - 32 * w, 0), 32);
+    if (b > a) m[w] |= (b == 32 ? 0xffffffffu : ((1u << b) - 1u)) & ~((a == 32) ? 0xffffffffu : ((1u << a) - 1u));
+  }
+}
+// Visible-key mask of query span qs over keys [kb0, kb0 + 128) of the key sequence.
+__device__ void visible_bits(const SpanTable& st, int qs, int kb0, int kv_len, uint32_t (&m)[4]) {
+  m[0] = m[1] = m[2] = m[3] = 0u;
+  const int kend = min(kb0 + 128, kv_len);
+  set_bits(m, 0, min(st.valid, kend) - kb0);  // committed part
+  if (kend <= st.valid) return;
+  const int ka = max(kb0, st.valid) - st.valid, kb = kend - st.valid;
+  for (int ks = span_at(st, ka); ks < st.n && st.start[ks] < kb; ++ks)
+    if (span_vis(st, qs, ks))
+      set_bits(m, max(st.start[ks], ka) + st.valid - kb0, min(st.start[ks + 1], kb) + st.valid - kb0);
+}
+// first and last non-SKIP step of query group g (every group has one: a query sees its own span)
+__device__ __forceinline__ void active_range(const SpanTable& st, int g, int nq, int kv_len, int nkv, int& jf,
+                                             int& jl) {
+  jf = 0;
+  jl = nkv - 1;
+  if (st.n == 1) return;
+  while (jf < nkv - 1 && step_class(st, g, jf, nq, kv_len) == kSkip) ++jf;
+  while (jl > jf && step_class(st, g, jl, nq, kv_len) == kSkip) --jl;
+}
+
 __device__ __forceinline__ void decode_unit(int u, int n_groups, int H, int& b, int& h, int& g) {
   g = u % n_groups;
   const int bh = u / n_groups;
@@ -130,7 +196,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ out, int64_t o_bstride,
                     int64_t o_tstride, float* __restrict__ lse, uint8_t* __restrict__ tile_map, int B, int H,
-                    int nq, int kv_len, float scale_log2, float m_static, int dbg) {
+                    int nq, int kv_len, float scale_log2, float m_static, int dbg,
+                    const __grid_constant__ SpanTable st) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
@@ -149,7 +216,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int n_groups = (n_qtiles + 1) / 2;                 // 2 query tiles per cluster unit
   const int n_units = B * H * n_groups;
   const int nkv = (kv_len + BN - 1) / BN;                  // 256-key steps
-  const int nkv128 = (kv_len + 127) / 128;                 // 128-key tiles (tile-map granularity)
   const int cid = (int)ptx::cluster_id_x(), ncl = (int)ptx::nclusters_x();
   const bool trace_on = g_dz_trace_on != 0 && cid == 0;
   uint32_t* const trace = g_dz_trace + rank * kTraceSteps * 16;
@@ -210,6 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * 64, h, qt * BM, b, pol_q);
       }
       for (int j = 0; j < nkv; ++j) {
+        if (step_class(st, g, j, nq, kv_len) == kSkip) continue;
         for (int kv = 0; kv < 2; ++kv, ++ld) {  // K_j half (128 keys x D), then V_j half (256 keys x D/2)
           uint32_t st, ph;
           slot(ld, st, ph);
@@ -244,78 +311,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // release their own K / V stages, so their streams need no mutual order.
     const bool do_qk = warp == kWarpMma;
     uint32_t q_phase = 0, sf_phase = 0, pf_phase = 0, oe_phase = 0;
-    const int my_units = cid < n_units ? (n_units - cid + ncl - 1) / ncl : 0;
-    const int G = my_units * nkv;
-    for (int gs = 0; gs <= G; ++gs) {
-      const int j = gs % nkv;
-      const bool tr = trace_on && gs < kTraceSteps && gs < nkv && lane == 0;
-      if (do_qk && gs < G) {
-        if (j == 0) {  // first step of a new unit: its Q tiles
-          ptx::mbar_wait(bar(bars->q_full), q_phase);
-          q_phase ^= 1;
-        }
-        uint32_t k_st, k_ph;
-        slot(2 * gs, k_st, k_ph);
-        ptx::mbar_wait(bar(bars->kv_full[k_st]), k_ph);
-        // S in two halves of 128 keys (N = 128 each): the half-hh softmax warps release
-        // their half as soon as they hold it, so each QK half waits only for the copy
-        // of the same half of the previous step
-        for (int hh = 0; hh < 2; ++hh) {
-          if (tr && hh == 0) trace[j * 8 + 0] = (uint32_t)clock();
-          if (gs > 0) {
-            ptx::mbar_wait(bar(bars->s_free[hh]), sf_phase);
-            if (hh == 1) sf_phase ^= 1;
+    int gs = 0;  // this issuer's running count of executed (non-SKIP) steps
+    for (int u = cid; u < n_units; u += ncl) {
+      int b, h, g;
+      decode_unit(u, n_groups, H, b, h, g);
+      int jf, jl;
+      active_range(st, g, nq, kv_len, nkv, jf, jl);
+      for (int j = jf; j <= jl; ++j) {
+        if (j > jf && j < jl && step_class(st, g, j, nq, kv_len) == kSkip) continue;
+        const bool tr = trace_on && u == cid && j < kTraceSteps && lane == 0;
+        if (do_qk) {
+          if (j == jf) {  // first step of a new unit: its Q tiles
+            ptx::mbar_wait(bar(bars->q_full), q_phase);
+            q_phase ^= 1;
           }
-          if (tr && hh == 0) trace[j * 8 + 1] = (uint32_t)clock();
+          uint32_t k_st, k_ph;
+          slot(2 * gs, k_st, k_ph);
+          ptx::mbar_wait(bar(bars->kv_full[k_st]), k_ph);
+          // S in two halves of 128 keys (N = 128 each): the half-hh softmax warps release
+          // their half as soon as they hold it, so each QK half waits only for the copy
+          // of the same half of the previous step
+          for (int hh = 0; hh < 2; ++hh) {
+            if (tr && hh == 0) trace[j * 8 + 0] = (uint32_t)clock();
+            if (gs > 0) {
+              ptx::mbar_wait(bar(bars->s_free[hh]), sf_phase);
+              if (hh == 1) sf_phase ^= 1;
+            }
+            if (tr && hh == 0) trace[j * 8 + 1] = (uint32_t)clock();
+            ptx::tc_fence_after();
+            if (lane == 0) {
+              const uint32_t ka = sKV + k_st * C::kStageBytes + hh * C::kQBoxes * 64 * 128;
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t qoff = (kk / 4) * (128 * 128) + (kk % 4) * 32;  // Q: 128 rows per box
+                const uint32_t koff = (kk / 4) * (64 * 128) + (kk % 4) * 32;   // K half: 64 rows per box
+                ptx::mma_ss_2cta(tmem + kColS + hh * 128, ptx::sdesc_sw128(sQ + qoff, 16, 1024),
+                                 ptx::sdesc_sw128(ka + koff, 16, 1024), C::kIdescQK, kk > 0);
+                if (tr && j == 9) trace[kTraceSteps * 8 + hh * 8 + kk] = (uint32_t)clock();
+              }
+              ptx::tc_commit_2cta(bar(bars->s_full[hh]), kBoth);
+              if (hh == 1) {
+                ptx::tc_commit_2cta(bar(bars->kv_empty[k_st]), kBoth);
+                if (j == jl) ptx::tc_commit_2cta(bar(bars->q_empty), kBoth);
+              }
+            }
+            __syncwarp();
+          }
+        } else {
+          uint32_t v_st, v_ph;
+          slot(2 * gs + 1, v_st, v_ph);
+          ptx::mbar_wait(bar(bars->kv_full[v_st]), v_ph);
+          if (tr) trace[j * 8 + 2] = (uint32_t)clock();
+          ptx::mbar_wait(bar(bars->p_full), pf_phase);
+          pf_phase ^= 1;
+          if (j == jf) {  // the previous unit's epilogue has read O
+            ptx::mbar_wait(bar(bars->o_empty), oe_phase ^ 1);
+            oe_phase ^= 1;
+          }
+          if (tr) trace[j * 8 + 3] = (uint32_t)clock();
           ptx::tc_fence_after();
           if (lane == 0) {
-            const uint32_t ka = sKV + k_st * C::kStageBytes + hh * C::kQBoxes * 64 * 128;
+            const uint32_t va = sKV + v_st * C::kStageBytes;
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t qoff = (kk / 4) * (128 * 128) + (kk % 4) * 32;  // Q: 128 rows per box
-              const uint32_t koff = (kk / 4) * (64 * 128) + (kk % 4) * 32;   // K half: 64 rows per box
-              ptx::mma_ss_2cta(tmem + kColS + hh * 128, ptx::sdesc_sw128(sQ + qoff, 16, 1024),
-                               ptx::sdesc_sw128(ka + koff, 16, 1024), C::kIdescQK, kk > 0);
-              if (tr && j == 9) trace[kTraceSteps * 8 + hh * 8 + kk] = (uint32_t)clock();
+            for (int kk = 0; kk < BN / 16; ++kk) {
+              const uint64_t bd = D == 128 ? ptx::sdesc_sw128(va + kk * 16 * C::kVRowBytes, 16, 1024)
+                                           : ptx::sdesc_sw64(va + kk * 16 * C::kVRowBytes, 16, 512);
+              ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + kk * 8, bd, C::kIdescPV,
+                               (j > jf || kk > 0) ? 1u : 0u);
+              if (tr && j == 9) trace[kTraceSteps * 8 + 16 + kk] = (uint32_t)clock();
             }
-            ptx::tc_commit_2cta(bar(bars->s_full[hh]), kBoth);
-            if (hh == 1) {
-              ptx::tc_commit_2cta(bar(bars->kv_empty[k_st]), kBoth);
-              if (j == nkv - 1) ptx::tc_commit_2cta(bar(bars->q_empty), kBoth);
-            }
+            ptx::tc_commit_2cta(bar(bars->p_empty), kBoth);              // P may be overwritten
+            if (j == jl) ptx::tc_commit_2cta(bar(bars->o_full), kBoth);
+            ptx::tc_commit_2cta(bar(bars->kv_empty[v_st]), kBoth);
           }
           __syncwarp();
         }
-      }
-      if (!do_qk && gs > 0) {
-        const int jp = (gs - 1) % nkv;
-        const bool trp = trace_on && gs - 1 < nkv && lane == 0;
-        uint32_t v_st, v_ph;
-        slot(2 * (gs - 1) + 1, v_st, v_ph);
-        ptx::mbar_wait(bar(bars->kv_full[v_st]), v_ph);
-        if (trp) trace[jp * 8 + 2] = (uint32_t)clock();
-        ptx::mbar_wait(bar(bars->p_full), pf_phase);
-        pf_phase ^= 1;
-        if (jp == 0) {  // the previous unit's epilogue has read O
-          ptx::mbar_wait(bar(bars->o_empty), oe_phase ^ 1);
-          oe_phase ^= 1;
-        }
-        if (trp) trace[jp * 8 + 3] = (uint32_t)clock();
-        ptx::tc_fence_after();
-        if (lane == 0) {
-          const uint32_t va = sKV + v_st * C::kStageBytes;
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            const uint64_t bd = D == 128 ? ptx::sdesc_sw128(va + kk * 16 * C::kVRowBytes, 16, 1024)
-                                         : ptx::sdesc_sw64(va + kk * 16 * C::kVRowBytes, 16, 512);
-            ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + kk * 8, bd, C::kIdescPV, (jp > 0 || kk > 0) ? 1u : 0u);
-            if (trp && jp == 9) trace[kTraceSteps * 8 + 16 + kk] = (uint32_t)clock();
-          }
-          ptx::tc_commit_2cta(bar(bars->p_empty), kBoth);              // P may be overwritten
-          if (jp == nkv - 1) ptx::tc_commit_2cta(bar(bars->o_full), kBoth);
-          ptx::tc_commit_2cta(bar(bars->kv_empty[v_st]), kBoth);
-        }
-        __syncwarp();
+        ++gs;
       }
     }
   }
@@ -337,7 +408,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int qt = 2 * g + (int)rank;
       float m_used = m_static > 0.f ? 0.f : -INFINITY;  // softmax base, log2 units (fixed base: 0)
       float l = 0.f;                                          // partial row sum over this warp's keys
-      for (int j = 0; j < nkv; ++j) {
+      const int s_row = qt * BM + row;                        // this thread's query (row of the new tokens)
+      const int qs = st.n == 1 ? 0 : span_at(st, min(s_row, nq - 1));  // its span (rows past nq: never stored)
+      int jf, jl;
+      active_range(st, g, nq, kv_len, nkv, jf, jl);
+      for (int j = jf; j <= jl; ++j) {
+        const uint8_t cls = step_class(st, g, j, nq, kv_len);
+        if (tile_map != nullptr && u < n_groups && rank == 0 && row == 0 && hc == 0)
+          for (int jj = (j == jf ? 0 : j); jj <= (j == jl ? nkv - 1 : j); ++jj)  // incl. skipped steps
+            tile_map[g * nkv + jj] = jj == j ? cls : step_class(st, g, jj, nq, kv_len);
+        if (cls == kSkip) continue;
         ptx::mbar_wait(bar(bars->s_full[hc]), s_phase);
         s_phase ^= 1;
         const bool tr = trace_on && u == cid && j < kTraceSteps && row == 0 && hc == 0;
@@ -362,15 +442,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->s_free[hc]));
         if (tr) trace[j * 8 + 6] = (uint32_t)clock();
-        const int kt = 2 * j + hc;                  // this warp's 128-key tile
-        const int kv_valid = kv_len - kt * 128;     // valid keys among its 128 columns
-        if (tile_map != nullptr && u < n_groups && row == 0 && qt < n_qtiles && kt < nkv128)
-          // debug: the kernel's own per-tile decision for (b, h) = (0, 0): 2 FULL, 1 PARTIAL
-          tile_map[qt * nkv128 + kt] = (kv_valid >= 128 && nq - qt * BM >= BM) ? 2 : 1;
-        if (kv_valid < 128) {
+        if (cls == kPartial) {  // Fig. 10 mask and key bounds for this warp's 128 keys
+          uint32_t vm[4];
+          visible_bits(st, qs, j * BN + 128 * hc, kv_len, vm);
 #pragma unroll
           for (int i = 0; i < 128; ++i)
-            if (i >= kv_valid) s[i] = -INFINITY;
+            if (!((vm[i / 32] >> (i % 32)) & 1u)) s[i] = -INFINITY;
         }
         const bool online = m_static <= 0.f;
         if (online) {
@@ -387,7 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mx = fmaxf(mx, red[(hc ^ 1) * BM + row]);
           ptx::named_bar_sync(pair_bar, 64);  // both read before the next exchange
           const bool grow = mx > m_used + kRescaleLog2;
-          const bool rescale = grow && j > 0 && m_used != -INFINITY;
+          const bool rescale = grow && j > jf && m_used != -INFINITY;
           if (__any_sync(0xffffffffu, rescale)) {
             ptx::mbar_wait(bar(bars->p_empty), pe_phase ^ 1);  // PV(j-1) done
             ptx::tc_fence_after();
@@ -411,7 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // offset nor a clamp is needed; online base: p = 2^(s - m).
         const float nbase = (!online || m_used == -INFINITY) ? 0.f : -m_used;
         const uint64_t nb2 = ptx::f2_pack(nbase, nbase);
-        const bool plain = !online && kv_valid >= 128;
+        const bool plain = !online && cls == kFull;
         __syncwarp();
         uint64_t acc[4] = {0, 0, 0, 0};
         // two halves of 64 keys: exponentials of half h, then its P store (the first store
@@ -498,7 +575,7 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   k<<<a.grid, kThreads, C::kSmem, s>>>(a.tm_q, a.tm_k, a.tm_v, static_cast<__nv_bfloat16*>(a.out), a.o_bstride,
                                        a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq, a.kv_len, a.scale_log2,
-                                       a.m_static, a.debug_flags);
+                                       a.m_static, a.debug_flags, a.spans);
   return cudaGetLastError();
 }
 

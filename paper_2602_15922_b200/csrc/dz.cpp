@@ -51,6 +51,13 @@ bool basic_cfg_ok(const dz_config* c) {
   return s == c->head_dim;
 }
 
+// debug tile map: [query groups of kTileQ rows][key steps of kTileK keys]
+size_t map_bytes(const dz_config* c) {
+  const int64_t mc = c->max_chunk_tokens;
+  const int64_t keys = c->cache_capacity_tokens + mc + c->window_slack_tokens;
+  return 256 + (size_t)((mc + dz::kTileQ - 1) / dz::kTileQ) * ((keys + dz::kTileK - 1) / dz::kTileK);
+}
+
 Layout make_layout(const dz_config* c) {
   Layout L;
   const int64_t B = c->batch, Hl = c->heads / c->world_size, D = c->head_dim, N = c->world_size;
@@ -66,7 +73,7 @@ Layout make_layout(const dz_config* c) {
   L.v_off = take((size_t)B * L.slots * Hl * D * 2);
   L.q_off = take((size_t)B * mc * Hl * D * 2);                       // Q' fp16
   L.lse_off = take((c->flags & DZ_FLAG_WRITE_LSE) ? (size_t)B * Hl * mc * 4 : 0);
-  L.map_off = take(4096 + (size_t)((mc + 127) / 128) * ((c->cache_capacity_tokens + mc + 127) / 128));
+  L.map_off = take(map_bytes(c));
   if (N > 1) {
     const size_t sb = (size_t)B * (mc / N) * c->heads * D * 2;       // [N][B][n_loc][Hl][D]
     L.sq_off = take(sb);
@@ -248,22 +255,23 @@ dz_status ensure_staging_room(dz_ctx* c, cudaStream_t st) {
   return DZ_OK;
 }
 
-void fill_prologue_common(dz_ctx* c, dz::PrologueArgs& a, const dz_span* s, int64_t n_loc) {
+void fill_prologue_common(dz_ctx* c, dz::PrologueArgs& a, const int32_t* pos, int64_t n_loc) {
   a = c->pro;
   a.B = c->B;
   a.n = (int32_t)n_loc;
   a.H = c->H;
   a.D = c->D;
   a.x_bstride = n_loc * c->H * c->D;
-  a.pos = s->pos_thw;
+  a.pos = pos;
 }
 
 // K1 prologue for the current chunk: Q' and the chunk's K'/V, written either
 // straight into the staging slot (N == 1) or into the all-to-all send layout.
-dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, const dz_span* s, cudaStream_t st) {
-  const int64_t n = s->n_tokens, n_loc = n / c->N;
+dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, const int32_t* pos, int64_t n,
+                       cudaStream_t st) {
+  const int64_t n_loc = n / c->N;
   dz::PrologueArgs a;
-  fill_prologue_common(c, a, s, n_loc);
+  fill_prologue_common(c, a, pos, n_loc);
   a.q_scale = c->scale * 1.4426950408889634f;  // scores leave the QK MMA in log2 units
   a.x[0] = q;
   a.x[1] = k;
@@ -319,9 +327,11 @@ dz_status exchange_post(dz_ctx* c, int64_t n, cudaStream_t st) {
 }
 
 // K2 over local heads and the full sequence: committed slots + the staged chunk.
-dz_status run_attention(dz_ctx* c, int64_t n, void* out_local, int64_t o_bstride, int64_t o_tstride,
-                        cudaStream_t st) {
+dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* out_local, int64_t o_bstride,
+                        int64_t o_tstride, cudaStream_t st) {
   dz::AttnArgs a;
+  a.spans = spans;
+  a.spans.valid = (int32_t)c->valid;
   const int64_t kv_len = c->valid + n;
   const int64_t bs = c->L.slots * c->Hl * c->D;
   // Q: 128-row tiles per CTA; K: each CTA of a pair loads 2 x 64 of a step's 256 keys;
@@ -344,13 +354,11 @@ dz_status run_attention(dz_ctx* c, int64_t n, void* out_local, int64_t o_bstride
   if (const char* e = getenv("DZ_DEBUG_KERNEL")) a.debug_flags = atoi(e);  // diagnostics: results are garbage
   const int units = dz::attention_units(c->B, c->Hl, (int32_t)n);  // CTA-pair units
   a.grid = 2 * std::min(units, c->num_sms / 2);                      // persistent: one CTA pair per TPC
-  const int nqt = (int)((n + 127) / 128), nkt = (int)((kv_len + 127) / 128);
-  const size_t map_cap = 4096 + (size_t)((c->cfg.max_chunk_tokens + 127) / 128) *
-                                    ((c->cfg.cache_capacity_tokens + c->cfg.max_chunk_tokens + 127) / 128);
-  if ((size_t)nqt * nkt <= map_cap) {
+  const int ngr = (int)((n + dz::kTileQ - 1) / dz::kTileQ), nst = (int)((kv_len + dz::kTileK - 1) / dz::kTileK);
+  if ((size_t)ngr * nst <= map_bytes(&c->cfg)) {
     a.tile_map = reinterpret_cast<uint8_t*>(c->base + c->L.map_off);
-    c->last_nq_tiles = nqt;
-    c->last_nkv_tiles = nkt;
+    c->last_nq_tiles = ngr;
+    c->last_nkv_tiles = nst;
     c->have_map = true;
   }
   c->last_nq = (int32_t)n;
@@ -440,7 +448,7 @@ dz_status dz_append_kv(dz_ctx* c, const void* k_raw, const void* v_raw, const dz
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool prof = c->ev_app[0] != nullptr;
   if (prof) cudaEventRecord(c->ev_app[0], st);
-  if ((r = run_prologue(c, nullptr, k_raw, v_raw, s, st))) return r;
+  if ((r = run_prologue(c, nullptr, k_raw, v_raw, s->pos_thw, s->n_tokens, st))) return r;
   if (c->N > 1 && (r = exchange_pre(c, false, s->n_tokens, st))) return r;
   if (prof) cudaEventRecord(c->ev_app[1], st);
   c->have_append_ev = prof;
@@ -451,30 +459,30 @@ dz_status dz_append_kv(dz_ctx* c, const void* k_raw, const void* v_raw, const dz
   return ensure_staging_room(c, st);
 }
 
-dz_status dz_attend_chunk(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const dz_span* s,
-                          void* out, void* stream) {
-  dz_status r = check_ready(c);
-  if (r) return r;
-  if (!q_raw || !k_raw || !v_raw || !out) return fail(c, DZ_EINVAL, "null q/k/v/out");
-  if (!aligned16(q_raw) || !aligned16(k_raw) || !aligned16(v_raw) || !aligned16(out))
-    return fail(c, DZ_EINVAL, "q/k/v/out must be 16-byte aligned");
-  if ((r = check_span(c, s))) return r;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t n = s->n_tokens;
+}  // extern "C"
+
+namespace {
+
+// One attention call (K1 prologue [+ exchange] + K2 [+ exchange + unpack]) over
+// n new tokens described by `spans`; keys = committed chunks + the new tokens.
+dz_status attend_impl(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const int32_t* pos,
+                      int64_t n, const dz::SpanTable& spans, void* out, cudaStream_t st) {
+  dz_status r;
   c->staged = false;
   const bool prof = c->ev[0] != nullptr;
   auto mark = [&](int i) { if (prof) cudaEventRecord(c->ev[i], st); };
   mark(0);
-  if ((r = run_prologue(c, q_raw, k_raw, v_raw, s, st))) return r;
+  if ((r = run_prologue(c, q_raw, k_raw, v_raw, pos, n, st))) return r;
   mark(1);
   if (c->N == 1) {
     mark(2);
-    if ((r = run_attention(c, n, out, n * c->H * c->D, (int64_t)c->H * c->D, st))) return r;
+    if ((r = run_attention(c, n, spans, out, n * c->H * c->D, (int64_t)c->H * c->D, st))) return r;
     mark(3);
   } else {
     if ((r = exchange_pre(c, true, n, st))) return r;
     mark(2);
-    if ((r = run_attention(c, n, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, st))) return r;
+    if ((r = run_attention(c, n, spans, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, st)))
+      return r;
     mark(3);
     if ((r = exchange_post(c, n, st))) return r;
     if ((r = cuda_check(c, dz::launch_sp_unpack(c->base + c->L.or_off, out, c->N, c->B, (int32_t)(n / c->N), c->Hl,
@@ -484,11 +492,71 @@ dz_status dz_attend_chunk(dz_ctx* c, const void* q_raw, const void* k_raw, const
   }
   mark(4);
   c->have_attend_ev = prof;
+  return DZ_OK;
+}
+
+dz_status check_attend_ptrs(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const void* out) {
+  if (!q_raw || !k_raw || !v_raw || !out) return fail(c, DZ_EINVAL, "null q/k/v/out");
+  if (!aligned16(q_raw) || !aligned16(k_raw) || !aligned16(v_raw) || !aligned16(out))
+    return fail(c, DZ_EINVAL, "q/k/v/out must be 16-byte aligned");
+  return DZ_OK;
+}
+
+// span table entry i (Fig. 10 rule, R3)
+void set_span(dz::SpanTable& t, int i, int32_t chunk_id, int32_t kind, int32_t start, int32_t n) {
+  t.start[i] = start;
+  t.start[i + 1] = start + n;
+  t.kc[i] = kind == DZ_CLEAN ? chunk_id : INT32_MAX;
+  t.qth[i] = kind == DZ_NOISY ? chunk_id : chunk_id + 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+dz_status dz_attend_chunk(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const dz_span* s,
+                          void* out, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if ((r = check_attend_ptrs(c, q_raw, k_raw, v_raw, out))) return r;
+  if ((r = check_span(c, s))) return r;
+  dz::SpanTable t;
+  t.n = 1;
+  set_span(t, 0, s->chunk_id, s->kind, 0, s->n_tokens);
+  if ((r = attend_impl(c, q_raw, k_raw, v_raw, s->pos_thw, s->n_tokens, t, out, static_cast<cudaStream_t>(stream))))
+    return r;
   c->staged = true;
   c->staged_id = s->chunk_id;
   c->staged_kind = s->kind;
-  c->staged_n = n;
+  c->staged_n = s->n_tokens;
   return DZ_OK;
+}
+
+dz_status dz_attend_spans(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const int32_t* pos_thw,
+                          const dz_span* spans, int32_t n_spans, void* out, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if ((r = check_attend_ptrs(c, q_raw, k_raw, v_raw, out))) return r;
+  if (!pos_thw || !spans) return fail(c, DZ_EINVAL, "null positions or spans");
+  if (n_spans <= 0 || n_spans > dz::kMaxSpans)
+    return fail(c, DZ_EINVAL, "n_spans %d outside [1, %d]", n_spans, dz::kMaxSpans);
+  dz::SpanTable t;
+  t.n = n_spans;
+  int64_t n = 0;
+  for (int i = 0; i < n_spans; ++i) {
+    const dz_span& s = spans[i];
+    if (s.kind != DZ_CLEAN && s.kind != DZ_NOISY) return fail(c, DZ_EINVAL, "span %d: bad kind %d", i, s.kind);
+    if (s.n_tokens <= 0) return fail(c, DZ_ESHAPE, "span %d: n_tokens %d must be positive", i, s.n_tokens);
+    if (s.chunk_id <= c->last_id || s.chunk_id == INT32_MAX)
+      return fail(c, DZ_ESTATE, "span %d: chunk id %d must exceed the last committed id %d", i, s.chunk_id,
+                  c->last_id);
+    set_span(t, i, s.chunk_id, s.kind, (int32_t)n, s.n_tokens);
+    n += s.n_tokens;
+  }
+  if (n % c->N) return fail(c, DZ_ESHAPE, "%lld tokens not a multiple of world_size %d", (long long)n, c->N);
+  if (n > c->cfg.max_chunk_tokens)
+    return fail(c, DZ_ECAPACITY, "%lld span tokens exceed max_chunk_tokens %d", (long long)n, c->cfg.max_chunk_tokens);
+  return attend_impl(c, q_raw, k_raw, v_raw, pos_thw, n, t, out, static_cast<cudaStream_t>(stream));
 }
 
 dz_status dz_commit_staged(dz_ctx* c, int32_t chunk_id, void* stream) {
@@ -554,8 +622,8 @@ dz_status dz_get_tile_map(const dz_ctx* c, uint8_t* host, size_t cap, int32_t* n
   const size_t need = (size_t)c->last_nq_tiles * c->last_nkv_tiles;
   if (nq) *nq = c->last_nq_tiles;
   if (nk) *nk = c->last_nkv_tiles;
-  if (bm) *bm = 128;
-  if (bn) *bn = 128;
+  if (bm) *bm = dz::kTileQ;
+  if (bn) *bn = dz::kTileK;
   if (!host) return DZ_OK;
   if (cap < need) return DZ_EINVAL;
   // synchronous device read of the kernel-written debug map (tests only)

@@ -33,14 +33,31 @@ struct PrologueArgs {
 cudaError_t launch_prologue(const PrologueArgs& a, cudaStream_t s);
 
 // ---- K2: block-causal flash attention (tcgen05 + TMEM + TMA) --------------
+// Fig. 10 visibility in span form (R3).  Queries are
+// the nq new tokens, split into n spans [start[i], start[i+1]); keys are the
+// `valid` committed tokens (visible to every query: every span id exceeds the
+// last committed id) followed by the same nq new tokens.  A query of span qs
+// sees a new key of span ks iff qs == ks (own span, bidirectional) or
+// kc[ks] < qth[qs] (kc: the key span's chunk id if CLEAN, else INT32_MAX; qth:
+// the query span's chunk id if NOISY, chunk id + 1 if CLEAN).
+constexpr int kMaxSpans = 64;
+struct SpanTable {
+  int32_t n = 1;
+  int32_t valid = 0;
+  int32_t start[kMaxSpans + 1] = {};
+  int32_t kc[kMaxSpans] = {};
+  int32_t qth[kMaxSpans] = {};
+};
+
 struct AttnArgs {
+  SpanTable spans;
   CUtensorMap tm_q;   // Q' fp16, dims (D, H, nq, B), box (64, 1, 128, 1), SW128
   CUtensorMap tm_k;   // K' fp16 cache, dims (D, H, kv_len, B)
   CUtensorMap tm_v;   // V  bf16 cache, dims (D, H, kv_len, B)
   void* out = nullptr;            // bf16, row (b, s, h) at out + b*o_bstride + s*o_tstride + h*D
   int64_t o_bstride = 0, o_tstride = 0;
   float* lse = nullptr;           // optional fp32 [B][H][nq] natural-log LSE
-  uint8_t* tile_map = nullptr;    // optional debug [n_q_tiles][n_kv_tiles] for (b, h) = (0, 0)
+  uint8_t* tile_map = nullptr;    // optional debug [n_groups][n_steps] (256 x 256 tiles) for (b, h) = (0, 0)
   int32_t B = 0, H = 0, D = 0, nq = 0, kv_len = 0;
   float scale_log2 = 0.f;         // unused by the kernel: Q' is pre-scaled by softmax_scale * log2(e)
   float m_static = 0.f;           // > 0: fixed softmax base (log2 units) bounding every logit; 0: online max
@@ -49,6 +66,7 @@ struct AttnArgs {
 };
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);
 int attention_units(int32_t B, int32_t H, int32_t nq);
+constexpr int kTileQ = 256, kTileK = 256;  // skip / mask decision granularity (query rows of a CTA pair x keys of a step)
 cudaError_t read_watchdog(uint32_t* host8);   // {fired, block, warp, bar addr, parity, smid, bars base, 0}
 cudaError_t reset_watchdog();
 cudaError_t trace_control(int enable, uint32_t* host, size_t n);  // K2 cycle trace (CTA 0, first unit)  // work units (b, h, q-tile pair)

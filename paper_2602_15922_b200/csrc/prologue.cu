@@ -9,12 +9,14 @@
 // multiplied by softmax_scale * log2(e), so the attention kernel's scores come
 // out of the tensor core already in log2 units (one FMA per score saved).
 //
-// Layout: one CTA per (token, batch element).  The token's D/2 rotation
-// angles are computed once in fp64 (sincos of p_a * omega_j) into shared
-// memory and reused by all 2H (Q, K) rows.  A row is handled by D/8 threads
-// with one 16-byte load and one 16-byte store each; the row's sum of squares
-// is reduced with __shfl_xor inside that thread group.  HBM-bound by design:
-// per token it moves (read + write) 2 B x D x H for each of Q, K, V.
+// Layout: one CTA per (token, batch element).  Every thread first issues
+// all of its 16-byte loads for the token (up to kVecPerThread in flight), and
+// only then do two warps compute the token's D/2 rotation angles (fp64 sincos
+// of p_a * omega_j) into shared memory, so the angle latency hides under the
+// HBM latency instead of preceding it.  A row is handled by D/8 threads with
+// one 16-byte load and one 16-byte store each; the row's sum of squares is
+// reduced with __shfl_xor inside that thread group.  HBM-bound by design: per
+// token it moves (read + write) 2 B x D x H for each of Q, K, V.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -27,7 +29,7 @@ namespace dz {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kRowsInFlight = 4;
+constexpr int kVecPerThread = 8;   // 16-byte loads in flight per thread: 3 H D / 8 <= 2048 vectors per token
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -36,6 +38,15 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
     f[2 * i] = __uint_as_float(w[i] << 16);
     f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
   }
+}
+
+// read-once activations: non-coherent path, no L1 allocation
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
 }
 
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
@@ -51,34 +62,35 @@ __global__ void __launch_bounds__(kThreads) prologue_kernel(const PrologueArgs a
   const int t = blockIdx.x;
   const int b = blockIdx.y;
   const int tid = threadIdx.x;
-  if (tid < D / 2) {
-    const double p = (double)__ldg(a.pos + 3 * t + a.axis[tid]);
-    double sn, cn;
-    sincos(p * a.omega[tid], &sn, &cn);
-    cs[tid] = make_float2((float)cn, (float)sn);
-  }
-  __syncthreads();
-
   const int g = tid / G;               // row group
   const int li = tid % G;              // 8-element slice index inside the row
   const int H = a.H;
   const int n_rows = 3 * H;            // (q rows, k rows, v rows) of this token
   const int64_t xrow0 = (int64_t)b * a.x_bstride + (int64_t)t * H * D;
 
-  for (int r0 = 0; r0 < n_rows; r0 += kGroups * kRowsInFlight) {  // warp-uniform trip count
-    uint4 in[kRowsInFlight];
+  for (int r0 = 0; r0 < n_rows; r0 += kGroups * kVecPerThread) {  // one trip for H <= 85 at D = 128
+    uint4 in[kVecPerThread];
 #pragma unroll
-    for (int k = 0; k < kRowsInFlight; ++k) {
+    for (int k = 0; k < kVecPerThread; ++k) {
       const int r = r0 + g + k * kGroups;
       in[k] = make_uint4(0, 0, 0, 0);
       if (r < n_rows) {
         const int which = r / H, h = r % H;
         const uint4* src = reinterpret_cast<const uint4*>(a.x[which]);
-        if (src) in[k] = __ldg(src + (xrow0 + (int64_t)h * D) / 8 + li);
+        if (src) in[k] = ld_stream(src + (xrow0 + (int64_t)h * D) / 8 + li);
       }
     }
+    if (r0 == 0) {  // angles while the loads are in flight
+      if (tid < D / 2) {
+        const double p = (double)__ldg(a.pos + 3 * t + a.axis[tid]);
+        double sn, cn;
+        sincos(p * a.omega[tid], &sn, &cn);
+        cs[tid] = make_float2((float)cn, (float)sn);
+      }
+      __syncthreads();
+    }
 #pragma unroll
-    for (int k = 0; k < kRowsInFlight; ++k) {
+    for (int k = 0; k < kVecPerThread; ++k) {
       const int r = r0 + g + k * kGroups;
       const int which = r < n_rows ? r / H : 3, h = r % H;
       float f[8];

@@ -234,3 +234,34 @@ def draw_stream(w: Workload, b: int, heads: Tuple[int, int] | None = None,
         s.cur_v.append(v)
     s.cur_pos = chunk_positions(w, C)
     return s
+
+
+def span_inputs(w: Workload, spans: List[Span], b: int = 0):
+    """Raw bf16 Q, K, V [n_total, H, D] and int32 positions [n_total, 3] for a
+    list of spans laid out consecutively (the general Fig. 10 form).
+
+    Span i of chunk c and kind k draws its own seeded tensors (seed
+    ``seed_for(w, b, c, 100 + k)``, Q, K, V in that order, N(0, 1) -> bf16; C2
+    outliers as in ``draw_qkv``) and takes the first n positions of chunk c's
+    layout, cycling when n exceeds a chunk.
+    """
+    qs, ks, vs, ps = [], [], [], []
+    H, D = w.heads, w.head_dim
+    for s in spans:
+        g = torch.Generator(device="cpu")
+        g.manual_seed(seed_for(w, b, s.chunk, 100 + s.kind))
+        n = s.n_tokens
+        q = torch.randn(n, H, D, generator=g, dtype=torch.float32)
+        k = torch.randn(n, H, D, generator=g, dtype=torch.float32)
+        v = torch.randn(n, H, D, generator=g, dtype=torch.float32)
+        if w.outliers:
+            u1 = torch.rand(n, H, D, generator=g, dtype=torch.float32)
+            u2 = torch.rand(n, H, D, generator=g, dtype=torch.float32)
+            k = torch.where(u1 < 0.01, 8.0 * torch.sign(u2 - 0.5), k)
+        qs.append(q.to(torch.bfloat16))
+        ks.append(k.to(torch.bfloat16))
+        vs.append(v.to(torch.bfloat16))
+        cp = chunk_positions(w, s.chunk)
+        ps.append(cp[torch.arange(n) % cp.shape[0]])
+    cat = lambda xs: torch.cat(xs, 0).contiguous()
+    return cat(qs), cat(ks), cat(vs), cat(ps)
