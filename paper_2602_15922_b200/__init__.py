@@ -27,7 +27,7 @@ __all__ = ["DzError", "lib", "ChunkKVCache", "CLEAN", "NOISY", "FLAG_WRITE_LSE",
            "nccl_comm_init", "nccl_comm_destroy", "status_string"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdz.so")
+LIB_PATH = os.environ.get("DZ_LIB_PATH") or os.path.join(_HERE, "libdz.so")  # override: A/B diagnostics only
 
 CLEAN, NOISY = 0, 1
 FLAG_WRITE_LSE = 1
@@ -102,6 +102,8 @@ def lib() -> ctypes.CDLL:
                               "(there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         for name, res, args in SIGNATURES:
+            if os.environ.get("DZ_LIB_PATH") and not hasattr(L, name):
+                continue  # an older library under A/B comparison
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

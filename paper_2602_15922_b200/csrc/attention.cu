@@ -137,11 +137,13 @@ __device__ __forceinline__ int span_at(const SpanTable& st, int x) {
 // (query, key) pair in it is visible, FULL if all are visible and in bounds,
 // else PARTIAL.  Visibility is constant over a (query span, key span) pair, so
 // the tile's class follows from the spans overlapping its row and key ranges.
-__device__ uint8_t step_class(const SpanTable& st, int g, int j, int nq, int kv_len) {
+// rows_in_bounds: judge only the rows < nq (the softmax's masking decision:
+// rows past nq are computed but never stored, so they need no mask).
+__device__ __forceinline__ uint8_t step_class(const SpanTable& st, int g, int j, int nq, int kv_len, bool rows_in_bounds = false) {
   const int r0 = g * kTileQ, r1 = min(r0 + kTileQ, nq);
   const int k0 = j * kTileK, k1 = min(k0 + kTileK, kv_len);
   bool any = k0 < st.valid;  // committed keys are visible to every query
-  bool all = (r1 - r0 == kTileQ) && (k1 - k0 == kTileK);
+  bool all = (rows_in_bounds || r1 - r0 == kTileQ) && (k1 - k0 == kTileK);
   if (st.n == 1) return (any || k1 > st.valid) ? (all ? kFull : kPartial) : kSkip;
   if (k1 > st.valid) {
     const int ka = max(k0, st.valid) - st.valid, kb = k1 - st.valid;
@@ -164,7 +166,7 @@ __device__ __forceinline__ void set_bits(uint32_t (&m)[4], int lo, int hi) {
   }
 }
 // Visible-key mask of query span qs over keys [kb0, kb0 + 128) of the key sequence.
-__device__ void visible_bits(const SpanTable& st, int qs, int kb0, int kv_len, uint32_t (&m)[4]) {
+__device__ __forceinline__ void visible_bits(const SpanTable& st, int qs, int kb0, int kv_len, uint32_t (&m)[4]) {
   m[0] = m[1] = m[2] = m[3] = 0u;
   const int kend = min(kb0 + 128, kv_len);
   set_bits(m, 0, min(st.valid, kend) - kb0);  // committed part
@@ -418,6 +420,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int jj = (j == jf ? 0 : j); jj <= (j == jl ? nkv - 1 : j); ++jj)  // incl. skipped steps
             tile_map[g * nkv + jj] = jj == j ? cls : step_class(st, g, jj, nq, kv_len);
         if (cls == kSkip) continue;
+        // mask needed iff an in-bounds row of the tile misses a key of the step (Fig. 10 or key bounds)
+        const bool masked = cls == kPartial && step_class(st, g, j, nq, kv_len, true) == kPartial;
         ptx::mbar_wait(bar(bars->s_full[hc]), s_phase);
         s_phase ^= 1;
         const bool tr = trace_on && u == cid && j < kTraceSteps && row == 0 && hc == 0;
@@ -442,7 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->s_free[hc]));
         if (tr) trace[j * 8 + 6] = (uint32_t)clock();
-        if (cls == kPartial) {  // Fig. 10 mask and key bounds for this warp's 128 keys
+        if (masked) {  // Fig. 10 mask and key bounds for this warp's 128 keys
           uint32_t vm[4];
           visible_bits(st, qs, j * BN + 128 * hc, kv_len, vm);
 #pragma unroll
@@ -488,7 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // offset nor a clamp is needed; online base: p = 2^(s - m).
         const float nbase = (!online || m_used == -INFINITY) ? 0.f : -m_used;
         const uint64_t nb2 = ptx::f2_pack(nbase, nbase);
-        const bool plain = !online && cls == kFull;
+        const bool plain = !online && !masked;
         __syncwarp();
         uint64_t acc[4] = {0, 0, 0, 0};
         // two halves of 64 keys: exponentials of half h, then its P store (the first store

@@ -10,12 +10,13 @@
 // out of the tensor core already in log2 units (one FMA per score saved).
 //
 // Layout: one CTA per (token, batch element).  Every thread first issues
-// all of its 16-byte loads for the token (up to kVecPerThread in flight), and
+// all of its 16-byte loads for the token (3 tensors x kPer heads in flight), and
 // only then do two warps compute the token's D/2 rotation angles (fp64 sincos
 // of p_a * omega_j) into shared memory, so the angle latency hides under the
 // HBM latency instead of preceding it.  A row is handled by D/8 threads with
 // one 16-byte load and one 16-byte store each; the row's sum of squares is
-// reduced with __shfl_xor inside that thread group.  HBM-bound by design: per
+// reduced with __shfl_xor inside that thread group.  Heads are walked with
+// loop counters (no runtime integer division per row).  HBM-bound by design: per
 // token it moves (read + write) 2 B x D x H for each of Q, K, V.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -29,7 +30,6 @@ namespace dz {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kVecPerThread = 8;   // 16-byte loads in flight per thread: 3 H D / 8 <= 2048 vectors per token
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -56,8 +56,9 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
 
 template <int D>
 __global__ void __launch_bounds__(kThreads) prologue_kernel(const PrologueArgs a) {
-  constexpr int G = D / 8;             // threads per row
-  constexpr int kGroups = kThreads / G;
+  constexpr int G = D / 8;             // threads per row (one 16-byte vector each)
+  constexpr int kGroups = kThreads / G;  // rows processed side by side
+  constexpr int kPer = 3;              // heads per thread and tensor in one pass
   __shared__ float2 cs[D / 2];         // (cos, sin) per pair of this token
   const int t = blockIdx.x;
   const int b = blockIdx.y;
@@ -65,22 +66,22 @@ __global__ void __launch_bounds__(kThreads) prologue_kernel(const PrologueArgs a
   const int g = tid / G;               // row group
   const int li = tid % G;              // 8-element slice index inside the row
   const int H = a.H;
-  const int n_rows = 3 * H;            // (q rows, k rows, v rows) of this token
   const int64_t xrow0 = (int64_t)b * a.x_bstride + (int64_t)t * H * D;
 
-  for (int r0 = 0; r0 < n_rows; r0 += kGroups * kVecPerThread) {  // one trip for H <= 85 at D = 128
-    uint4 in[kVecPerThread];
+  // passes over blocks of kGroups * kPer heads (one pass for H <= 48 at D = 128); the trip
+  // count is block-uniform, so the __syncthreads below is reached by every thread
+  for (int h0 = 0; h0 < H; h0 += kGroups * kPer) {
+    uint4 in[3][kPer];
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const int r = r0 + g + k * kGroups;
-      in[k] = make_uint4(0, 0, 0, 0);
-      if (r < n_rows) {
-        const int which = r / H, h = r % H;
-        const uint4* src = reinterpret_cast<const uint4*>(a.x[which]);
-        if (src) in[k] = ld_stream(src + (xrow0 + (int64_t)h * D) / 8 + li);
+    for (int w = 0; w < 3; ++w)
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int h = h0 + g + k * kGroups;
+        const uint4* src = reinterpret_cast<const uint4*>(a.x[w]);
+        in[w][k] = (src != nullptr && h < H) ? ld_stream(src + (xrow0 + (int64_t)h * D) / 8 + li)
+                                             : make_uint4(0, 0, 0, 0);
       }
-    }
-    if (r0 == 0) {  // angles while the loads are in flight
+    if (h0 == 0) {  // the token's rotation angles while the loads are in flight
       if (tid < D / 2) {
         const double p = (double)__ldg(a.pos + 3 * t + a.axis[tid]);
         double sn, cn;
@@ -89,41 +90,49 @@ __global__ void __launch_bounds__(kThreads) prologue_kernel(const PrologueArgs a
       }
       __syncthreads();
     }
+    int64_t row_off[kPer];  // output row offset (without the tensor base) of head h
 #pragma unroll
-    for (int k = 0; k < kVecPerThread; ++k) {
-      const int r = r0 + g + k * kGroups;
-      const int which = r < n_rows ? r / H : 3, h = r % H;
-      float f[8];
-      bf16x8_to_f32(in[k], f);
-      float ss = 0.f;
+    for (int k = 0; k < kPer; ++k) {
+      const int h = h0 + g + k * kGroups;
+      const int dest = h / a.heads_per_dest, hl = h - dest * a.heads_per_dest;
+      row_off[k] = (int64_t)dest * a.y[0].dstride + (int64_t)hl * D;  // dstride is the same for q, k, v slots
+    }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
-      // all 32 lanes take part in the reduction (rows of a warp may differ in kind)
+    for (int w = 0; w < 3; ++w) {
+      if (a.x[w] == nullptr) continue;  // block-uniform
+      const OutSlot& o = a.y[w];
+      const int64_t base = (int64_t)b * o.bstride + (int64_t)t * o.tstride;
 #pragma unroll
-      for (int m = G / 2; m >= 1; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
-      if (which == 3 || a.x[which] == nullptr) continue;
-      const OutSlot& o = a.y[which];
-      const int dest = h / a.heads_per_dest, hl = h % a.heads_per_dest;
-      const int64_t off = (int64_t)b * o.bstride + (int64_t)dest * o.dstride + (int64_t)t * o.tstride +
-                          (int64_t)hl * D;
-      if (which == 2) {  // V: unchanged bf16 copy into the cache / send slot
-        reinterpret_cast<uint4*>(o.base)[off / 8 + li] = in[k];
-        continue;
+      for (int k = 0; k < kPer; ++k) {
+        const int h = h0 + g + k * kGroups;
+        if (w == 2) {  // V: unchanged bf16 copy into the cache / send slot
+          if (h < H) reinterpret_cast<uint4*>(o.base)[(base + row_off[k]) / 8 + li] = in[w][k];
+          continue;
+        }
+        float f[8];
+        bf16x8_to_f32(in[w][k], f);
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
+        // every lane takes part (the two row groups of a warp may differ in validity)
+#pragma unroll
+        for (int m = G / 2; m >= 1; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+        if (h >= H) continue;
+        const float inv = rsqrtf(ss * (1.0f / D) + a.eps);
+        const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
+        const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float sc = w == 0 ? a.q_scale : 1.f;  // Q' leaves pre-scaled by softmax_scale*log2(e)
+        uint32_t pk[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float u = f[2 * i] * inv * gg[2 * i];
+          const float v = f[2 * i + 1] * inv * gg[2 * i + 1];
+          const float2 c = cs[li * 4 + i];
+          pk[i] = pack_half2((u * c.x - v * c.y) * sc, (u * c.y + v * c.x) * sc);
+        }
+        reinterpret_cast<uint4*>(o.base)[(base + row_off[k]) / 8 + li] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-      const float inv = 1.0f / sqrtf(ss * (1.0f / D) + a.eps);
-      const float4* gp = reinterpret_cast<const float4*>(a.gain[which] + h * D + li * 8);
-      const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      uint32_t pk[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float u = f[2 * i] * inv * gg[2 * i];
-        const float w = f[2 * i + 1] * inv * gg[2 * i + 1];
-        const float2 c = cs[li * 4 + i];
-        const float sc = which == 0 ? a.q_scale : 1.f;  // Q' leaves pre-scaled by softmax_scale*log2(e)
-        pk[i] = pack_half2((u * c.x - w * c.y) * sc, (u * c.y + w * c.x) * sc);
-      }
-      reinterpret_cast<uint4*>(o.base)[off / 8 + li] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
   }
 }

@@ -101,7 +101,7 @@ def test_ragged_spans_over_committed_cache():
              synth.Span(4, NOISY, 129), synth.Span(5, CLEAN, 64)]
     q, k, v, pos = synth.span_inputs(w, spans)
     n = q.shape[0]
-    cache, gq, gk = _cache(w, 2 * w.chunk_tokens, n)
+    cache, gq, gk = _cache(w, 2 * w.chunk_tokens, max(n, w.chunk_tokens))
     comm_k, comm_v, comm_p = [], [], []
     for c in range(2):
         _, kc, vc = synth.draw_qkv(w, 0, c)
@@ -178,7 +178,7 @@ def test_online_softmax_spans():
 def test_spans_validation():
     import paper_2602_15922_b200 as dz
     w = synth.scaled(synth.workload("C1"), heads=2)
-    cache, _, _ = _cache(w, w.chunk_tokens, 512)
+    cache, _, _ = _cache(w, w.chunk_tokens, w.chunk_tokens)
     dev = torch.device("cuda")
     _, kc, vc = synth.draw_qkv(w, 0, 0)
     cache.append(kc[None].to(dev), vc[None].to(dev), synth.chunk_positions(w, 0).to(dev), 0)
@@ -186,9 +186,10 @@ def test_spans_validation():
     pos = torch.zeros(256, 3, dtype=torch.int32, device=dev)
     with pytest.raises(dz.DzError, match="DZ_ESTATE"):      # span id must exceed the committed id 0
         cache.attend_spans(q, q, q, pos, [(0, NOISY, 256)])
-    with pytest.raises(dz.DzError, match="DZ_ECAPACITY"):   # 640 > max_chunk 512
-        q2 = torch.zeros(1, 640, 2, 128, dtype=torch.bfloat16, device=dev)
-        cache.attend_spans(q2, q2, q2, torch.zeros(640, 3, dtype=torch.int32, device=dev), [(1, NOISY, 640)])
+    big = w.chunk_tokens + 64
+    with pytest.raises(dz.DzError, match="DZ_ECAPACITY"):   # more tokens than max_chunk
+        q2 = torch.zeros(1, big, 2, 128, dtype=torch.bfloat16, device=dev)
+        cache.attend_spans(q2, q2, q2, torch.zeros(big, 3, dtype=torch.int32, device=dev), [(1, NOISY, big)])
     with pytest.raises(dz.DzError, match="DZ_ESTATE"):      # nothing staged by attend_spans
         cache.attend_spans(q, q, q, pos, [(1, CLEAN, 128), (2, NOISY, 128)])
         cache.commit_staged(1)

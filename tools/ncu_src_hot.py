@@ -4,7 +4,13 @@ import sys
 from collections import Counter
 
 rows = list(csv.reader(open(sys.argv[1])))
-hdr, data = rows[1], rows[2:]
+hdr = rows[1]
+data = []
+for r in rows[2:]:          # first kernel section only
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 iS, iX = hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
 iE = hdr.index("Instructions Executed")
