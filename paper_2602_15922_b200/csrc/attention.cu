@@ -93,20 +93,23 @@ struct Bars {
   uint32_t tmem_base;
 };
 
-// p = 2^(x + nb) for 32 pairs of scores (already in log2 units): kPolyPairs of
-// every 8 pairs through the FMA-pipe polynomial, the rest through MUFU.EX2;
-// row-sum partials in acc, bf16 pairs in pk.  kOffset: add the softmax base nb
-// (online mode); kClamp: x may be -inf / below -126 (masked tile, online mode).
-template <bool kOffset, bool kClamp>
+// p = 2^(x + nb) for 32 pairs of scores (already in log2 units); row-sum
+// partials in acc, bf16 pairs in pk.
+//   kMixed (fixed base, unmasked step: every x in [-40, 40], nb = 0): kPolyPairs
+//     of every 8 pairs through the FMA-pipe polynomial, the rest through MUFU.EX2;
+//   !kMixed (online base or masked step: x may be -inf): every pair through
+//     MUFU.EX2 after adding nb (ex2(-inf) = +0 exactly, so masked keys add 0).
+// Two variants only, to keep the softmax loop inside the instruction cache.
+template <bool kMixed>
 __device__ __forceinline__ void exp_half(const float* s, uint64_t nb2, uint32_t (&pk)[32], uint64_t (&acc)[4]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     uint64_t x = ptx::f2_pack(s[2 * i], s[2 * i + 1]);
-    if (kOffset) x = ptx::f2_add(x, nb2);
     uint64_t p;
-    if ((i % 8) >= 8 - kPolyPairs) {
-      p = ptx::f2_exp2_poly<kClamp>(x);
+    if (kMixed && (i % 8) >= 8 - kPolyPairs) {
+      p = ptx::f2_exp2_poly<false>(x);
     } else {
+      if (!kMixed) x = ptx::f2_add(x, nb2);
       float x0, x1;
       ptx::f2_unpack(x, x0, x1);
       p = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
@@ -430,14 +433,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float s[128];
         {
           uint32_t r[128];
-          if (dbg & 2) {  // diagnostics: no TMEM loads of S
 #pragma unroll
-            for (int i = 0; i < 128; ++i) r[i] = __float_as_uint((float)((i * 7 + row) & 15) * 0.01f);
-          } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[c * 32]));
-            ptx::tmem_wait_ld();
-          }
+          for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[c * 32]));
+          ptx::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 128; ++i) s[i] = __uint_as_float(r[i]);
         }
@@ -500,14 +498,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t pk[32];
-          if (dbg & 4) {  // diagnostics: no exponentials (P = packed S)
-#pragma unroll
-            for (int i = 0; i < 32; ++i) pk[i] = ptx::pack_bf16x2(s[64 * half + 2 * i], s[64 * half + 2 * i + 1]);
-          } else if (plain) {
-            exp_half<false, false>(s + 64 * half, nb2, pk, acc);
-          } else {
-            exp_half<true, true>(s + 64 * half, nb2, pk, acc);
-          }
+          if (plain)
+            exp_half<true>(s + 64 * half, nb2, pk, acc);
+          else
+            exp_half<false>(s + 64 * half, nb2, pk, acc);
           if (half == 0) {
             if (tr) trace[j * 8 + 7] = (uint32_t)clock();
             // P may be overwritten once PV(j-1) has read it

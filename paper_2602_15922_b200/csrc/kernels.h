@@ -61,7 +61,7 @@ struct AttnArgs {
   int32_t B = 0, H = 0, D = 0, nq = 0, kv_len = 0;
   float scale_log2 = 0.f;         // unused by the kernel: Q' is pre-scaled by softmax_scale * log2(e)
   float m_static = 0.f;           // > 0: fixed softmax base (log2 units) bounding every logit; 0: online max
-  int32_t debug_flags = 0;        // diagnostics only (DZ_DEBUG_KERNEL env): 1 no K/V TMA, 2 no S loads
+  int32_t debug_flags = 0;        // diagnostics only (DZ_DEBUG_KERNEL env): 1 no K/V TMA (results are garbage)
   int32_t grid = 0;               // persistent CTAs (<= #SMs)
 };
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);
