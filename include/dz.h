@@ -75,8 +75,9 @@ enum {
   DZ_FLAG_NONE = 0,
   DZ_FLAG_WRITE_LSE = 1, /* keep a per-row log-sum-exp of the last attend (dz_copy_lse) */
   DZ_FLAG_PROFILE = 2,   /* record CUDA events around every kernel/exchange (dz_profile_last) */
-  DZ_FLAG_ONLINE_SOFTMAX = 4 /* always track the running row max, even when the QK-norm bound
-                                D*max|g|^2*scale would allow a fixed softmax base (see dz_create) */
+  DZ_FLAG_ONLINE_SOFTMAX = 4, /* always track the running row max, even when the QK-norm bound
+                                 D*max|g|^2*scale would allow a fixed softmax base (see dz_create) */
+  DZ_FLAG_TILE_MAP = 8        /* record the attention kernel's tile decisions (dz_get_tile_map; tests) */
 };
 
 typedef struct {
@@ -226,8 +227,10 @@ DZ_API dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset);
 
 /* Pipeline diagnostics: enable != 0 makes later attention launches record a
  * clock() trace of CTA 0's first work unit (MMA waits/issues, softmax S-ready /
- * P-done per KV step, up to 256 steps; layout documented in attention.cu).
- * host != NULL copies up to n words of the last trace.  Synchronous. */
+ * P-done per KV step, up to 256 steps; layout documented in attention.cu),
+ * followed (words 8192 ..) by a per-CTA timeline of up to 160 CTAs x 64 words
+ * (globaltimer ns of each work segment's start / end).  host != NULL copies up
+ * to n words of the last trace.  Synchronous. */
 DZ_API dz_status dz_debug_trace(int32_t enable, uint32_t* host, size_t n);
 
 /* Number of attention work units (batch x heads/world_size x query-tile pairs)

@@ -33,6 +33,7 @@ CLEAN, NOISY = 0, 1
 FLAG_WRITE_LSE = 1
 FLAG_PROFILE = 2
 FLAG_ONLINE_SOFTMAX = 4
+FLAG_TILE_MAP = 8
 
 STATUS = {0: "DZ_OK", -1: "DZ_EINVAL", -2: "DZ_ESHAPE", -3: "DZ_ECAPACITY", -4: "DZ_ESTATE",
           -5: "DZ_ECUDA", -6: "DZ_ENCCL", -7: "DZ_ERANGE"}
@@ -143,9 +144,11 @@ def watchdog(reset: bool = True):
 
 
 def debug_trace(enable: bool, read: bool = False) -> Optional[np.ndarray]:
-    """Toggle / read the attention kernel's cycle trace (uint32 [8192]); see dz.h."""
-    buf = np.zeros(8192, dtype=np.uint32) if read else None
-    s = lib().dz_debug_trace(int(enable), buf.ctypes.data if read else None, 8192 if read else 0)
+    """Toggle / read the attention kernel's traces: uint32 [8192] cycle trace of CTA 0, then
+    [160][64] per-CTA timeline (globaltimer ns); see dz.h and attention.cu."""
+    n = 8192 + 160 * 64
+    buf = np.zeros(n, dtype=np.uint32) if read else None
+    s = lib().dz_debug_trace(int(enable), buf.ctypes.data if read else None, n if read else 0)
     if s:
         raise DzError(s, "dz_debug_trace")
     return buf

@@ -70,6 +70,16 @@ constexpr uint32_t kRegsLight = 88, kRegsSoftmax = 208;  // setmaxnreg: 128*88 +
 constexpr int kTraceSteps = 256;
 __device__ uint32_t g_dz_trace[kTraceSteps * 32];
 __device__ int g_dz_trace_on;
+// Per-CTA timeline (globaltimer ns, low 32 bits), softmax warp 0 lane 0 of every CTA:
+// [0] start, [1] end, [2] / [3] clock() at start / end, [4] segments, [5] combines; segment i < 14:
+// [8 + 4i] start, [9 + 4i] last step's P written, [10 + 4i] O complete (o_full), [11 + 4i] end (clock()).
+constexpr int kTimelineCtas = 160, kTimelineWords = 64, kTlSegs = 14;
+__device__ uint32_t g_dz_timeline[kTimelineCtas * kTimelineWords];
+__device__ __forceinline__ uint32_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (uint32_t)t;
+}
 
 template <int D>
 struct Cfg {
@@ -81,17 +91,22 @@ struct Cfg {
   static constexpr int kKVOff = kQTileBytes;
   static constexpr int kRedOff = kKVOff + kStages * kStageBytes;  // row max / row sum exchange [2][BM]
   static constexpr int kBarOff = kRedOff + 2 * BM * 4;
-  static constexpr int kSmem = kBarOff + 256 + 1024;              // + barriers + alignment slack
+  static constexpr int kSmem = kBarOff + 576 + 1024;              // + barriers/schedule + alignment slack
   static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, 2 * BM, BN / 2);  // f16 x f16, K-major, per half
   static constexpr uint32_t kIdescPV = ptx::idesc_f16(1, 1, 0, 1, 2 * BM, D);   // P (TMEM) x V (MN-major)
   static constexpr int kVRowBytes = D;                      // V half row: D/2 bf16
 };
 
+constexpr int kMaxGroups = 64;    // stream-K schedule needs <= 64 query groups (16384 query rows)
+
 struct Bars {
   uint64_t q_full, q_empty, s_full[2], s_free[2], p_full, p_empty, o_full, o_empty;
   uint64_t kv_full[12], kv_empty[12];
   uint32_t tmem_base;
+  int32_t last_piece;               // combine election result (softmax warps)
+  int32_t gpre[kMaxGroups + 1];     // prefix sums of executed steps per query group
 };
+static_assert(sizeof(Bars) <= 576, "Bars must fit its shared-memory slot");
 
 // p = 2^(x + nb) for 32 pairs of scores (already in log2 units); row-sum
 // partials in acc, bf16 pairs in pk.
@@ -189,19 +204,84 @@ __device__ __forceinline__ void active_range(const SpanTable& st, int g, int nq,
   while (jl > jf && step_class(st, g, jl, nq, kv_len) == kSkip) --jl;
 }
 
-__device__ __forceinline__ void decode_unit(int u, int n_groups, int H, int& b, int& h, int& g) {
-  g = u % n_groups;
+// ------------------------------------------------------------ work schedule --
+// Stream-K over executed steps: the sequence of (unit, executed step), units
+// u = (b, h, g) in order and their non-SKIP steps in key order, is cut into
+// ncl equal ranges, one per CTA pair, so every pair does the same number of
+// steps (+-1) whatever the unit count.  A unit cut by a range boundary is
+// computed in pieces, each a contiguous run of its steps; every piece writes
+// its unnormalised O, row sum and base to the workspace and the last piece to
+// finish (atomic count) combines them in key order -- deterministic, no
+// waiting.  With more than kMaxGroups query groups the schedule falls back to
+// whole units dealt round-robin.
+struct Seg {
+  int b, h, g;
+  int k0, k1, cnt;  // executed-step range [k0, k1) of the unit's cnt steps
+};
+struct Sched {
+  bool streamk;
+  int lo, hi, wbh, W;  // stream-K: this pair's range, steps per (b, h), total steps (host keeps W * P < 2^31)
+  int P;               // pairs
+  int u;               // round-robin: next unit
+};
+__device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_groups, int n_units, int H,
+                                      const SpanTable& st, int nq, int kv_len, int nkv, Seg& sg) {
+  if (sc.streamk) {
+    if (sc.lo >= sc.hi) return false;
+    const int bh = sc.lo / sc.wbh;
+    const int r = sc.lo - bh * sc.wbh;
+    int g = 0;
+    while (gpre[g + 1] <= r) ++g;
+    sg.g = g;
+    sg.h = bh % H;
+    sg.b = bh / H;
+    sg.cnt = gpre[g + 1] - gpre[g];
+    sg.k0 = r - gpre[g];
+    sg.k1 = min(sg.cnt, sg.k0 + (sc.hi - sc.lo));
+    sc.lo += sg.k1 - sg.k0;
+    return true;
+  }
+  if (sc.u >= n_units) return false;
+  const int u = sc.u;
+  sc.u += sc.P;
+  sg.g = u % n_groups;
   const int bh = u / n_groups;
-  h = bh % H;
-  b = bh / H;
+  sg.h = bh % H;
+  sg.b = bh / H;
+  sg.k0 = 0;
+  int cnt = nkv;  // whole unit: all of its executed steps
+  if (st.n != 1) {
+    cnt = 0;
+    for (int j = 0; j < nkv; ++j) cnt += step_class(st, sg.g, j, nq, kv_len) != kSkip;
+  }
+  sg.k1 = sg.cnt = cnt;
+  return true;
 }
+// stream-K range boundary of pair p
+__device__ __forceinline__ int pair_lo(int W, int P, int p) { return W * p / P; }
+__device__ __forceinline__ int pair_of(int W, int P, int x) {
+  int p = x * P / W;
+  while (p + 1 < P && pair_lo(W, P, p + 1) <= x) ++p;
+  while (p > 0 && pair_lo(W, P, p) > x) --p;
+  return p;
+}
+// key step of the k-th executed step of group g (k counted from the group's first executed step)
+__device__ __forceinline__ int step_of(const SpanTable& st, int g, int k, int nq, int kv_len, int nkv) {
+  if (st.n == 1) return k;
+  int j = 0;
+  for (;; ++j) {
+    if (step_class(st, g, j, nq, kv_len) == kSkip) continue;
+    if (k-- == 0) return j;
+  }
+}
+
 
 template <int D>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ out, int64_t o_bstride,
                     int64_t o_tstride, float* __restrict__ lse, uint8_t* __restrict__ tile_map, int B, int H,
-                    int nq, int kv_len, float scale_log2, float m_static, int dbg,
+                    int nq, int kv_len, float m_static, int dbg, float* __restrict__ ws, int* __restrict__ ws_cnt,
                     const __grid_constant__ SpanTable st) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -234,6 +314,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ph = (i / C::kStages) & 1;
   };
 
+  // executed steps per query group -> prefix sums (every role walks the same schedule)
+  const bool streamk = ws != nullptr && n_groups <= kMaxGroups;
+  if (streamk) {
+    if (st.n == 1) {
+      for (int g = threadIdx.x; g <= n_groups; g += kThreads) bars->gpre[g] = g * nkv;
+    } else {
+      for (int g = threadIdx.x; g <= n_groups; g += kThreads) bars->gpre[g] = 0;
+      __syncthreads();
+      for (int x = threadIdx.x; x < n_groups * nkv; x += kThreads)
+        if (step_class(st, x / nkv, x % nkv, nq, kv_len) != kSkip) atomicAdd(&bars->gpre[x / nkv + 1], 1);
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int g = 1; g <= n_groups; ++g) bars->gpre[g] += bars->gpre[g - 1];
+    }
+  }
   if (warp == kWarpTma && lane == 0) {
     ptx::mbar_init(bar(bars->q_full), 1);
     ptx::mbar_init(bar(bars->q_empty), 1);
@@ -260,6 +355,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::cluster_sync();  // both CTAs' barriers initialised and TMEM allocated before any remote traffic
   ptx::tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  const int32_t* gpre = bars->gpre;
+
+  Sched sched0;
+  sched0.streamk = streamk;
+  sched0.P = ncl;
+  sched0.u = cid;
+  if (streamk) {
+    sched0.wbh = gpre[n_groups];
+    sched0.W = B * H * sched0.wbh;
+    sched0.lo = pair_lo(sched0.W, ncl, cid);
+    sched0.hi = pair_lo(sched0.W, ncl, cid + 1);
+  }
 
   if (warp >= 8) {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsLight));
@@ -268,9 +375,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint64_t pol_q = ptx::l2_policy_evict_first();
     const uint64_t pol_kv = ptx::l2_policy_evict_last();
     uint32_t ld = 0, q_phase = 0;
-    for (int u = cid; u < n_units; u += ncl) {
-      int b, h, g;
-      decode_unit(u, n_groups, H, b, h, g);
+    Sched sc = sched0;
+    Seg sg;
+    while (next_seg(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+      const int b = sg.b, h = sg.h, g = sg.g;
       ptx::mbar_wait(bar(bars->q_empty), q_phase ^ 1);
       q_phase ^= 1;
       const int qt = 2 * g + (int)rank;
@@ -280,8 +388,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int x = 0; x < C::kQBoxes; ++x)
             ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * 64, h, qt * BM, b, pol_q);
       }
-      for (int j = 0; j < nkv; ++j) {
-        if (step_class(st, g, j, nq, kv_len) == kSkip) continue;
+      int j = step_of(st, g, sg.k0, nq, kv_len, nkv);
+      for (int k = sg.k0; k < sg.k1; ++k, ++j) {
+        while (step_class(st, g, j, nq, kv_len) == kSkip) ++j;
         for (int kv = 0; kv < 2; ++kv, ++ld) {  // K_j half (128 keys x D), then V_j half (256 keys x D/2)
           uint32_t st, ph;
           slot(ld, st, ph);
@@ -308,25 +417,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if ((warp == kWarpMma || warp == kWarpPv) && leader) {
     // ------------------------------------------------------ MMA issuers --
-    // Two single-thread issuers walk the flattened steps g of this cluster's
-    // units: warp 11 issues QK(g), warp 9 issues PV(g-1).  tcgen05.mma issue
-    // blocks at the tensor pipe's rate (the queue is shallow), so an issuer that
-    // waits on a barrier starves the pipe; with two issuers, one keeps it fed
-    // while the other waits.  QK and PV touch disjoint TMEM (S vs P/O) and
-    // release their own K / V stages, so their streams need no mutual order.
+    // Two single-thread issuers walk the same schedule: warp 11 issues QK(j),
+    // warp 9 issues PV(j) once the softmax has written P(j).  tcgen05.mma
+    // issue blocks at the tensor pipe's rate (the queue is shallow), so an
+    // issuer that waits on a barrier starves the pipe; with two issuers, one
+    // keeps it fed while the other waits.  QK and PV touch disjoint TMEM (S vs
+    // P/O) and release their own K / V stages, so their streams need no mutual
+    // order.
     const bool do_qk = warp == kWarpMma;
     uint32_t q_phase = 0, sf_phase = 0, pf_phase = 0, oe_phase = 0;
-    int gs = 0;  // this issuer's running count of executed (non-SKIP) steps
-    for (int u = cid; u < n_units; u += ncl) {
-      int b, h, g;
-      decode_unit(u, n_groups, H, b, h, g);
-      int jf, jl;
-      active_range(st, g, nq, kv_len, nkv, jf, jl);
-      for (int j = jf; j <= jl; ++j) {
-        if (j > jf && j < jl && step_class(st, g, j, nq, kv_len) == kSkip) continue;
-        const bool tr = trace_on && u == cid && j < kTraceSteps && lane == 0;
+    int gs = 0;  // this issuer's running count of executed steps
+    Sched sc = sched0;
+    Seg sg;
+    bool first_seg = true;
+    while (next_seg(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+      const int g = sg.g;
+      int j = step_of(st, g, sg.k0, nq, kv_len, nkv);
+      for (int k = sg.k0; k < sg.k1; ++k, ++j) {
+        while (step_class(st, g, j, nq, kv_len) == kSkip) ++j;
+        const bool first = k == sg.k0, last = k == sg.k1 - 1;
+        const bool tr = trace_on && first_seg && j < kTraceSteps && lane == 0;
         if (do_qk) {
-          if (j == jf) {  // first step of a new unit: its Q tiles
+          if (first) {  // first step of a piece: its Q tiles
             ptx::mbar_wait(bar(bars->q_full), q_phase);
             q_phase ^= 1;
           }
@@ -357,7 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               ptx::tc_commit_2cta(bar(bars->s_full[hh]), kBoth);
               if (hh == 1) {
                 ptx::tc_commit_2cta(bar(bars->kv_empty[k_st]), kBoth);
-                if (j == jl) ptx::tc_commit_2cta(bar(bars->q_empty), kBoth);
+                if (last) ptx::tc_commit_2cta(bar(bars->q_empty), kBoth);
               }
             }
             __syncwarp();
@@ -369,7 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (tr) trace[j * 8 + 2] = (uint32_t)clock();
           ptx::mbar_wait(bar(bars->p_full), pf_phase);
           pf_phase ^= 1;
-          if (j == jf) {  // the previous unit's epilogue has read O
+          if (first) {  // the previous piece's epilogue has read O
             ptx::mbar_wait(bar(bars->o_empty), oe_phase ^ 1);
             oe_phase ^= 1;
           }
@@ -381,18 +493,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < BN / 16; ++kk) {
               const uint64_t bd = D == 128 ? ptx::sdesc_sw128(va + kk * 16 * C::kVRowBytes, 16, 1024)
                                            : ptx::sdesc_sw64(va + kk * 16 * C::kVRowBytes, 16, 512);
-              ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + kk * 8, bd, C::kIdescPV,
-                               (j > jf || kk > 0) ? 1u : 0u);
+              ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + kk * 8, bd, C::kIdescPV, (!first || kk > 0) ? 1u : 0u);
               if (tr && j == 9) trace[kTraceSteps * 8 + 16 + kk] = (uint32_t)clock();
             }
             ptx::tc_commit_2cta(bar(bars->p_empty), kBoth);              // P may be overwritten
-            if (j == jl) ptx::tc_commit_2cta(bar(bars->o_full), kBoth);
+            if (last) ptx::tc_commit_2cta(bar(bars->o_full), kBoth);
             ptx::tc_commit_2cta(bar(bars->kv_empty[v_st]), kBoth);
           }
           __syncwarp();
         }
         ++gs;
       }
+      first_seg = false;
     }
   }
   } else {
@@ -406,28 +518,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tP = tmem + lane_bits + kColP + hc * 64;
     const uint32_t tO = tmem + lane_bits + kColO + hc * (D / 2);
     const uint32_t pair_bar = 1 + quad;         // named barrier: the two warps of these rows
+    constexpr uint32_t kSoftmaxBar = 5;         // named barrier: all 8 softmax warps
+    const bool online = m_static <= 0.f;
     uint32_t s_phase = 0, pe_phase = 0, of_phase = 0;
-    for (int u = cid; u < n_units; u += ncl) {
-      int b, h, g;
-      decode_unit(u, n_groups, H, b, h, g);
+    Sched sc = sched0;
+    Seg sg;
+    bool first_seg = true;
+    const bool tl = g_dz_trace_on != 0 && threadIdx.x == 0 && blockIdx.x < kTimelineCtas;
+    uint32_t* const tline = g_dz_timeline + blockIdx.x * kTimelineWords;
+    int n_seg = 0, n_comb = 0, n_part = 0;
+    if (tl) {
+      tline[0] = gtime();
+      tline[2] = (uint32_t)clock();
+    }
+    while (next_seg(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+      const int b = sg.b, h = sg.h, g = sg.g;
       const int qt = 2 * g + (int)rank;
-      float m_used = m_static > 0.f ? 0.f : -INFINITY;  // softmax base, log2 units (fixed base: 0)
-      float l = 0.f;                                          // partial row sum over this warp's keys
-      const int s_row = qt * BM + row;                        // this thread's query (row of the new tokens)
+      if (tl && n_seg < kTlSegs) tline[8 + 4 * n_seg] = (uint32_t)clock();
+      float m_used = online ? -INFINITY : 0.f;   // softmax base, log2 units (fixed base: 0)
+      float l = 0.f;                              // partial row sum over this warp's keys
+      const int s_row = qt * BM + row;            // this thread's query (row of the new tokens)
       const int qs = st.n == 1 ? 0 : span_at(st, min(s_row, nq - 1));  // its span (rows past nq: never stored)
-      int jf, jl;
-      active_range(st, g, nq, kv_len, nkv, jf, jl);
-      for (int j = jf; j <= jl; ++j) {
+      const bool map_thread = tile_map != nullptr && b == 0 && h == 0 && rank == 0 && row == 0 && hc == 0;
+      int j = step_of(st, g, sg.k0, nq, kv_len, nkv);
+      for (int k = sg.k0; k < sg.k1; ++k, ++j) {
+        while (step_class(st, g, j, nq, kv_len) == kSkip) ++j;
+        const bool first = k == sg.k0;
         const uint8_t cls = step_class(st, g, j, nq, kv_len);
-        if (tile_map != nullptr && u < n_groups && rank == 0 && row == 0 && hc == 0)
-          for (int jj = (j == jf ? 0 : j); jj <= (j == jl ? nkv - 1 : j); ++jj)  // incl. skipped steps
-            tile_map[g * nkv + jj] = jj == j ? cls : step_class(st, g, jj, nq, kv_len);
-        if (cls == kSkip) continue;
+        if (map_thread) tile_map[g * nkv + j] = cls;  // executed steps only; the host zeroes (SKIP) the map
         // mask needed iff an in-bounds row of the tile misses a key of the step (Fig. 10 or key bounds)
         const bool masked = cls == kPartial && step_class(st, g, j, nq, kv_len, true) == kPartial;
         ptx::mbar_wait(bar(bars->s_full[hc]), s_phase);
         s_phase ^= 1;
-        const bool tr = trace_on && u == cid && j < kTraceSteps && row == 0 && hc == 0;
+        const bool tr = trace_on && first_seg && j < kTraceSteps && row == 0 && hc == 0;
         if (tr) trace[j * 8 + 4] = (uint32_t)clock();
         ptx::tc_fence_after();
         float s[128];
@@ -451,7 +574,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 128; ++i)
             if (!((vm[i / 32] >> (i % 32)) & 1u)) s[i] = -INFINITY;
         }
-        const bool online = m_static <= 0.f;
         if (online) {
           // Online softmax with lazy rescaling: a row moves its base only when its max
           // grew by more than 2^8; both warps of a row take the same decision from the
@@ -466,7 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mx = fmaxf(mx, red[(hc ^ 1) * BM + row]);
           ptx::named_bar_sync(pair_bar, 64);  // both read before the next exchange
           const bool grow = mx > m_used + kRescaleLog2;
-          const bool rescale = grow && j > jf && m_used != -INFINITY;
+          const bool rescale = grow && !first && m_used != -INFINITY;
           if (__any_sync(0xffffffffu, rescale)) {
             ptx::mbar_wait(bar(bars->p_empty), pe_phase ^ 1);  // PV(j-1) done
             ptx::tc_fence_after();
@@ -523,7 +645,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->p_full));
         if (tr) trace[j * 8 + 5] = (uint32_t)clock();
       }
-      // epilogue: total row sum over both key halves, O / l -> bf16 -> HBM (this warp's D/2 columns)
+      first_seg = false;
+      if (tl && n_seg < kTlSegs) tline[9 + 4 * n_seg] = (uint32_t)clock();
+      // total row sum over both key halves
       red[hc * BM + row] = l;
       ptx::named_bar_sync(pair_bar, 64);
       const float lt = l + red[(hc ^ 1) * BM + row];
@@ -531,31 +655,135 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(bar(bars->o_full), of_phase);
       of_phase ^= 1;
       ptx::tc_fence_after();
+      if (tl && n_seg < kTlSegs) tline[10 + 4 * n_seg] = (uint32_t)clock();
       const int s_idx = qt * BM + row;
-      const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
       __nv_bfloat16* orow = out + b * o_bstride + (int64_t)s_idx * o_tstride + (int64_t)h * D + hc * (D / 2);
+      if (sg.k0 == 0 && sg.k1 == sg.cnt) {
+        // whole unit: O / l -> bf16 -> HBM (this warp's D/2 columns)
+        const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
 #pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          uint32_t r[32];
+          __syncwarp();  // reconverge after the row-dependent store below
+          ptx::tmem_ld32(tO + c * 32, r);
+          ptx::tmem_wait_ld();
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            pk[i] = ptx::pack_bf16x2(__uint_as_float(r[2 * i]) * inv_l, __uint_as_float(r[2 * i + 1]) * inv_l);
+          if (s_idx < nq) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              ptx::st_global_v4(orow + c * 32 + v * 8, pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+          }
+        }
+        if (lse != nullptr && hc == 0 && s_idx < nq)
+          lse[((int64_t)b * H + h) * nq + s_idx] =
+              (lt > 0.f) ? (m_used + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));
+        if (tl && n_seg < kTlSegs) tline[11 + 4 * n_seg] = (uint32_t)clock();
+        ++n_seg;
+        continue;
+      }
+      // ---- a piece of a unit split across pairs (stream-K): publish (O, l, base) ----
+      // workspace slot: the pair's head piece (starts mid-unit) or tail piece (ends mid-unit);
+      // layout per (slot, rank): O [D][128] fp32 column-major (coalesced per column), l [128], m [128]
+      constexpr int kSlotFloats = (D + 2) * BM;
+      float* mine = ws + ((size_t)(2 * cid + (sg.k0 > 0 ? 0 : 1)) * 2 + rank) * kSlotFloats;
+#pragma unroll 1
       for (int c = 0; c < D / 64; ++c) {
         uint32_t r[32];
-        __syncwarp();  // reconverge after the row-dependent store below
         ptx::tmem_ld32(tO + c * 32, r);
         ptx::tmem_wait_ld();
-        uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[i] = ptx::pack_bf16x2(__uint_as_float(r[2 * i]) * inv_l, __uint_as_float(r[2 * i + 1]) * inv_l);
-        if (s_idx < nq) {
+        for (int i = 0; i < 32; ++i) __stcg(mine + (hc * (D / 2) + c * 32 + i) * BM + row, __uint_as_float(r[i]));
+      }
+      if (hc == 0) {
+        __stcg(mine + D * BM + row, lt);
+        __stcg(mine + (D + 1) * BM + row, m_used);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));  // TMEM O has been read
+      if (tl && n_part < 2) tline[50 + 5 * n_part] = (uint32_t)clock();
+      // publish: every thread's stores precede the barrier; one thread fences (cumulative) and counts
+      ptx::named_bar_sync(kSoftmaxBar, 256);
+      const int ustart = (b * H + h) * sched0.wbh + gpre[g];
+      const int pf = pair_of(sched0.W, ncl, ustart), pl = pair_of(sched0.W, ncl, ustart + sg.cnt - 1);
+      // pieces = pairs in [pf, pl] with a non-empty range (a pair's range may be empty when W < P)
+      int n_pieces = 0;
+      for (int q = pf; q <= pl; ++q) n_pieces += pair_lo(sched0.W, ncl, q) < pair_lo(sched0.W, ncl, q + 1);
+      int* cnt_ptr = ws_cnt + (((int64_t)b * H + h) * n_groups + g) * 2 + rank;
+      if (threadIdx.x == 0) {
+        __threadfence();
+        const bool last_piece = atomicAdd(cnt_ptr, 1) == n_pieces - 1;
+        if (last_piece) __threadfence();  // acquire the other pieces before the barrier releases the readers
+        bars->last_piece = last_piece;
+      }
+      ptx::named_bar_sync(kSoftmaxBar, 256);
+      if (tl && n_part < 2) tline[51 + 5 * n_part] = (uint32_t)clock();
+      if (!bars->last_piece) {
+        if (tl && n_seg < kTlSegs) tline[11 + 4 * n_seg] = (uint32_t)clock();
+        ++n_seg;
+        ++n_part;
+        continue;
+      }
+      // last piece to finish: combine all pieces of this unit in key order.  Each piece's
+      // D/2 columns of this row are loaded in one batch (64 loads in flight per thread), so
+      // a combine costs about one L2 round trip per piece.
+      float mmax = -INFINITY;
+#pragma unroll 1
+      for (int q = pf; q <= pl; ++q) {
+        if (pair_lo(sched0.W, ncl, q) == pair_lo(sched0.W, ncl, q + 1)) continue;
+        const float* pc = ws + ((size_t)(2 * q + (q == pf ? 1 : 0)) * 2 + rank) * kSlotFloats;
+        mmax = fmaxf(mmax, __ldcg(pc + (D + 1) * BM + row));
+      }
+      float wsum = 0.f;
+      float acc[D / 2];
 #pragma unroll
-          for (int v = 0; v < 4; ++v)
-            ptx::st_global_v4(orow + c * 32 + v * 8, pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+      for (int i = 0; i < D / 2; ++i) acc[i] = 0.f;
+#pragma unroll 1
+      for (int q = pf; q <= pl; ++q) {
+        if (pair_lo(sched0.W, ncl, q) == pair_lo(sched0.W, ncl, q + 1)) continue;
+        const float* pc = ws + ((size_t)(2 * q + (q == pf ? 1 : 0)) * 2 + rank) * kSlotFloats;
+        float v[D / 2];
+#pragma unroll
+        for (int i = 0; i < D / 2; ++i) v[i] = __ldcg(pc + (hc * (D / 2) + i) * BM + row);
+        const float mq = __ldcg(pc + (D + 1) * BM + row);
+        const float lq = __ldcg(pc + D * BM + row);
+        const float wq = mq == -INFINITY ? 0.f : ptx::ex2(mq - mmax);  // fixed base: every mq = 0, wq = 1
+        wsum += wq * lq;
+#pragma unroll
+        for (int i = 0; i < D / 2; ++i) acc[i] = fmaf(wq, v[i], acc[i]);
+      }
+      const float inv_l = wsum > 0.f ? 1.f / wsum : 0.f;
+      if (tl && n_part < 2) tline[52 + 5 * n_part] = (uint32_t)clock();
+      if (s_idx < nq) {
+#pragma unroll
+        for (int c8 = 0; c8 < D / 16; ++c8) {
+          const float* a8 = acc + c8 * 8;
+          ptx::st_global_v4(orow + c8 * 8, ptx::pack_bf16x2(a8[0] * inv_l, a8[1] * inv_l),
+                            ptx::pack_bf16x2(a8[2] * inv_l, a8[3] * inv_l), ptx::pack_bf16x2(a8[4] * inv_l, a8[5] * inv_l),
+                            ptx::pack_bf16x2(a8[6] * inv_l, a8[7] * inv_l));
         }
       }
       if (lse != nullptr && hc == 0 && s_idx < nq)
         lse[((int64_t)b * H + h) * nq + s_idx] =
-            (lt > 0.f) ? (m_used + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));
+            (wsum > 0.f) ? (mmax + __log2f(wsum)) * 0.69314718055994530942f : -INFINITY;
+      if (threadIdx.x == 0) *cnt_ptr = 0;  // ready for the next launch
+      if (tl && n_seg < kTlSegs) tline[11 + 4 * n_seg] = (uint32_t)clock();
+      if (tl && n_part < 2) tline[53 + 5 * n_part] = (uint32_t)clock();
+      ++n_seg;
+      ++n_comb;
+      ++n_part;
+    }
+    if (tl) {
+      tline[1] = gtime();
+      tline[3] = (uint32_t)clock();
+      tline[4] = n_seg;
+      tline[5] = n_comb;
     }
   }
 
@@ -572,8 +800,8 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return e;
   k<<<a.grid, kThreads, C::kSmem, s>>>(a.tm_q, a.tm_k, a.tm_v, static_cast<__nv_bfloat16*>(a.out), a.o_bstride,
-                                       a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq, a.kv_len, a.scale_log2,
-                                       a.m_static, a.debug_flags, a.spans);
+                                       a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq, a.kv_len, a.m_static,
+                                       a.debug_flags, a.ws, a.ws_cnt, a.spans);
   return cudaGetLastError();
 }
 
@@ -586,7 +814,11 @@ cudaError_t trace_control(int enable, uint32_t* host, size_t n) {
   cudaError_t e = cudaMemcpyToSymbol(g_dz_trace_on, &enable, sizeof(int));
   if (e != cudaSuccess || host == nullptr) return e;
   const size_t bytes = std::min(n, (size_t)kTraceSteps * 32) * sizeof(uint32_t);
-  return cudaMemcpyFromSymbol(host, g_dz_trace, bytes);
+  e = cudaMemcpyFromSymbol(host, g_dz_trace, bytes);
+  if (e != cudaSuccess || n <= (size_t)kTraceSteps * 32) return e;
+  // words past the step trace: the per-CTA timeline
+  const size_t tl = std::min(n - kTraceSteps * 32, (size_t)kTimelineCtas * kTimelineWords) * sizeof(uint32_t);
+  return cudaMemcpyFromSymbol(host + kTraceSteps * 32, g_dz_timeline, tl);
 }
 cudaError_t reset_watchdog() {
   static const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -32,7 +32,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct Layout {  // byte offsets inside the caller's storage
   int64_t slots = 0;
   size_t k_off = 0, v_off = 0, q_off = 0, lse_off = 0, sq_off = 0, sk_off = 0, sv_off = 0, ol_off = 0,
-         or_off = 0, map_off = 0, total = 0;
+         or_off = 0, map_off = 0, ws_off = 0, cnt_off = 0, cnt_bytes = 0, total = 0;
 };
 
 bool basic_cfg_ok(const dz_config* c) {
@@ -73,7 +73,11 @@ Layout make_layout(const dz_config* c) {
   L.v_off = take((size_t)B * L.slots * Hl * D * 2);
   L.q_off = take((size_t)B * mc * Hl * D * 2);                       // Q' fp16
   L.lse_off = take((c->flags & DZ_FLAG_WRITE_LSE) ? (size_t)B * Hl * mc * 4 : 0);
-  L.map_off = take(map_bytes(c));
+  L.map_off = take((c->flags & DZ_FLAG_TILE_MAP) ? map_bytes(c) : 0);
+  // K2 stream-K workspace: per pair a head and a tail piece, per CTA rank (D + 2) x 128 fp32
+  L.ws_off = take((size_t)2 * dz::kMaxPairs * 2 * (D + 2) * 128 * 4);
+  L.cnt_bytes = (size_t)B * Hl * ((mc + dz::kTileQ - 1) / dz::kTileQ) * 2 * 4;
+  L.cnt_off = take(L.cnt_bytes);
   if (N > 1) {
     const size_t sb = (size_t)B * (mc / N) * c->heads * D * 2;       // [N][B][n_loc][Hl][D]
     L.sq_off = take(sb);
@@ -141,6 +145,7 @@ struct dz_ctx {
   dz::PrologueArgs pro;  // RoPE frequencies, axes, gains
   ncclComm_t comm = nullptr;
   bool poisoned = false;
+  bool ws_zeroed = false;  // stream-K piece counters initialised
   // DZ_FLAG_PROFILE: events e[0..4] around the attend phases, a[0..1] around the append
   cudaEvent_t ev[5] = {}, ev_app[2] = {};
   bool have_attend_ev = false, have_append_ev = false;
@@ -352,11 +357,25 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   a.scale_log2 = c->scale * 1.4426950408889634f;
   a.m_static = c->m_static;
   if (const char* e = getenv("DZ_DEBUG_KERNEL")) a.debug_flags = atoi(e);  // diagnostics: results are garbage
-  const int units = dz::attention_units(c->B, c->Hl, (int32_t)n);  // CTA-pair units
-  a.grid = 2 * std::min(units, c->num_sms / 2);                      // persistent: one CTA pair per TPC
+  // persistent grid: one CTA pair per TPC; stream-K spreads the executed steps evenly over the pairs
+  a.grid = 2 * std::min(c->num_sms / 2, dz::kMaxPairs);
+  // stream-K needs <= 64 query groups and 32-bit step arithmetic (W * pairs < 2^31); else whole units round-robin
+  const int64_t n_groups = (n + dz::kTileQ - 1) / dz::kTileQ, n_steps = (kv_len + dz::kTileK - 1) / dz::kTileK;
+  const bool streamk = n_groups <= 64 && (int64_t)c->B * c->Hl * n_groups * n_steps * dz::kMaxPairs < (1ll << 31);
+  a.ws = streamk ? reinterpret_cast<float*>(c->base + c->L.ws_off) : nullptr;
+  a.ws_cnt = reinterpret_cast<int32_t*>(c->base + c->L.cnt_off);
+  if (!c->ws_zeroed) {  // piece counters start at zero; every combine resets its own
+    dz_status r = cuda_check(c, cudaMemsetAsync(a.ws_cnt, 0, c->L.cnt_bytes, st),
+                             "counter init");
+    if (r) return r;
+    c->ws_zeroed = true;
+  }
   const int ngr = (int)((n + dz::kTileQ - 1) / dz::kTileQ), nst = (int)((kv_len + dz::kTileK - 1) / dz::kTileK);
-  if ((size_t)ngr * nst <= map_bytes(&c->cfg)) {
+  if ((c->cfg.flags & DZ_FLAG_TILE_MAP) && (size_t)ngr * nst <= map_bytes(&c->cfg)) {
     a.tile_map = reinterpret_cast<uint8_t*>(c->base + c->L.map_off);
+    // the kernel writes the executed steps (FULL / PARTIAL); the rest stay SKIP
+    dz_status r = cuda_check(c, cudaMemsetAsync(a.tile_map, 0, (size_t)ngr * nst, st), "tile map clear");
+    if (r) return r;
     c->last_nq_tiles = ngr;
     c->last_nkv_tiles = nst;
     c->have_map = true;

@@ -63,8 +63,11 @@ struct AttnArgs {
   float m_static = 0.f;           // > 0: fixed softmax base (log2 units) bounding every logit; 0: online max
   int32_t debug_flags = 0;        // diagnostics only (DZ_DEBUG_KERNEL env): 1 no K/V TMA (results are garbage)
   int32_t grid = 0;               // persistent CTAs (<= #SMs)
+  float* ws = nullptr;            // stream-K piece workspace: [2 * pairs][2 ranks][(D + 2) * 128] fp32 (nullptr: no split)
+  int32_t* ws_cnt = nullptr;      // per (unit, rank) piece counters, zero between launches
 };
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);
+constexpr int kMaxPairs = 80;  // CTA pairs of the persistent grid (B200: 74)
 int attention_units(int32_t B, int32_t H, int32_t nq);
 constexpr int kTileQ = 256, kTileK = 256;  // skip / mask decision granularity (query rows of a CTA pair x keys of a step)
 cudaError_t read_watchdog(uint32_t* host8);   // {fired, block, warp, bar addr, parity, smid, bars base, 0}

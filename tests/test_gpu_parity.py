@@ -92,8 +92,9 @@ def test_determinism_and_cache_unchanged():
 
 
 def test_tile_map_matches_oracle_classifier():
+    import paper_2602_15922_b200 as dz
     w = synth.workload("C1")
-    run = GpuRun(w)
+    run = GpuRun(w, flags=dz.FLAG_TILE_MAP)
     run.fill()
     run.attend()
     torch.cuda.synchronize()

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 CLEAN, NOISY = synth.CLEAN, synth.NOISY
 
 
-def _cache(w, capacity, max_chunk, flags=0, gq=None, gk=None):
+def _cache(w, capacity, max_chunk, flags=8, gq=None, gk=None):   # 8 = FLAG_TILE_MAP
     import paper_2602_15922_b200 as dz
     dev = torch.device("cuda")
     if gq is None:
@@ -169,7 +169,7 @@ def test_online_softmax_spans():
     w = synth.scaled(synth.workload("C1"), heads=2)
     spans = synth.teacher_forcing_spans(3, 640)
     q, k, v, pos = synth.span_inputs(w, spans)
-    cache, gq, gk = _cache(w, 0, q.shape[0], flags=dz.FLAG_ONLINE_SOFTMAX)
+    cache, gq, gk = _cache(w, 0, q.shape[0], flags=dz.FLAG_ONLINE_SOFTMAX | dz.FLAG_TILE_MAP)
     out = _run(cache, spans, q, k, v, pos).cpu().double().numpy()
     want, _, _ = _oracle_spans(w, gq, gk, spans, q, k, v, pos)
     assert_parity(out, want, "online spans")
