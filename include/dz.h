@@ -233,6 +233,34 @@ DZ_API dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset);
  * to n words of the last trace.  Synchronous. */
 DZ_API dz_status dz_debug_trace(int32_t enable, uint32_t* host, size_t n);
 
+/* One transfer of the Ulysses all-to-all: this rank sends
+ * `bytes` at storage + send_off to rank `peer` and receives `bytes` from it at
+ * storage + recv_off (offsets into the caller's cache_storage).  tensor: 0 Q',
+ * 1 K', 2 V, 3 O. */
+typedef struct {
+  int32_t peer;
+  int32_t tensor;
+  int64_t send_off;
+  int64_t recv_off;
+  int64_t bytes;
+} dz_xfer;
+
+/* The exchange plan the library issues (as one grouped ncclSend/ncclRecv per
+ * entry) for an n_tokens chunk in the context's current cache state: phase 0
+ * = attend pre-exchange (sequence shard -> head shard of Q', K', V: K'/V land
+ * in the cache staging slots), 1 = append pre-exchange (K', V), 2 = attend
+ * post-exchange (O head shard -> the receive buffer unpacked by K5).  Copies
+ * up to cap entries to out (may be NULL) and returns the entry count, or a
+ * negative dz_status.  Host only, no device access: lets host-side tests check
+ * the plan with any process-group backend. */
+DZ_API int32_t dz_sp_plan(const dz_ctx* ctx, int32_t phase, int32_t n_tokens, dz_xfer* out, int32_t cap);
+
+/* K5 (the post-exchange unpack) on its own, for tests: recv bf16
+ * [world_size][batch][n_local][heads_local][head_dim] -> out bf16
+ * [batch][n_local][world_size * heads_local][head_dim], enqueued on stream. */
+DZ_API dz_status dz_debug_sp_unpack(const void* recv, void* out, int32_t world_size, int32_t batch, int32_t n_local,
+                                    int32_t heads_local, int32_t head_dim, void* stream);
+
 /* Number of attention work units (batch x heads/world_size x query-tile pairs)
  * for an n-token chunk; the persistent grid is min(units, SM count). */
 DZ_API int32_t dz_attention_units(const dz_ctx* ctx, int32_t n_tokens);

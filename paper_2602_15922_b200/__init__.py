@@ -59,6 +59,11 @@ class DzConfig(ctypes.Structure):
     ]
 
 
+class DzXfer(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("tensor", ctypes.c_int32), ("send_off", ctypes.c_int64),
+                ("recv_off", ctypes.c_int64), ("bytes", ctypes.c_int64)]
+
+
 class DzSpan(ctypes.Structure):
     _fields_ = [("chunk_id", ctypes.c_int32), ("kind", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
                 ("pos_thw", ctypes.c_void_p)]
@@ -86,6 +91,8 @@ SIGNATURES = [
     ("dz_nccl_comm_init", I32, [I32, P, I32, ctypes.POINTER(P)]),
     ("dz_nccl_comm_destroy", I32, [P]),
     ("dz_attention_units", I32, [P, I32]),
+    ("dz_sp_plan", I32, [P, I32, I32, ctypes.POINTER(DzXfer), I32]),
+    ("dz_debug_sp_unpack", I32, [P, P, I32, I32, I32, I32, I32, P]),
     ("dz_debug_watchdog", I32, [P, I32]),
     ("dz_profile_last", I32, [P, P]),
     ("dz_debug_trace", I32, [I32, P, SZ]),

@@ -17,6 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdz.so")
+TRACE_LIB = os.path.join(HERE, "libdz_trace.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -46,14 +47,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True builds the diagnostics variant libdz_trace.so (-DDZ_TRACE: K2 cycle trace and
+    per-CTA timeline, see dz_debug_trace); tools load it through DZ_LIB_PATH."""
+    out = TRACE_LIB if trace else LIB
+    extra = os.environ.get("DZ_BUILD_EXTRA", "").split()  # experiments: extra nvcc flags ...
+    if extra:
+        out = os.environ["DZ_BUILD_OUT"]                      # ... built into a separate library
+    if not force and not trace and not extra and up_to_date():
         return LIB
     inc, lib = nccl_dirs()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build_x" if extra else ("build_trace" if trace else "build"))
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", *ARCH,
-              "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
+              "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc] + (["-DDZ_TRACE"] if trace else []) + extra
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
@@ -66,16 +73,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-L", lib, "-l:libnccl.so.2",
             "-Xlinker", f"-rpath,{lib}", "-lrt", "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.check_call(link)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, trace="--trace" in sys.argv))

@@ -58,7 +58,7 @@ constexpr int BM = 128;           // query rows per CTA (MMA M = 256 per pair)
 constexpr int BN = 256;           // keys per KV step
 constexpr int kThreads = 384;     // 12 warps
 constexpr float kRescaleLog2 = 8.0f;
-constexpr int kPolyPairs = 2;     // of every 8 exp2 pairs, this many go to the FMA-pipe polynomial
+constexpr int kPolyPairs = 3;     // of every 8 exp2 pairs, this many go to the FMA-pipe polynomial (measured best of 2/3/4)
 constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr int kWarpMma = 11, kWarpTma = 10, kWarpPv = 9, kWarpTmem = 8;
 constexpr uint32_t kRegsLight = 88, kRegsSoftmax = 208;  // setmaxnreg: 128*88 + 256*208 = 384*168 (launch)
@@ -67,7 +67,23 @@ constexpr uint32_t kRegsLight = 88, kRegsSoftmax = 208;  // setmaxnreg: 128*88 +
 // rank r at [r * 16 * kTraceSteps]: per step j [8j+0,1] QK wait/issue,
 // [8j+2,3] PV wait/issue (of step j), [8j+4,5] softmax S-ready / P-done
 // (warp 0), [8j+6] S loaded, [8j+7] exp done.
+#ifdef DZ_TRACE
+constexpr bool kTrace = true;   // diagnostics build (libdz_trace.so): cycle trace + per-CTA timeline
+#else
+constexpr bool kTrace = false;  // production build: every trace statement below compiles away
+#endif
 constexpr int kTraceSteps = 256;
+#ifndef DZ_SP
+#define DZ_SP 0
+#endif
+// scheduling points of the softmax loop (experiment switch DZ_SP)
+#if DZ_SP == 1
+#define SCHED_POINT() do { uint32_t c_; asm volatile("mov.u32 %0, %%clock;" : "=r"(c_)); } while (0)
+#elif DZ_SP == 2
+#define SCHED_POINT() do { if (g_dz_trace_on == 12345) asm volatile("trap;"); } while (0)
+#else
+#define SCHED_POINT() do { } while (0)
+#endif
 __device__ uint32_t g_dz_trace[kTraceSteps * 32];
 __device__ int g_dz_trace_on;
 // Per-CTA timeline (globaltimer ns, low 32 bits), softmax warp 0 lane 0 of every CTA:
@@ -302,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int n_units = B * H * n_groups;
   const int nkv = (kv_len + BN - 1) / BN;                  // 256-key steps
   const int cid = (int)ptx::cluster_id_x(), ncl = (int)ptx::nclusters_x();
-  const bool trace_on = g_dz_trace_on != 0 && cid == 0;
+  const bool trace_on = kTrace && g_dz_trace_on != 0 && cid == 0;
   uint32_t* const trace = g_dz_trace + rank * kTraceSteps * 16;
   constexpr uint16_t kBoth = 0x3;
 
@@ -524,7 +540,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     Sched sc = sched0;
     Seg sg;
     bool first_seg = true;
-    const bool tl = g_dz_trace_on != 0 && threadIdx.x == 0 && blockIdx.x < kTimelineCtas;
+    const bool tl = kTrace && g_dz_trace_on != 0 && threadIdx.x == 0 && blockIdx.x < kTimelineCtas;
     uint32_t* const tline = g_dz_timeline + blockIdx.x * kTimelineWords;
     int n_seg = 0, n_comb = 0, n_part = 0;
     if (tl) {
@@ -552,6 +568,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         s_phase ^= 1;
         const bool tr = trace_on && first_seg && j < kTraceSteps && row == 0 && hc == 0;
         if (tr) trace[j * 8 + 4] = (uint32_t)clock();
+        SCHED_POINT();
         ptx::tc_fence_after();
         float s[128];
         {
@@ -567,6 +584,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->s_free[hc]));
         if (tr) trace[j * 8 + 6] = (uint32_t)clock();
+        SCHED_POINT();
         if (masked) {  // Fig. 10 mask and key bounds for this warp's 128 keys
           uint32_t vm[4];
           visible_bits(st, qs, j * BN + 128 * hc, kv_len, vm);
@@ -626,6 +644,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             exp_half<false>(s + 64 * half, nb2, pk, acc);
           if (half == 0) {
             if (tr) trace[j * 8 + 7] = (uint32_t)clock();
+        SCHED_POINT();
             // P may be overwritten once PV(j-1) has read it
             ptx::mbar_wait(bar(bars->p_empty), pe_phase ^ 1);
             pe_phase ^= 1;
@@ -644,6 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->p_full));
         if (tr) trace[j * 8 + 5] = (uint32_t)clock();
+        SCHED_POINT();
       }
       first_seg = false;
       if (tl && n_seg < kTlSegs) tline[9 + 4 * n_seg] = (uint32_t)clock();

@@ -186,39 +186,52 @@ dz_status nccl_check(dz_ctx* c, ncclResult_t r, const char* what) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Ulysses exchange plan: for tensor X of rank r, the block that
-// goes to peer p for batch element b, and where the block from peer p lands.
-struct Xfer {
-  const void* send;
-  void* recv;
-  size_t bytes;
-};
-
-// pre-attention: seq shard [n_loc, H] -> head shard [n, Hl]; which: 0 q, 1 k, 2 v
-Xfer pre_xfer(const dz_ctx* c, int which, int p, int b, int64_t n) {
+// Ulysses exchange plan: per (tensor, peer p, batch element b),
+// the block this rank sends to p and where the block it receives from p lands,
+// as byte offsets into the caller's storage.  One source of truth for the NCCL
+// calls below and for dz_sp_plan (host-side tests of the plan).
+//   phase 0 (attend) / 1 (append): seq shard [n_loc, H] -> head shard [n, Hl] for
+//     Q' (phase 0 only), K', V; the send layout is [N][B][n_loc][Hl][D] (written by
+//     K1), Q' lands in the Q' scratch [B][n][Hl][D], K'/V in the cache staging slots
+//     [start + valid + p * n_loc, ...) of batch element b;
+//   phase 2 (post): O head shard [B][n][Hl][D] -> the receive buffer [N][B][n_loc][Hl][D]
+//     (K5 then unpacks it to [B][n_loc][H][D]).
+std::vector<dz_xfer> make_plan(const dz_ctx* c, int phase, int64_t n) {
+  std::vector<dz_xfer> v;
   const int64_t n_loc = n / c->N;
-  const size_t blk = (size_t)n_loc * c->Hl * c->D * 2;
-  const size_t so = (which == 0 ? c->L.sq_off : which == 1 ? c->L.sk_off : c->L.sv_off);
-  Xfer x;
-  x.send = c->base + so + ((size_t)p * c->B + b) * blk;
-  x.bytes = blk;
-  const int64_t slot = c->start + c->valid + (int64_t)p * n_loc;
-  if (which == 0)
-    x.recv = c->base + c->L.q_off + ((size_t)b * n + (size_t)p * n_loc) * c->Hl * c->D * 2;
-  else
-    x.recv = which == 1 ? c->kslot(b, slot) : c->vslot(b, slot);
-  return x;
-}
-
-// post-attention: O head shard [n, Hl] -> seq shard [n_loc, H] (receive side packed [N][B][n_loc][Hl][D])
-Xfer post_xfer(const dz_ctx* c, int p, int b, int64_t n) {
-  const int64_t n_loc = n / c->N;
-  const size_t blk = (size_t)n_loc * c->Hl * c->D * 2;
-  Xfer x;
-  x.send = c->base + c->L.ol_off + ((size_t)b * n + (size_t)p * n_loc) * c->Hl * c->D * 2;
-  x.recv = c->base + c->L.or_off + ((size_t)p * c->B + b) * blk;
-  x.bytes = blk;
-  return x;
+  const int64_t row = (int64_t)c->Hl * c->D * 2;  // one token of one rank's heads
+  const int64_t blk = n_loc * row;
+  if (phase == 0 || phase == 1) {
+    for (int which = phase == 0 ? 0 : 1; which < 3; ++which) {
+      const int64_t so = (int64_t)(which == 0 ? c->L.sq_off : which == 1 ? c->L.sk_off : c->L.sv_off);
+      for (int p = 0; p < c->N; ++p)
+        for (int b = 0; b < c->B; ++b) {
+          dz_xfer x;
+          x.peer = p;
+          x.tensor = which;
+          x.bytes = blk;
+          x.send_off = so + ((int64_t)p * c->B + b) * blk;
+          const int64_t slot = c->start + c->valid + (int64_t)p * n_loc;
+          if (which == 0)
+            x.recv_off = (int64_t)c->L.q_off + ((int64_t)b * n + (int64_t)p * n_loc) * row;
+          else
+            x.recv_off = (int64_t)(which == 1 ? c->L.k_off : c->L.v_off) + ((int64_t)b * c->L.slots + slot) * row;
+          v.push_back(x);
+        }
+    }
+  } else {
+    for (int p = 0; p < c->N; ++p)
+      for (int b = 0; b < c->B; ++b) {
+        dz_xfer x;
+        x.peer = p;
+        x.tensor = 3;
+        x.bytes = blk;
+        x.send_off = (int64_t)c->L.ol_off + ((int64_t)b * n + (int64_t)p * n_loc) * row;
+        x.recv_off = (int64_t)c->L.or_off + ((int64_t)p * c->B + b) * blk;
+        v.push_back(x);
+      }
+  }
+  return v;
 }
 
 dz_status check_ready(dz_ctx* c) {
@@ -297,39 +310,23 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
   return cuda_check(c, dz::launch_prologue(a, st), "prologue launch");
 }
 
-dz_status exchange_pre(dz_ctx* c, bool with_q, int64_t n, cudaStream_t st) {
+// one grouped NCCL send/recv per plan entry (all peers, all tensors) on the caller's stream
+dz_status run_exchange(dz_ctx* c, int phase, int64_t n, cudaStream_t st) {
+  const std::vector<dz_xfer> plan = make_plan(c, phase, n);
   dz_status r = nccl_check(c, ncclGroupStart(), "ncclGroupStart");
   if (r) return r;
-  for (int which = with_q ? 0 : 1; which < 3; ++which)
-    for (int p = 0; p < c->N; ++p)
-      for (int b = 0; b < c->B; ++b) {
-        // what this rank sends to p, and what it receives from p
-        const Xfer x = pre_xfer(c, which, p, b, n);
-        r = nccl_check(c, ncclSend(x.send, x.bytes, ncclUint8, p, c->comm, st), "ncclSend");
-        if (!r) r = nccl_check(c, ncclRecv(x.recv, x.bytes, ncclUint8, p, c->comm, st), "ncclRecv");
-        if (r) {
-          ncclGroupEnd();
-          return r;
-        }
-      }
-  return nccl_check(c, ncclGroupEnd(), "ncclGroupEnd");
-}
-
-dz_status exchange_post(dz_ctx* c, int64_t n, cudaStream_t st) {
-  dz_status r = nccl_check(c, ncclGroupStart(), "ncclGroupStart");
-  if (r) return r;
-  for (int p = 0; p < c->N; ++p)
-    for (int b = 0; b < c->B; ++b) {
-      const Xfer x = post_xfer(c, p, b, n);
-      r = nccl_check(c, ncclSend(x.send, x.bytes, ncclUint8, p, c->comm, st), "ncclSend");
-      if (!r) r = nccl_check(c, ncclRecv(x.recv, x.bytes, ncclUint8, p, c->comm, st), "ncclRecv");
-      if (r) {
-        ncclGroupEnd();
-        return r;
-      }
+  for (const dz_xfer& x : plan) {
+    r = nccl_check(c, ncclSend(c->base + x.send_off, (size_t)x.bytes, ncclUint8, x.peer, c->comm, st), "ncclSend");
+    if (!r) r = nccl_check(c, ncclRecv(c->base + x.recv_off, (size_t)x.bytes, ncclUint8, x.peer, c->comm, st), "ncclRecv");
+    if (r) {
+      ncclGroupEnd();
+      return r;
     }
+  }
   return nccl_check(c, ncclGroupEnd(), "ncclGroupEnd");
 }
+dz_status exchange_pre(dz_ctx* c, bool with_q, int64_t n, cudaStream_t st) { return run_exchange(c, with_q ? 0 : 1, n, st); }
+dz_status exchange_post(dz_ctx* c, int64_t n, cudaStream_t st) { return run_exchange(c, 2, n, st); }
 
 // K2 over local heads and the full sequence: committed slots + the staged chunk.
 dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* out_local, int64_t o_bstride,
@@ -361,7 +358,9 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   a.grid = 2 * std::min(c->num_sms / 2, dz::kMaxPairs);
   // stream-K needs <= 64 query groups and 32-bit step arithmetic (W * pairs < 2^31); else whole units round-robin
   const int64_t n_groups = (n + dz::kTileQ - 1) / dz::kTileQ, n_steps = (kv_len + dz::kTileK - 1) / dz::kTileK;
-  const bool streamk = n_groups <= 64 && (int64_t)c->B * c->Hl * n_groups * n_steps * dz::kMaxPairs < (1ll << 31);
+  static const bool rr_forced = getenv("DZ_SCHED_RR") != nullptr;  // diagnostics: whole units round-robin
+  const bool streamk = !rr_forced && n_groups <= 64 &&
+                       (int64_t)c->B * c->Hl * n_groups * n_steps * dz::kMaxPairs < (1ll << 31);
   a.ws = streamk ? reinterpret_cast<float*>(c->base + c->L.ws_off) : nullptr;
   a.ws_cnt = reinterpret_cast<int32_t*>(c->base + c->L.cnt_off);
   if (!c->ws_zeroed) {  // piece counters start at zero; every combine resets its own
@@ -726,6 +725,24 @@ dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset) {
 
 dz_status dz_debug_trace(int32_t enable, uint32_t* host, size_t n) {
   return dz::trace_control(enable, host, n) == cudaSuccess ? DZ_OK : DZ_ECUDA;
+}
+
+int32_t dz_sp_plan(const dz_ctx* c, int32_t phase, int32_t n_tokens, dz_xfer* out, int32_t cap) {
+  if (!c || phase < 0 || phase > 2 || n_tokens <= 0 || n_tokens % c->N || cap < 0) return DZ_EINVAL;
+  const std::vector<dz_xfer> plan = make_plan(c, phase, n_tokens);
+  if (out)
+    for (int32_t i = 0; i < (int32_t)plan.size() && i < cap; ++i) out[i] = plan[i];
+  return (int32_t)plan.size();
+}
+
+dz_status dz_debug_sp_unpack(const void* recv, void* out, int32_t world_size, int32_t batch, int32_t n_local,
+                             int32_t heads_local, int32_t head_dim, void* stream) {
+  if (!recv || !out || world_size <= 0 || batch <= 0 || n_local < 0 || heads_local <= 0 || head_dim % 8)
+    return DZ_EINVAL;
+  return dz::launch_sp_unpack(recv, out, world_size, batch, n_local, heads_local, head_dim,
+                              static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? DZ_OK
+             : DZ_ECUDA;
 }
 
 int32_t dz_attention_units(const dz_ctx* c, int32_t n) {

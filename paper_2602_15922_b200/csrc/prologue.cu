@@ -9,15 +9,16 @@
 // multiplied by softmax_scale * log2(e), so the attention kernel's scores come
 // out of the tensor core already in log2 units (one FMA per score saved).
 //
-// Layout: one CTA per (token, batch element).  Every thread first issues
-// all of its 16-byte loads for the token (3 tensors x kPer heads in flight), and
-// only then do two warps compute the token's D/2 rotation angles (fp64 sincos
-// of p_a * omega_j) into shared memory, so the angle latency hides under the
-// HBM latency instead of preceding it.  A row is handled by D/8 threads with
-// one 16-byte load and one 16-byte store each; the row's sum of squares is
-// reduced with __shfl_xor inside that thread group.  Heads are walked with
-// loop counters (no runtime integer division per row).  HBM-bound by design: per
-// token it moves (read + write) 2 B x D x H for each of Q, K, V.
+// Layout: a persistent grid (2 CTAs per SM) walks the (batch, token) items.
+// Each item's Q, K, V rows are contiguous H x D blocks in the [B][n][H][D]
+// input, so one thread issues three 1D bulk copies (cp.async.bulk, TMA) per
+// item into a kStages-deep shared-memory ring, kStages - 1 items ahead of the
+// one being processed: HBM reads stay in flight while the CTA computes.  The
+// token's D/2 rotation angles (fp64 sincos of p_a * omega_j) go to shared
+// memory.  A row of D elements is handled by D/8 threads with one 16-byte
+// shared load and one 16-byte global store each; its sum of squares is reduced
+// with __shfl_xor inside that thread group.  HBM-bound by design: per token it
+// moves (read + write) 2 B x D x H for each of Q, K, V.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -25,11 +26,13 @@
 #include <algorithm>
 
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace dz {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kMaxStageBytes = 96 * 1024;  // ring size cap: 2 CTAs per SM
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -40,115 +43,200 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   }
 }
 
-// read-once activations: non-coherent path, no L1 allocation
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
-
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads) prologue_kernel(const PrologueArgs a) {
-  constexpr int G = D / 8;             // threads per row (one 16-byte vector each)
-  constexpr int kGroups = kThreads / G;  // rows processed side by side
-  constexpr int kPer = 3;              // heads per thread and tensor in one pass
-  __shared__ float2 cs[D / 2];         // (cos, sin) per pair of this token
-  const int t = blockIdx.x;
-  const int b = blockIdx.y;
-  const int tid = threadIdx.x;
-  const int g = tid / G;               // row group
-  const int li = tid % G;              // 8-element slice index inside the row
-  const int H = a.H;
-  const int64_t xrow0 = (int64_t)b * a.x_bstride + (int64_t)t * H * D;
+// shared-memory carve-up for H heads, nt tensors present, S stages
+struct ProSmem {
+  int row_bytes, stage_bytes, S;
+  __host__ __device__ ProSmem(int H, int D, int nt) {
+    row_bytes = H * D * 2;
+    stage_bytes = nt * row_bytes;
+    S = kMaxStageBytes / stage_bytes;
+    S = S < 2 ? 2 : (S > 4 ? 4 : S);
+  }
+  __host__ __device__ int cs_off() const { return S * stage_bytes; }           // float2 [S][D/2]
+  __host__ __device__ int row_off(int D) const { return cs_off() + S * (D / 2) * 8; }  // int64 [H]
+  __host__ __device__ int bar_off(int D, int H) const { return (row_off(D) + H * 8 + 7) / 8 * 8; }
+  __host__ __device__ int total(int D, int H) const { return bar_off(D, H) + S * 8 + 16; }
+};
 
-  // passes over blocks of kGroups * kPer heads (one pass for H <= 48 at D = 128); the trip
-  // count is block-uniform, so the __syncthreads below is reached by every thread
-  for (int h0 = 0; h0 < H; h0 += kGroups * kPer) {
-    uint4 in[3][kPer];
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) prologue_kernel(const PrologueArgs a) {
+  constexpr int G = D / 8;               // threads per row (one 16-byte vector each)
+  constexpr int kGroups = kThreads / G;  // rows processed side by side
+  constexpr int kPer = 3;                // heads per thread in one pass (H <= 48 at D = 128: one pass)
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int H = a.H, tid = threadIdx.x;
+  const int g = tid / G, li = tid % G;
+  int nt = 0, slot_of[3];
+#pragma unroll
+  for (int w = 0; w < 3; ++w) slot_of[w] = a.x[w] != nullptr ? nt++ : -1;
+  const ProSmem L(H, D, nt);
+  float2* cs = reinterpret_cast<float2*>(sm + L.cs_off());
+  int64_t* rowoff = reinterpret_cast<int64_t*>(sm + L.row_off(D));
+  const uint32_t bar0 = ptx::smem_u32(sm + L.bar_off(D, H));
+  const uint32_t ring = ptx::smem_u32(sm);
+  // output row offset of head h (destination rank block, local head): one division per head, here only
+  for (int h = tid; h < H; h += kThreads) {
+    const int dest = h / a.heads_per_dest;
+    rowoff[h] = (int64_t)dest * a.y[0].dstride + (int64_t)(h - dest * a.heads_per_dest) * D;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < L.S; ++s) ptx::mbar_init(bar0 + 8 * s, 1);
+    ptx::fence_mbar_init();
+  }
+  const int n_items = a.B * a.n;
+  const uint64_t pol = ptx::l2_policy_evict_first();  // activations are read once
+  auto issue = [&](int k) {  // bulk loads of this CTA's k-th item into stage k % S
+    const int item = blockIdx.x + k * gridDim.x;
+    if (item >= n_items) return;
+    const int b = item / a.n, t = item - b * a.n;
+    const uint32_t st = (uint32_t)(k % L.S), bar = bar0 + 8 * st;
+    ptx::mbar_arrive_expect_tx(bar, (uint32_t)L.stage_bytes);
+    const int64_t src = ((int64_t)b * a.x_bstride + (int64_t)t * H * D) * 2;
 #pragma unroll
     for (int w = 0; w < 3; ++w)
+      if (slot_of[w] >= 0)
+        ptx::bulk_load(ring + st * L.stage_bytes + slot_of[w] * L.row_bytes,
+                       static_cast<const uint8_t*>(a.x[w]) + src, (uint32_t)L.row_bytes, bar, pol);
+  };
+  // the token's D/2 rotation angles, one per 4th thread so every warp takes a share of the fp64 sincos
+  auto angles = [&](int k) {
+    const int item = blockIdx.x + k * gridDim.x;
+    if (item >= n_items || (tid & 3) != 0) return;
+    const int ai = tid >> 2;  // 0 .. 63 >= D/2 - 1
+    if (ai >= D / 2) return;
+    const int t = item % a.n;
+    const double p = (double)__ldg(a.pos + 3 * t + a.axis[ai]);
+    double sn, cn;
+    sincos(p * a.omega[ai], &sn, &cn);
+    cs[(k % L.S) * (D / 2) + ai] = make_float2((float)cn, (float)sn);
+  };
+  __syncthreads();  // barriers initialised, row offsets visible
+  if (tid == 0)
+    for (int k = 0; k < L.S - 1; ++k) issue(k);
+  // gains of this thread's heads (h = g + kGroups * i) and column slice, kept in registers
+  const bool gains_in_regs = H <= kGroups * kPer;
+  float gq[kPer][8], gk[kPer][8];
 #pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const int h = h0 + g + k * kGroups;
-        const uint4* src = reinterpret_cast<const uint4*>(a.x[w]);
-        in[w][k] = (src != nullptr && h < H) ? ld_stream(src + (xrow0 + (int64_t)h * D) / 8 + li)
-                                             : make_uint4(0, 0, 0, 0);
-      }
-    if (h0 == 0) {  // the token's rotation angles while the loads are in flight
-      if (tid < D / 2) {
-        const double p = (double)__ldg(a.pos + 3 * t + a.axis[tid]);
-        double sn, cn;
-        sincos(p * a.omega[tid], &sn, &cn);
-        cs[tid] = make_float2((float)cn, (float)sn);
-      }
-      __syncthreads();
-    }
-    int64_t row_off[kPer];  // output row offset (without the tensor base) of head h
+  for (int i = 0; i < kPer; ++i) {
+    const int h = g + kGroups * i;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int h = h0 + g + k * kGroups;
-      const int dest = h / a.heads_per_dest, hl = h - dest * a.heads_per_dest;
-      row_off[k] = (int64_t)dest * a.y[0].dstride + (int64_t)hl * D;  // dstride is the same for q, k, v slots
+    for (int e = 0; e < 8; ++e) {
+      gq[i][e] = (gains_in_regs && h < H && a.gain[0]) ? __ldg(a.gain[0] + h * D + li * 8 + e) : 0.f;
+      gk[i][e] = (gains_in_regs && h < H && a.gain[1]) ? __ldg(a.gain[1] + h * D + li * 8 + e) : 0.f;
     }
+  }
+  angles(0);
+
+  for (int k = 0;; ++k) {
+    const int item = blockIdx.x + k * gridDim.x;
+    if (item >= n_items) break;
+    const int b = item / a.n, t = item - b * a.n;
+    const int st = k % L.S;
+    if (tid == 0) issue(k + L.S - 1);  // its stage was released by the __syncthreads ending item k - 1
+    ptx::mbar_wait(bar0 + 8 * st, (uint32_t)((k / L.S) & 1));
+    __syncthreads();  // angles of item k visible (written before the barrier that ended item k - 1)
+    const uint8_t* stage = sm + st * L.stage_bytes;
+    const float2* csk = cs + st * (D / 2);
 #pragma unroll
     for (int w = 0; w < 3; ++w) {
-      if (a.x[w] == nullptr) continue;  // block-uniform
+      if (slot_of[w] < 0) continue;  // block-uniform
       const OutSlot& o = a.y[w];
       const int64_t base = (int64_t)b * o.bstride + (int64_t)t * o.tstride;
+      const uint8_t* src = stage + slot_of[w] * L.row_bytes;
+      for (int h0 = 0; h0 < H; h0 += kGroups * kPer) {  // block-uniform trip count (one pass for H <= 48)
+        uint4 v[kPer];
 #pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const int h = h0 + g + k * kGroups;
+        for (int i = 0; i < kPer; ++i) {
+          const int h = h0 + g + kGroups * i;
+          v[i] = h < H ? *reinterpret_cast<const uint4*>(src + (h * D + li * 8) * 2) : make_uint4(0, 0, 0, 0);
+        }
         if (w == 2) {  // V: unchanged bf16 copy into the cache / send slot
-          if (h < H) reinterpret_cast<uint4*>(o.base)[(base + row_off[k]) / 8 + li] = in[w][k];
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) {
+            const int h = h0 + g + kGroups * i;
+            if (h < H) reinterpret_cast<uint4*>(o.base)[(base + rowoff[h]) / 8 + li] = v[i];
+          }
           continue;
         }
-        float f[8];
-        bf16x8_to_f32(in[w][k], f);
-        float ss = 0.f;
+        float f[kPer][8], ss[kPer];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) ss = fmaf(f[i], f[i], ss);
-        // every lane takes part (the two row groups of a warp may differ in validity)
+        for (int i = 0; i < kPer; ++i) {
+          bf16x8_to_f32(v[i], f[i]);
+          ss[i] = 0.f;
 #pragma unroll
-        for (int m = G / 2; m >= 1; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
-        if (h >= H) continue;
-        const float inv = rsqrtf(ss * (1.0f / D) + a.eps);
-        const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
-        const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
-        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-        const float sc = w == 0 ? a.q_scale : 1.f;  // Q' leaves pre-scaled by softmax_scale*log2(e)
-        uint32_t pk[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float u = f[2 * i] * inv * gg[2 * i];
-          const float v = f[2 * i + 1] * inv * gg[2 * i + 1];
-          const float2 c = cs[li * 4 + i];
-          pk[i] = pack_half2((u * c.x - v * c.y) * sc, (u * c.y + v * c.x) * sc);
+          for (int e = 0; e < 8; ++e) ss[i] = fmaf(f[i][e], f[i][e], ss[i]);
         }
-        reinterpret_cast<uint4*>(o.base)[(base + row_off[k]) / 8 + li] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+#pragma unroll
+        for (int m = G / 2; m >= 1; m >>= 1)
+#pragma unroll
+          for (int i = 0; i < kPer; ++i) ss[i] += __shfl_xor_sync(0xffffffffu, ss[i], m);
+        const float sc = w == 0 ? a.q_scale : 1.f;  // Q' leaves pre-scaled by softmax_scale*log2(e)
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int h = h0 + g + kGroups * i;
+          if (h >= H) continue;
+          const float inv = rsqrtf(ss[i] * (1.0f / D) + a.eps);
+          float gg[8];
+          if (gains_in_regs) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) gg[e] = w == 0 ? gq[i][e] : gk[i][e];
+          } else {
+            const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
+            const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
+            gg[0] = g0.x; gg[1] = g0.y; gg[2] = g0.z; gg[3] = g0.w;
+            gg[4] = g1.x; gg[5] = g1.y; gg[6] = g1.z; gg[7] = g1.w;
+          }
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float u = f[i][2 * e] * inv * gg[2 * e];
+            const float x = f[i][2 * e + 1] * inv * gg[2 * e + 1];
+            const float2 c = csk[li * 4 + e];
+            pk[e] = pack_half2((u * c.x - x * c.y) * sc, (u * c.y + x * c.x) * sc);
+          }
+          reinterpret_cast<uint4*>(o.base)[(base + rowoff[h]) / 8 + li] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
       }
     }
+    angles(k + 1);    // next item's angles into its own slot, off the critical path of the copies
+    __syncthreads();  // stage and angles of item k may be refilled
   }
 }
 
 }  // namespace
 
+template <int D>
+cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
+  int nt = 0;
+  for (int w = 0; w < 3; ++w) nt += a.x[w] != nullptr;
+  const ProSmem L(a.H, D, nt);
+  const int smem = L.total(D, a.H);
+  if (L.stage_bytes > 2 * kMaxStageBytes) return cudaErrorInvalidValue;  // heads beyond the ring's reach
+  auto k = prologue_kernel<D>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int items = a.B * a.n;
+  const int grid = items < 2 * sms ? items : 2 * sms;
+  k<<<grid, kThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prologue(const PrologueArgs& a, cudaStream_t s) {
   if (a.n == 0 || a.B == 0) return cudaSuccess;
-  dim3 grid(a.n, a.B);
-  if (a.D == 128)
-    prologue_kernel<128><<<grid, kThreads, 0, s>>>(a);
-  else if (a.D == 64)
-    prologue_kernel<64><<<grid, kThreads, 0, s>>>(a);
-  else
-    return cudaErrorInvalidValue;
-  return cudaGetLastError();
+  if (a.D == 128) return launch_pro<128>(a, s);
+  if (a.D == 64) return launch_pro<64>(a, s);
+  return cudaErrorInvalidValue;
 }
 
 // K5: [N src][B][n_loc][Hl][D] -> [B][n_loc][H = N*Hl][D], one 16-byte vector per thread.

@@ -229,3 +229,18 @@ def test_large_gains_stress_online_path():
     scale = max(1.0, float(np.abs(want).max()))
     assert np.isfinite(out).all()
     assert rel_fro <= 5e-3 and max_abs <= 2e-2 * scale, (max_abs, rel_fro, scale)
+
+
+@pytest.mark.parametrize("N,B,nl,Hl,D", [(2, 1, 1344, 20, 128), (8, 2, 336, 5, 128), (4, 1, 37, 3, 64)])
+def test_sp_unpack_kernel(N, B, nl, Hl, D):
+    # K5: receive blocks [N][B][n_loc][Hl][D] -> [B][n_loc][N*Hl][D] (the post-exchange layout of SP)
+    import paper_2602_15922_b200 as dz
+    g = torch.Generator().manual_seed(N * 1000 + nl)
+    recv = torch.randn(N, B, nl, Hl, D, generator=g).to(torch.bfloat16).cuda()
+    out = torch.empty(B, nl, N * Hl, D, dtype=torch.bfloat16, device="cuda")
+    s = dz.lib().dz_debug_sp_unpack(recv.data_ptr(), out.data_ptr(), N, B, nl, Hl, D,
+                                    torch.cuda.current_stream().cuda_stream)
+    assert s == 0
+    torch.cuda.synchronize()
+    want = recv.permute(1, 2, 0, 3, 4).reshape(B, nl, N * Hl, D)
+    assert torch.equal(out, want)
