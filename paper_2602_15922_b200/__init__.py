@@ -315,7 +315,9 @@ class ChunkKVCache:
             return self.storage[off:off + nb].view(dt).view(tokens, self.heads_local, self.head_dim)
         return view(k0.value, torch.float16), view(v0.value, torch.bfloat16)
 
-    def tile_map(self) -> np.ndarray:
+    def tile_map(self, with_tiles: bool = False):
+        """The kernel's tile decisions of the last attend for (b, h) = (0, 0) (needs FLAG_TILE_MAP):
+        uint8 [query tiles][key steps], 0 SKIP / 1 PARTIAL / 2 FULL; with_tiles: (map, bm, bn)."""
         nq, nk, bm, bn = I32(), I32(), I32(), I32()
         self._check(lib().dz_get_tile_map(self._ctx, None, 0, ctypes.byref(nq), ctypes.byref(nk),
                                           ctypes.byref(bm), ctypes.byref(bn)), "dz_get_tile_map")
@@ -323,7 +325,7 @@ class ChunkKVCache:
         self._check(lib().dz_get_tile_map(self._ctx, buf.ctypes.data, buf.size, ctypes.byref(nq),
                                           ctypes.byref(nk), ctypes.byref(bm), ctypes.byref(bn)),
                     "dz_get_tile_map")
-        return buf
+        return (buf, bm.value, bn.value) if with_tiles else buf
 
     def lse(self, n: int, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
         out = torch.empty(self.batch, self.heads_local, n, dtype=torch.float32, device=self.device)

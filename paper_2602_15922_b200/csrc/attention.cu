@@ -97,12 +97,16 @@ __device__ __forceinline__ uint32_t gtime() {
   return (uint32_t)t;
 }
 
-template <int D>
+// PP (ping-pong, fixed softmax base): 128-key steps, S and P double-buffered, the two
+// softmax warp groups take alternate steps.  !PP (online base): 256-key steps, each step
+// split in two key halves between the two warp groups.
+template <int D, bool PP>
 struct Cfg {
+  static constexpr int kBN = PP ? 128 : 256;               // keys per step
   static constexpr int kQBoxes = D / 64;                  // 64-column SW128 boxes per Q / K row
   static constexpr int kQTileBytes = BM * D * 2;          // one CTA's query tile (fp16)
-  static constexpr int kStageBytes = 256 * D;             // K half (128 keys x D) or V half (256 keys x D/2)
-  static constexpr int kStages = D == 128 ? 6 : 12;
+  static constexpr int kStageBytes = kBN * D;             // K (kBN/2 keys x D) or V (kBN keys x D/2) per CTA
+  static constexpr int kStages = (PP || D == 64) ? 12 : 6;
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = kQTileBytes;
   static constexpr int kRedOff = kKVOff + kStages * kStageBytes;  // row max / row sum exchange [2][BM]
@@ -116,7 +120,7 @@ struct Cfg {
 constexpr int kMaxGroups = 64;    // stream-K schedule needs <= 64 query groups (16384 query rows)
 
 struct Bars {
-  uint64_t q_full, q_empty, s_full[2], s_free[2], p_full, p_empty, o_full, o_empty;
+  uint64_t q_full, q_empty, s_full[2], s_free[2], p_full[2], p_empty[2], o_full, o_empty;
   uint64_t kv_full[12], kv_empty[12];
   uint32_t tmem_base;
   int32_t last_piece;               // combine election result (softmax warps)
@@ -173,11 +177,12 @@ __device__ __forceinline__ int span_at(const SpanTable& st, int x) {
 // the tile's class follows from the spans overlapping its row and key ranges.
 // rows_in_bounds: judge only the rows < nq (the softmax's masking decision:
 // rows past nq are computed but never stored, so they need no mask).
+template <int TK>
 __device__ __forceinline__ uint8_t step_class(const SpanTable& st, int g, int j, int nq, int kv_len, bool rows_in_bounds = false) {
   const int r0 = g * kTileQ, r1 = min(r0 + kTileQ, nq);
-  const int k0 = j * kTileK, k1 = min(k0 + kTileK, kv_len);
+  const int k0 = j * TK, k1 = min(k0 + TK, kv_len);
   bool any = k0 < st.valid;  // committed keys are visible to every query
-  bool all = (rows_in_bounds || r1 - r0 == kTileQ) && (k1 - k0 == kTileK);
+  bool all = (rows_in_bounds || r1 - r0 == kTileQ) && (k1 - k0 == TK);
   if (st.n == 1) return (any || k1 > st.valid) ? (all ? kFull : kPartial) : kSkip;
   if (k1 > st.valid) {
     const int ka = max(k0, st.valid) - st.valid, kb = k1 - st.valid;
@@ -210,16 +215,6 @@ __device__ __forceinline__ void visible_bits(const SpanTable& st, int qs, int kb
     if (span_vis(st, qs, ks))
       set_bits(m, max(st.start[ks], ka) + st.valid - kb0, min(st.start[ks + 1], kb) + st.valid - kb0);
 }
-// first and last non-SKIP step of query group g (every group has one: a query sees its own span)
-__device__ __forceinline__ void active_range(const SpanTable& st, int g, int nq, int kv_len, int nkv, int& jf,
-                                             int& jl) {
-  jf = 0;
-  jl = nkv - 1;
-  if (st.n == 1) return;
-  while (jf < nkv - 1 && step_class(st, g, jf, nq, kv_len) == kSkip) ++jf;
-  while (jl > jf && step_class(st, g, jl, nq, kv_len) == kSkip) --jl;
-}
-
 // ------------------------------------------------------------ work schedule --
 // Stream-K over executed steps: the sequence of (unit, executed step), units
 // u = (b, h, g) in order and their non-SKIP steps in key order, is cut into
@@ -240,6 +235,7 @@ struct Sched {
   int P;               // pairs
   int u;               // round-robin: next unit
 };
+template <int TK>
 __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_groups, int n_units, int H,
                                       const SpanTable& st, int nq, int kv_len, int nkv, Seg& sg) {
   if (sc.streamk) {
@@ -268,7 +264,7 @@ __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_g
   int cnt = nkv;  // whole unit: all of its executed steps
   if (st.n != 1) {
     cnt = 0;
-    for (int j = 0; j < nkv; ++j) cnt += step_class(st, sg.g, j, nq, kv_len) != kSkip;
+    for (int j = 0; j < nkv; ++j) cnt += step_class<TK>(st, sg.g, j, nq, kv_len) != kSkip;
   }
   sg.k1 = sg.cnt = cnt;
   return true;
@@ -282,24 +278,26 @@ __device__ __forceinline__ int pair_of(int W, int P, int x) {
   return p;
 }
 // key step of the k-th executed step of group g (k counted from the group's first executed step)
+template <int TK>
 __device__ __forceinline__ int step_of(const SpanTable& st, int g, int k, int nq, int kv_len, int nkv) {
   if (st.n == 1) return k;
   int j = 0;
   for (;; ++j) {
-    if (step_class(st, g, j, nq, kv_len) == kSkip) continue;
+    if (step_class<TK>(st, g, j, nq, kv_len) == kSkip) continue;
     if (k-- == 0) return j;
   }
 }
 
 
-template <int D>
+template <int D, bool PP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ out, int64_t o_bstride,
                     int64_t o_tstride, float* __restrict__ lse, uint8_t* __restrict__ tile_map, int B, int H,
                     int nq, int kv_len, float m_static, int dbg, float* __restrict__ ws, int* __restrict__ ws_cnt,
                     const __grid_constant__ SpanTable st) {
-  using C = Cfg<D>;
+  using C = Cfg<D, PP>;
+  constexpr int BN = C::kBN;  // keys per step (shadows the file-level 256)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;           // SW128 tiles need 1024-byte alignment
@@ -316,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int n_qtiles = (nq + BM - 1) / BM;
   const int n_groups = (n_qtiles + 1) / 2;                 // 2 query tiles per cluster unit
   const int n_units = B * H * n_groups;
-  const int nkv = (kv_len + BN - 1) / BN;                  // 256-key steps
+  const int nkv = (kv_len + BN - 1) / BN;                  // key steps
   const int cid = (int)ptx::cluster_id_x(), ncl = (int)ptx::nclusters_x();
   const bool trace_on = kTrace && g_dz_trace_on != 0 && cid == 0;
   uint32_t* const trace = g_dz_trace + rank * kTraceSteps * 16;
@@ -339,7 +337,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int g = threadIdx.x; g <= n_groups; g += kThreads) bars->gpre[g] = 0;
       __syncthreads();
       for (int x = threadIdx.x; x < n_groups * nkv; x += kThreads)
-        if (step_class(st, x / nkv, x % nkv, nq, kv_len) != kSkip) atomicAdd(&bars->gpre[x / nkv + 1], 1);
+        if (step_class<BN>(st, x / nkv, x % nkv, nq, kv_len) != kSkip) atomicAdd(&bars->gpre[x / nkv + 1], 1);
       __syncthreads();
       if (threadIdx.x == 0)
         for (int g = 1; g <= n_groups; ++g) bars->gpre[g] += bars->gpre[g - 1];
@@ -352,8 +350,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::mbar_init(bar(bars->s_full[hh]), 1);
       ptx::mbar_init(bar(bars->s_free[hh]), 8);  // 4 softmax warps of that key half x 2 CTAs
     }
-    ptx::mbar_init(bar(bars->p_full), 16);
-    ptx::mbar_init(bar(bars->p_empty), 1);
+    for (int pb = 0; pb < 2; ++pb) {
+      // PP: one P buffer per warp group (4 warps x 2 CTAs); !PP: one P buffer for all 8 warps
+      ptx::mbar_init(bar(bars->p_full[pb]), PP ? 8 : 16);
+      ptx::mbar_init(bar(bars->p_empty[pb]), 1);
+    }
     ptx::mbar_init(bar(bars->o_full), 1);
     ptx::mbar_init(bar(bars->o_empty), 16);
     for (int s = 0; s < C::kStages; ++s) {
@@ -393,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t ld = 0, q_phase = 0;
     Sched sc = sched0;
     Seg sg;
-    while (next_seg(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+    while (next_seg<BN>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
       const int b = sg.b, h = sg.h, g = sg.g;
       ptx::mbar_wait(bar(bars->q_empty), q_phase ^ 1);
       q_phase ^= 1;
@@ -404,9 +405,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int x = 0; x < C::kQBoxes; ++x)
             ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * 64, h, qt * BM, b, pol_q);
       }
-      int j = step_of(st, g, sg.k0, nq, kv_len, nkv);
+      int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j) {
-        while (step_class(st, g, j, nq, kv_len) == kSkip) ++j;
+        while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
         for (int kv = 0; kv < 2; ++kv, ++ld) {  // K_j half (128 keys x D), then V_j half (256 keys x D/2)
           uint32_t st, ph;
           slot(ld, st, ph);
@@ -419,7 +420,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (kv == 0) {
               // S half hh (keys 128hh..128hh+127 of the step) takes 64 keys from each CTA:
               // this CTA loads keys 128hh + 64*rank .. +63 into [hh][dim box] of 64 x 128 B
-              for (int hh = 0; hh < 2; ++hh)
+              for (int hh = 0; hh < BN / 128; ++hh)
                 for (int x = 0; x < C::kQBoxes; ++x)
                   ptx::tma_load_4d_2cta(dst + (hh * C::kQBoxes + x) * 64 * 128, &tm_k, lbar(bars->kv_full[st]),
                                         x * 64, h, j * BN + 128 * hh + 64 * (int)rank, b, pol_kv);
@@ -446,11 +447,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     Sched sc = sched0;
     Seg sg;
     bool first_seg = true;
-    while (next_seg(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+    while (next_seg<BN>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
       const int g = sg.g;
-      int j = step_of(st, g, sg.k0, nq, kv_len, nkv);
+      int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j) {
-        while (step_class(st, g, j, nq, kv_len) == kSkip) ++j;
+        while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
         const bool first = k == sg.k0, last = k == sg.k1 - 1;
         const bool tr = trace_on && first_seg && j < kTraceSteps && lane == 0;
         if (do_qk) {
@@ -461,12 +462,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint32_t k_st, k_ph;
           slot(2 * gs, k_st, k_ph);
           ptx::mbar_wait(bar(bars->kv_full[k_st]), k_ph);
-          // S in two halves of 128 keys (N = 128 each): the half-hh softmax warps release
-          // their half as soon as they hold it, so each QK half waits only for the copy
-          // of the same half of the previous step
-          for (int hh = 0; hh < 2; ++hh) {
+          // !PP: S in two halves of 128 keys (N = 128 each): the half-hh softmax warps release
+          // their half as soon as they hold it, so each QK half waits only for the copy of the
+          // same half of the previous step.  PP: one 128-key S per step, written into buffer
+          // gs % 2, which the softmax of step gs - 2 has released.
+          constexpr int kHalves = BN / 128;
+          for (int hh = 0; hh < kHalves; ++hh) {
+            const int sb = PP ? (gs & 1) : hh;  // S buffer written
             if (tr && hh == 0) trace[j * 8 + 0] = (uint32_t)clock();
-            if (gs > 0) {
+            if constexpr (PP) {
+              ptx::mbar_wait(bar(bars->s_free[sb]), ((gs >> 1) & 1) ^ 1);
+            } else if (gs > 0) {
               ptx::mbar_wait(bar(bars->s_free[hh]), sf_phase);
               if (hh == 1) sf_phase ^= 1;
             }
@@ -478,12 +484,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int kk = 0; kk < D / 16; ++kk) {
                 const uint32_t qoff = (kk / 4) * (128 * 128) + (kk % 4) * 32;  // Q: 128 rows per box
                 const uint32_t koff = (kk / 4) * (64 * 128) + (kk % 4) * 32;   // K half: 64 rows per box
-                ptx::mma_ss_2cta(tmem + kColS + hh * 128, ptx::sdesc_sw128(sQ + qoff, 16, 1024),
+                ptx::mma_ss_2cta(tmem + kColS + sb * 128, ptx::sdesc_sw128(sQ + qoff, 16, 1024),
                                  ptx::sdesc_sw128(ka + koff, 16, 1024), C::kIdescQK, kk > 0);
                 if (tr && j == 9) trace[kTraceSteps * 8 + hh * 8 + kk] = (uint32_t)clock();
               }
-              ptx::tc_commit_2cta(bar(bars->s_full[hh]), kBoth);
-              if (hh == 1) {
+              ptx::tc_commit_2cta(bar(bars->s_full[sb]), kBoth);
+              if (hh == kHalves - 1) {
                 ptx::tc_commit_2cta(bar(bars->kv_empty[k_st]), kBoth);
                 if (last) ptx::tc_commit_2cta(bar(bars->q_empty), kBoth);
               }
@@ -495,8 +501,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           slot(2 * gs + 1, v_st, v_ph);
           ptx::mbar_wait(bar(bars->kv_full[v_st]), v_ph);
           if (tr) trace[j * 8 + 2] = (uint32_t)clock();
-          ptx::mbar_wait(bar(bars->p_full), pf_phase);
-          pf_phase ^= 1;
+          const int pb = PP ? (gs & 1) : 0;  // P buffer read
+          if constexpr (PP) {
+            ptx::mbar_wait(bar(bars->p_full[pb]), (gs >> 1) & 1);
+          } else {
+            ptx::mbar_wait(bar(bars->p_full[0]), pf_phase);
+            pf_phase ^= 1;
+          }
           if (first) {  // the previous piece's epilogue has read O
             ptx::mbar_wait(bar(bars->o_empty), oe_phase ^ 1);
             oe_phase ^= 1;
@@ -509,10 +520,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < BN / 16; ++kk) {
               const uint64_t bd = D == 128 ? ptx::sdesc_sw128(va + kk * 16 * C::kVRowBytes, 16, 1024)
                                            : ptx::sdesc_sw64(va + kk * 16 * C::kVRowBytes, 16, 512);
-              ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + kk * 8, bd, C::kIdescPV, (!first || kk > 0) ? 1u : 0u);
+              ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + pb * 64 + kk * 8, bd, C::kIdescPV,
+                               (!first || kk > 0) ? 1u : 0u);
               if (tr && j == 9) trace[kTraceSteps * 8 + 16 + kk] = (uint32_t)clock();
             }
-            ptx::tc_commit_2cta(bar(bars->p_empty), kBoth);              // P may be overwritten
+            ptx::tc_commit_2cta(bar(bars->p_empty[pb]), kBoth);              // P may be overwritten
             if (last) ptx::tc_commit_2cta(bar(bars->o_full), kBoth);
             ptx::tc_commit_2cta(bar(bars->kv_empty[v_st]), kBoth);
           }
@@ -537,6 +549,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     constexpr uint32_t kSoftmaxBar = 5;         // named barrier: all 8 softmax warps
     const bool online = m_static <= 0.f;
     uint32_t s_phase = 0, pe_phase = 0, of_phase = 0;
+    int gsm = 0;  // executed steps so far (PP: this warp group takes the steps with gsm % 2 == hc)
     Sched sc = sched0;
     Seg sg;
     bool first_seg = true;
@@ -547,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tline[0] = gtime();
       tline[2] = (uint32_t)clock();
     }
-    while (next_seg(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+    while (next_seg<BN>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
       const int b = sg.b, h = sg.h, g = sg.g;
       const int qt = 2 * g + (int)rank;
       if (tl && n_seg < kTlSegs) tline[8 + 4 * n_seg] = (uint32_t)clock();
@@ -556,16 +569,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int s_row = qt * BM + row;            // this thread's query (row of the new tokens)
       const int qs = st.n == 1 ? 0 : span_at(st, min(s_row, nq - 1));  // its span (rows past nq: never stored)
       const bool map_thread = tile_map != nullptr && b == 0 && h == 0 && rank == 0 && row == 0 && hc == 0;
-      int j = step_of(st, g, sg.k0, nq, kv_len, nkv);
+      int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j) {
-        while (step_class(st, g, j, nq, kv_len) == kSkip) ++j;
+        while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
         const bool first = k == sg.k0;
-        const uint8_t cls = step_class(st, g, j, nq, kv_len);
+        const uint8_t cls = step_class<BN>(st, g, j, nq, kv_len);
         if (map_thread) tile_map[g * nkv + j] = cls;  // executed steps only; the host zeroes (SKIP) the map
+        const int my_u = gsm >> 1;                    // PP: use count of this group's S / P buffer
+        if (PP && (gsm++ & 1) != hc) continue;        // the other warp group's step
         // mask needed iff an in-bounds row of the tile misses a key of the step (Fig. 10 or key bounds)
-        const bool masked = cls == kPartial && step_class(st, g, j, nq, kv_len, true) == kPartial;
-        ptx::mbar_wait(bar(bars->s_full[hc]), s_phase);
-        s_phase ^= 1;
+        const bool masked = cls == kPartial && step_class<BN>(st, g, j, nq, kv_len, true) == kPartial;
+        if constexpr (PP) {
+          ptx::mbar_wait(bar(bars->s_full[hc]), my_u & 1);
+        } else {
+          ptx::mbar_wait(bar(bars->s_full[hc]), s_phase);
+          s_phase ^= 1;
+        }
         const bool tr = trace_on && first_seg && j < kTraceSteps && row == 0 && hc == 0;
         if (tr) trace[j * 8 + 4] = (uint32_t)clock();
         SCHED_POINT();
@@ -587,12 +606,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         SCHED_POINT();
         if (masked) {  // Fig. 10 mask and key bounds for this warp's 128 keys
           uint32_t vm[4];
-          visible_bits(st, qs, j * BN + 128 * hc, kv_len, vm);
+          visible_bits(st, qs, j * BN + (PP ? 0 : 128 * hc), kv_len, vm);
 #pragma unroll
           for (int i = 0; i < 128; ++i)
             if (!((vm[i / 32] >> (i % 32)) & 1u)) s[i] = -INFINITY;
         }
-        if (online) {
+        if (!PP && online) {  // (the host selects !PP whenever the softmax base is online)
           // Online softmax with lazy rescaling: a row moves its base only when its max
           // grew by more than 2^8; both warps of a row take the same decision from the
           // exchanged maxima.  O may be rescaled only when no PV into it is in flight:
@@ -608,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const bool grow = mx > m_used + kRescaleLog2;
           const bool rescale = grow && !first && m_used != -INFINITY;
           if (__any_sync(0xffffffffu, rescale)) {
-            ptx::mbar_wait(bar(bars->p_empty), pe_phase ^ 1);  // PV(j-1) done
+            ptx::mbar_wait(bar(bars->p_empty[0]), pe_phase ^ 1);  // PV(j-1) done
             ptx::tc_fence_after();
             const float alpha = rescale ? ptx::ex2(m_used - mx) : 1.f;
             l *= alpha;
@@ -645,9 +664,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (half == 0) {
             if (tr) trace[j * 8 + 7] = (uint32_t)clock();
         SCHED_POINT();
-            // P may be overwritten once PV(j-1) has read it
-            ptx::mbar_wait(bar(bars->p_empty), pe_phase ^ 1);
-            pe_phase ^= 1;
+            // P may be overwritten once the PV that last read it is done (PP: PV(j-2), own buffer)
+            if constexpr (PP) {
+              ptx::mbar_wait(bar(bars->p_empty[hc]), (my_u & 1) ^ 1);
+            } else {
+              ptx::mbar_wait(bar(bars->p_empty[0]), pe_phase ^ 1);
+              pe_phase ^= 1;
+            }
             ptx::tc_fence_after();
           }
           ptx::tmem_st32(tP + 32 * half, pk);
@@ -661,7 +684,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->p_full));
+        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->p_full[PP ? hc : 0]));
         if (tr) trace[j * 8 + 5] = (uint32_t)clock();
         SCHED_POINT();
       }
@@ -813,10 +836,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == kWarpTmem) ptx::tmem_dealloc_2cta<512>(tmem);
 }
 
-template <int D>
+template <int D, bool PP>
 cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
-  using C = Cfg<D>;
-  auto k = attn_fwd_kernel<D>;
+  using C = Cfg<D, PP>;
+  auto k = attn_fwd_kernel<D, PP>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return e;
   k<<<a.grid, kThreads, C::kSmem, s>>>(a.tm_q, a.tm_k, a.tm_v, static_cast<__nv_bfloat16*>(a.out), a.o_bstride,
@@ -851,9 +874,12 @@ int attention_units(int32_t B, int32_t H, int32_t nq) {
 }
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s) {
-  if (a.D == 128) return launch_t<128>(a, s);
-  if (a.D == 64) return launch_t<64>(a, s);
+  const bool pp = attention_step_keys(a.m_static) == 128;
+  if (a.D == 128) return pp ? launch_t<128, true>(a, s) : launch_t<128, false>(a, s);
+  if (a.D == 64) return pp ? launch_t<64, true>(a, s) : launch_t<64, false>(a, s);
   return cudaErrorInvalidValue;
 }
+
+int attention_step_keys(float m_static) { return m_static > 0.f ? 128 : 256; }
 
 }  // namespace dz

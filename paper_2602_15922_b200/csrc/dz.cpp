@@ -51,11 +51,11 @@ bool basic_cfg_ok(const dz_config* c) {
   return s == c->head_dim;
 }
 
-// debug tile map: [query groups of kTileQ rows][key steps of kTileK keys]
+// debug tile map: [query groups of kTileQ rows][key steps] (sized for the smallest step, 128 keys)
 size_t map_bytes(const dz_config* c) {
   const int64_t mc = c->max_chunk_tokens;
   const int64_t keys = c->cache_capacity_tokens + mc + c->window_slack_tokens;
-  return 256 + (size_t)((mc + dz::kTileQ - 1) / dz::kTileQ) * ((keys + dz::kTileK - 1) / dz::kTileK);
+  return 256 + (size_t)((mc + dz::kTileQ - 1) / dz::kTileQ) * ((keys + 127) / 128);
 }
 
 Layout make_layout(const dz_config* c) {
@@ -138,7 +138,7 @@ struct dz_ctx {
   int32_t staged_id = 0, staged_kind = 0;
   int64_t staged_n = 0;
   // last attend geometry (tile map / lse)
-  int32_t last_nq = 0, last_nkv_tiles = 0, last_nq_tiles = 0;
+  int32_t last_nq = 0, last_nkv_tiles = 0, last_nq_tiles = 0, last_step_keys = 256;
   bool have_map = false;
   // device pointers into the caller's storage
   char* base = nullptr;
@@ -340,7 +340,8 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   // V: each CTA loads D/2 of the columns of all 256 keys (see attention.cu).
   if (!make_tmap(&a.tm_q, c->base + c->L.q_off, false, c->D, c->Hl, n, c->B, n * c->Hl * c->D, 64, 128) ||
       !make_tmap(&a.tm_k, c->kslot(0, c->start), false, c->D, c->Hl, kv_len, c->B, bs, 64, 64) ||
-      !make_tmap(&a.tm_v, c->vslot(0, c->start), true, c->D, c->Hl, kv_len, c->B, bs, (uint32_t)c->D / 2, 256))
+      !make_tmap(&a.tm_v, c->vslot(0, c->start), true, c->D, c->Hl, kv_len, c->B, bs, (uint32_t)c->D / 2,
+                 (uint32_t)dz::attention_step_keys(c->m_static)))
     return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled failed");
   a.out = out_local;
   a.o_bstride = o_bstride;
@@ -357,7 +358,8 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   // persistent grid: one CTA pair per TPC; stream-K spreads the executed steps evenly over the pairs
   a.grid = 2 * std::min(c->num_sms / 2, dz::kMaxPairs);
   // stream-K needs <= 64 query groups and 32-bit step arithmetic (W * pairs < 2^31); else whole units round-robin
-  const int64_t n_groups = (n + dz::kTileQ - 1) / dz::kTileQ, n_steps = (kv_len + dz::kTileK - 1) / dz::kTileK;
+  const int step_keys = dz::attention_step_keys(c->m_static);
+  const int64_t n_groups = (n + dz::kTileQ - 1) / dz::kTileQ, n_steps = (kv_len + step_keys - 1) / step_keys;
   static const bool rr_forced = getenv("DZ_SCHED_RR") != nullptr;  // diagnostics: whole units round-robin
   const bool streamk = !rr_forced && n_groups <= 64 &&
                        (int64_t)c->B * c->Hl * n_groups * n_steps * dz::kMaxPairs < (1ll << 31);
@@ -369,13 +371,14 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
     if (r) return r;
     c->ws_zeroed = true;
   }
-  const int ngr = (int)((n + dz::kTileQ - 1) / dz::kTileQ), nst = (int)((kv_len + dz::kTileK - 1) / dz::kTileK);
+  const int ngr = (int)n_groups, nst = (int)n_steps;
   if ((c->cfg.flags & DZ_FLAG_TILE_MAP) && (size_t)ngr * nst <= map_bytes(&c->cfg)) {
     a.tile_map = reinterpret_cast<uint8_t*>(c->base + c->L.map_off);
     // the kernel writes the executed steps (FULL / PARTIAL); the rest stay SKIP
     dz_status r = cuda_check(c, cudaMemsetAsync(a.tile_map, 0, (size_t)ngr * nst, st), "tile map clear");
     if (r) return r;
     c->last_nq_tiles = ngr;
+    c->last_step_keys = step_keys;
     c->last_nkv_tiles = nst;
     c->have_map = true;
   }
@@ -641,7 +644,7 @@ dz_status dz_get_tile_map(const dz_ctx* c, uint8_t* host, size_t cap, int32_t* n
   if (nq) *nq = c->last_nq_tiles;
   if (nk) *nk = c->last_nkv_tiles;
   if (bm) *bm = dz::kTileQ;
-  if (bn) *bn = dz::kTileK;
+  if (bn) *bn = c->last_step_keys;
   if (!host) return DZ_OK;
   if (cap < need) return DZ_EINVAL;
   // synchronous device read of the kernel-written debug map (tests only)

@@ -98,11 +98,11 @@ def test_tile_map_matches_oracle_classifier():
     run.fill()
     run.attend()
     torch.cuda.synchronize()
-    got = run.cache.tile_map()
+    got, bm, bn = run.cache.tile_map(with_tiles=True)
     C, n = w.cached_chunks, w.chunk_tokens
     kt = oracle.chunk_tags(list(range(C)) + [C], [oracle.CLEAN] * C + [oracle.NOISY], [n] * (C + 1))
     qt = (np.full(n, C, np.int32), np.full(n, oracle.NOISY, np.int32), np.full(n, C, np.int32))
-    want = oracle.tile_map(qt, kt, 256, 256)   # the kernel's (query group, key step) tiles
+    want = oracle.tile_map(qt, kt, bm, bn)   # the kernel's (query group, key step) tiles
     assert got.shape == want.shape
     assert np.array_equal(got, want), oracle.tile_map_str(got) + " vs " + oracle.tile_map_str(want)
 

@@ -73,8 +73,8 @@ def test_teacher_forcing_c0(M):
     out = _run(cache, spans, q, k, v, pos).cpu().double().numpy()
     want, qt, kt = _oracle_spans(w, gq, gk, spans, q, k, v, pos)
     assert_parity(out, want, f"teacher forcing M={M}")
-    got_map = cache.tile_map()
-    assert np.array_equal(got_map, oracle.tile_map(qt, kt, 256, 256)), oracle.tile_map_str(got_map)
+    got_map, bm, bn = cache.tile_map(with_tiles=True)
+    assert np.array_equal(got_map, oracle.tile_map(qt, kt, bm, bn)), oracle.tile_map_str(got_map)
 
 
 def test_teacher_forcing_wan_shape_skips_tiles():
@@ -87,8 +87,8 @@ def test_teacher_forcing_wan_shape_skips_tiles():
     out = _run(cache, spans, q, k, v, pos).cpu().double().numpy()
     want, qt, kt = _oracle_spans(w, gq, gk, spans, q, k, v, pos)
     assert_parity(out, want, "teacher forcing M=4 x 1344")
-    got_map = cache.tile_map()
-    want_map = oracle.tile_map(qt, kt, 256, 256)
+    got_map, bm, bn = cache.tile_map(with_tiles=True)
+    want_map = oracle.tile_map(qt, kt, bm, bn)
     assert np.array_equal(got_map, want_map)
     assert (want_map == 0).sum() > 0.3 * want_map.size, "layout must exercise tile skipping"
 
@@ -113,7 +113,8 @@ def test_ragged_spans_over_committed_cache():
     out = _run(cache, spans, q, k, v, pos).cpu().double().numpy()
     want, qt, kt = _oracle_spans(w, gq, gk, spans, q, k, v, pos, (comm_k, comm_v, comm_p))
     assert_parity(out, want, "ragged spans + cache")
-    assert np.array_equal(cache.tile_map(), oracle.tile_map(qt, kt, 256, 256))
+    got_map, bm, bn = cache.tile_map(with_tiles=True)
+    assert np.array_equal(got_map, oracle.tile_map(qt, kt, bm, bn))
     # the committed cache is untouched and still usable for a plain attend
     assert cache.state() == (2 * w.chunk_tokens, 2, 1)
 

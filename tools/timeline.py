@@ -2,6 +2,7 @@
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
+os.environ.setdefault("DZ_LIB_PATH", os.path.join(ROOT, "paper_2602_15922_b200", "libdz_trace.so"))
 import numpy as np, torch, synth
 import paper_2602_15922_b200 as dz
 from helpers import GpuRun

@@ -2,6 +2,7 @@
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
+os.environ.setdefault("DZ_LIB_PATH", os.path.join(ROOT, "paper_2602_15922_b200", "libdz_trace.so"))
 import numpy as np, torch, synth
 import paper_2602_15922_b200 as dz
 from helpers import GpuRun
@@ -12,7 +13,7 @@ tr = dz.debug_trace(False, read=True).astype(np.int64)
 base = tr[0]
 R = lambda x: int((x - base) & 0xffffffff)
 print(" j | QK wait issue | PV wait issue | SM S-ready S-loaded exp-done P-done | QK->S  S->P")
-for j in range(0, 16):
+for j in range(0, int(os.environ.get("NSTEPS", "16"))):
     r = tr[8 * j: 8 * j + 8]
     print(f"{j:2d} | {R(r[0]):6d} {R(r[1]):6d} | {R(r[2]):6d} {R(r[3]):6d} | {R(r[4]):6d} {R(r[6]):6d} {R(r[7]):6d} {R(r[5]):6d} |"
           f" {R(r[4]) - R(r[1]):5d} {R(r[5]) - R(r[4]):5d}")
