@@ -58,7 +58,10 @@ constexpr int BM = 128;           // query rows per CTA (MMA M = 256 per pair)
 constexpr int BN = 256;           // keys per KV step
 constexpr int kThreads = 384;     // 12 warps
 constexpr float kRescaleLog2 = 8.0f;
-constexpr int kPolyPairs = 3;     // of every 8 exp2 pairs, this many go to the FMA-pipe polynomial (measured best of 2/3/4)
+#ifndef DZ_POLY
+#define DZ_POLY 2
+#endif
+constexpr int kPolyPairs = DZ_POLY;  // of every 8 exp2 pairs, this many go to the FMA-pipe polynomial (measured on the ping-pong kernel: 0/2/3/4 -> 234/205/212/218 us)
 constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr int kWarpMma = 11, kWarpTma = 10, kWarpPv = 9, kWarpTmem = 8;
 constexpr uint32_t kRegsLight = 88, kRegsSoftmax = 208;  // setmaxnreg: 128*88 + 256*208 = 384*168 (launch)
@@ -107,6 +110,10 @@ struct Cfg {
   static constexpr int kQTileBytes = BM * D * 2;          // one CTA's query tile (fp16)
   static constexpr int kStageBytes = kBN * D;             // K (kBN/2 keys x D) or V (kBN keys x D/2) per CTA
   static constexpr int kStages = (PP || D == 64) ? 12 : 6;
+  // separate K and V rings: a V stage is held until its PV completes, several steps after
+  // its QK, so a shared in-order ring would let V recycling throttle the K prefetch
+  static constexpr int kKStages = kStages == 12 ? 7 : 3;
+  static constexpr int kVStages = kStages - kKStages;
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = kQTileBytes;
   static constexpr int kRedOff = kKVOff + kStages * kStageBytes;  // row max / row sum exchange [2][BM]
@@ -322,10 +329,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   auto bar = [&](uint64_t& b) { return ptx::smem_u32(&b); };
   auto lbar = [&](uint64_t& b) { return ptx::mapa(ptx::smem_u32(&b), 0); };  // leader's copy
-  // ring slot of the i-th K/V load (TMA order K0 V0 K1 V1 ...)
-  auto slot = [&](uint32_t i, uint32_t& st, uint32_t& ph) {
-    st = i % C::kStages;
-    ph = (i / C::kStages) & 1;
+  // ring slots of the i-th K load and the i-th V load (barrier index; the V ring follows the K ring)
+  auto kslot = [&](uint32_t i, uint32_t& st, uint32_t& ph) {
+    st = i % C::kKStages;
+    ph = (i / C::kKStages) & 1;
+  };
+  auto vslot = [&](uint32_t i, uint32_t& st, uint32_t& ph) {
+    st = C::kKStages + i % C::kVStages;
+    ph = (i / C::kVStages) & 1;
   };
 
   // executed steps per query group -> prefix sums (every role walks the same schedule)
@@ -387,50 +398,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp >= 8) {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsLight));
-  if (warp == kWarpTma) {
-    // ------------------------------------------------------ TMA producer --
+  if (warp == kWarpTma || warp == kWarpTmem) {
+    // ------------------------------------------------ TMA producers (K + Q, V) --
+    // warp kWarpTma loads each piece's Q tiles and the K tiles into the K ring; warp
+    // kWarpTmem (idle between TMEM alloc and dealloc) loads the V tiles into the V ring.
+    const bool do_k = warp == kWarpTma;
     const uint64_t pol_q = ptx::l2_policy_evict_first();
     const uint64_t pol_kv = ptx::l2_policy_evict_last();
     uint32_t ld = 0, q_phase = 0;
     Sched sc = sched0;
     Seg sg;
+    bool first_seg = true;
     while (next_seg<BN>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
       const int b = sg.b, h = sg.h, g = sg.g;
-      ptx::mbar_wait(bar(bars->q_empty), q_phase ^ 1);
-      q_phase ^= 1;
-      const int qt = 2 * g + (int)rank;
-      if (lane == 0) {
-        if (leader) ptx::mbar_arrive_expect_tx(bar(bars->q_full), min(2, n_qtiles - 2 * g) * C::kQTileBytes);
-        if (qt < n_qtiles)  // a tile wholly past nq is not loaded (its rows are never stored)
-          for (int x = 0; x < C::kQBoxes; ++x)
-            ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * 64, h, qt * BM, b, pol_q);
-      }
-      int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
-      for (int k = sg.k0; k < sg.k1; ++k, ++j) {
-        while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
-        for (int kv = 0; kv < 2; ++kv, ++ld) {  // K_j half (128 keys x D), then V_j half (256 keys x D/2)
-          uint32_t st, ph;
-          slot(ld, st, ph);
-          ptx::mbar_wait(bar(bars->kv_empty[st]), ph ^ 1);
-          if (lane == 0 && (dbg & 1)) {  // diagnostics: no K/V traffic, MMAs read stale smem
-            if (leader) ptx::mbar_arrive(bar(bars->kv_full[st]));
-          } else if (lane == 0) {
-            if (leader) ptx::mbar_arrive_expect_tx(bar(bars->kv_full[st]), 2 * C::kStageBytes);
-            const uint32_t dst = sKV + st * C::kStageBytes;
-            if (kv == 0) {
-              // S half hh (keys 128hh..128hh+127 of the step) takes 64 keys from each CTA:
-              // this CTA loads keys 128hh + 64*rank .. +63 into [hh][dim box] of 64 x 128 B
-              for (int hh = 0; hh < BN / 128; ++hh)
-                for (int x = 0; x < C::kQBoxes; ++x)
-                  ptx::tma_load_4d_2cta(dst + (hh * C::kQBoxes + x) * 64 * 128, &tm_k, lbar(bars->kv_full[st]),
-                                        x * 64, h, j * BN + 128 * hh + 64 * (int)rank, b, pol_kv);
-            } else {
-              ptx::tma_load_4d_2cta(dst, &tm_v, lbar(bars->kv_full[st]), (int)rank * (D / 2), h, j * BN, b, pol_kv);
-            }
-          }
+      if (do_k) {
+        ptx::mbar_wait(bar(bars->q_empty), q_phase ^ 1);
+        q_phase ^= 1;
+        const int qt = 2 * g + (int)rank;
+        if (lane == 0) {
+          if (leader) ptx::mbar_arrive_expect_tx(bar(bars->q_full), min(2, n_qtiles - 2 * g) * C::kQTileBytes);
+          if (qt < n_qtiles)  // a tile wholly past nq is not loaded (its rows are never stored)
+            for (int x = 0; x < C::kQBoxes; ++x)
+              ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * 64, h, qt * BM, b, pol_q);
         }
       }
-      __syncwarp();
+      int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
+      for (int k = sg.k0; k < sg.k1; ++k, ++j, ++ld) {
+        while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+        uint32_t sl, ph;
+        if (do_k)
+          kslot(ld, sl, ph);
+        else
+          vslot(ld, sl, ph);
+        ptx::mbar_wait(bar(bars->kv_empty[sl]), ph ^ 1);
+        if (trace_on && first_seg && j < kTraceSteps && lane == 0) trace[2560 + 2 * j + (do_k ? 0 : 1)] = (uint32_t)clock();
+        if (lane == 0 && (dbg & 1)) {  // diagnostics: no K/V traffic, MMAs read stale smem
+          if (leader) ptx::mbar_arrive(bar(bars->kv_full[sl]));
+        } else if (lane == 0) {
+          if (leader) ptx::mbar_arrive_expect_tx(bar(bars->kv_full[sl]), 2 * C::kStageBytes);
+          const uint32_t dst = sKV + sl * C::kStageBytes;
+          if (do_k) {
+            // S half hh (keys 128hh..128hh+127 of the step) takes 64 keys from each CTA:
+            // this CTA loads keys 128hh + 64*rank .. +63 into [hh][dim box] of 64 x 128 B
+            for (int hh = 0; hh < BN / 128; ++hh)
+              for (int x = 0; x < C::kQBoxes; ++x)
+                ptx::tma_load_4d_2cta(dst + (hh * C::kQBoxes + x) * 64 * 128, &tm_k, lbar(bars->kv_full[sl]),
+                                      x * 64, h, j * BN + 128 * hh + 64 * (int)rank, b, pol_kv);
+          } else {
+            ptx::tma_load_4d_2cta(dst, &tm_v, lbar(bars->kv_full[sl]), (int)rank * (D / 2), h, j * BN, b, pol_kv);
+          }
+        }
+        __syncwarp();
+      }
+      first_seg = false;
     }
   } else if ((warp == kWarpMma || warp == kWarpPv) && leader) {
     // ------------------------------------------------------ MMA issuers --
@@ -460,7 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             q_phase ^= 1;
           }
           uint32_t k_st, k_ph;
-          slot(2 * gs, k_st, k_ph);
+          kslot(gs, k_st, k_ph);
           ptx::mbar_wait(bar(bars->kv_full[k_st]), k_ph);
           // !PP: S in two halves of 128 keys (N = 128 each): the half-hh softmax warps release
           // their half as soon as they hold it, so each QK half waits only for the copy of the
@@ -498,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         } else {
           uint32_t v_st, v_ph;
-          slot(2 * gs + 1, v_st, v_ph);
+          vslot(gs, v_st, v_ph);
           ptx::mbar_wait(bar(bars->kv_full[v_st]), v_ph);
           if (tr) trace[j * 8 + 2] = (uint32_t)clock();
           const int pb = PP ? (gs & 1) : 0;  // P buffer read
