@@ -1,6 +1,7 @@
 // umma2_bench.cu -- cta_group::2 tcgen05.mma throughput (M=256 across a CTA pair).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2602_15922_b200/csrc tools/umma2_bench.cu -o tools/umma2_bench
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
@@ -67,7 +68,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long l
     ptx::mbar_wait(ptx::smem_u32(&bar), 0);
     *(volatile uint32_t*)&tbase = 0xFFFFFFFFu;
   }
-  if (ALU && warp >= 4) {  // 8 warps of softmax-like MUFU/FMA/F2FP math (issue-slot pressure)
+  // ALU 2: math on all 4 SMSPs; ALU 20: the same math but never on SMSP 0 (the MMA issuer's)
+  if ((ALU == 1 || ALU == 2 || ALU == 20) && warp >= 4 && !(ALU == 20 && warp % 4 == 0)) {
     float a[16];
     for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
     uint32_t acc = 0;
@@ -77,7 +79,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long l
         const uint64_t x = ptx::f2_fma(ptx::f2_pack(a[i], a[i + 1]), ptx::f2_pack(0.5f, 0.5f), ptx::f2_pack(-1.f, -1.f));
         float x0, x1;
         ptx::f2_unpack(x, x0, x1);
-        if (ALU == 2 && (i & 2)) {
+        if ((ALU == 2 || ALU == 20) && (i & 2)) {
           const uint64_t p = ptx::f2_exp2_poly(x);
           ptx::f2_unpack(p, x0, x1);
         } else {
@@ -90,6 +92,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long l
       }
     }
     if (acc == 0x12345) cycles[100] = acc;
+  }
+  if (ALU >= 3 && warp >= 4) {  // 8 warps of one instruction kind only (which pipes interfere with the MMA?)
+    float a[16];
+    uint64_t v[8];
+    uint32_t u[8];
+    for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+    for (int i = 0; i < 8; ++i) { v[i] = ptx::f2_pack(a[i], a[i + 8]); u[i] = threadIdx.x + i; }
+    const uint64_t c2 = ptx::f2_pack(0.999f, 0.999f), d2 = ptx::f2_pack(0.001f, 0.001f);
+    for (int k = 0; *(volatile uint32_t*)&tbase != 0xFFFFFFFFu; ++k) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (ALU == 3) a[i] = fmaf(a[i], 0.999f, a[i + 8]);
+          if (ALU == 4) v[i] = ptx::f2_fma(v[i], c2, d2);
+          if (ALU == 5) u[i] = ptx::pack_bf16x2(__uint_as_float(u[i]), a[i]);
+          if (ALU == 6) a[i] = ptx::ex2(a[i]);
+          if (ALU == 7) v[i] = ptx::f2_add(v[i], d2);
+          if (ALU == 8) u[i] = u[i] * 0x9E3779B1u + 7u;
+          if (ALU == 9) v[i] = ptx::f2_exp2_poly<false>(v[i]);
+          if (ALU == 10) v[i] = ptx::f2_exp2_poly<true>(v[i]);
+          if (ALU == 11) { float x, y; ptx::f2_unpack(v[i], x, y); v[i] = ptx::f2_fma(ptx::f2_pack(ptx::ex2(x), ptx::ex2(y)), c2, d2); }
+          if (ALU == 12) a[i] = fmaxf(a[i], a[i + 8]) * 0.999f;
+          if (ALU == 13) u[i] = __float_as_uint(a[i]) + (u[i] << 23);
+        }
+    }
+    float sacc = 0;
+    for (int i = 0; i < 8; ++i) { float x, y; ptx::f2_unpack(v[i], x, y); sacc += a[i] + x + y + __uint_as_float(u[i]); }
+    if (sacc == 1.2345f) cycles[100] = 1;
   }
   if (TMEM_TRAFFIC && warp >= 4) {  // 8 warps: softmax-like S loads and P stores
     const uint32_t lanes = (uint32_t)((warp % 4) * 32) << 16;
@@ -137,6 +168,16 @@ void run(const char* name, double instr_per_iter) {
 }
 
 int main() {
+  if (getenv("ONLY_ALU")) {
+    run<2, true, false, 1, 0, 2>("TS+SS + 8 warps MUFU+poly math", 16);
+    run<2, true, false, 1, 0, 20>("TS+SS + 6 warps MUFU+poly, SMSP0 free", 16);
+    run<2, true, false, 1, 0, 9>("TS+SS + 8 warps poly (no clamp)", 16);
+    run<2, true, false, 1, 0, 10>("TS+SS + 8 warps poly (clamp)", 16);
+    run<2, true, false, 1, 0, 11>("TS+SS + 8 warps MUFU+FFMA2", 16);
+    run<2, true, false, 1, 0, 12>("TS+SS + 8 warps FMNMX+FMUL", 16);
+    run<2, true, false, 1, 0, 13>("TS+SS + 8 warps shl+add", 16);
+    return 0;
+  }
   run<0, false, false>("2CTA SS M256 N128 zeros", 8);
   run<0, true, false>("2CTA SS M256 N128 random", 8);
   run<1, true, false>("2CTA TS M256 N128 random", 8);
@@ -150,5 +191,18 @@ int main() {
   run<2, true, false, 1, 3>("... + both per 16", 16);
   run<2, true, false, 1, 0, 1>("TS+SS + 8 warps MUFU math", 16);
   run<2, true, false, 1, 0, 2>("TS+SS + 8 warps MUFU+poly math", 16);
+  run<2, true, false, 1, 0, 3>("TS+SS + 8 warps FFMA", 16);
+  run<2, true, false, 1, 0, 4>("TS+SS + 8 warps FFMA2", 16);
+  run<2, true, false, 1, 0, 5>("TS+SS + 8 warps F2FP", 16);
+  run<2, true, false, 1, 0, 6>("TS+SS + 8 warps MUFU.EX2", 16);
+  run<2, true, false, 1, 0, 7>("TS+SS + 8 warps FADD2", 16);
+  run<2, true, false, 1, 0, 8>("TS+SS + 8 warps IMAD", 16);
+  run<2, true, false, 1, 0, 9>("TS+SS + 8 warps poly (no clamp)", 16);
+  run<2, true, false, 1, 0, 10>("TS+SS + 8 warps poly (clamp)", 16);
+  run<2, true, false, 1, 0, 11>("TS+SS + 8 warps MUFU+FFMA2", 16);
+  run<2, true, false, 1, 0, 12>("TS+SS + 8 warps FMNMX+FMUL", 16);
+  run<2, true, false, 1, 0, 13>("TS+SS + 8 warps shl+add", 16);
+  run<1, true, false, 1, 0, 4>("TS only + 8 warps FFMA2", 8);
+  run<0, true, false, 1, 0, 4>("SS only + 8 warps FFMA2", 8);
   return 0;
 }
