@@ -424,7 +424,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j, ++ld) {
-        while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+        if (st.n != 1)
+          while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
         uint32_t sl, ph;
         if (do_k)
           kslot(ld, sl, ph);
@@ -471,7 +472,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int g = sg.g;
       int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j) {
-        while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+        if (st.n != 1)
+          while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
         const bool first = k == sg.k0, last = k == sg.k1 - 1;
         const bool tr = trace_on && first_seg && j < kTraceSteps && lane == 0;
         if (do_qk) {
@@ -591,14 +593,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool map_thread = tile_map != nullptr && b == 0 && h == 0 && rank == 0 && row == 0 && hc == 0;
       int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j) {
-        while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+        if (st.n != 1)
+          while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
         const bool first = k == sg.k0;
-        const uint8_t cls = step_class<BN>(st, g, j, nq, kv_len);
-        if (map_thread) tile_map[g * nkv + j] = cls;  // executed steps only; the host zeroes (SKIP) the map
+        // executed steps only; the host zeroes (SKIP) the map
+        if (map_thread) tile_map[g * nkv + j] = step_class<BN>(st, g, j, nq, kv_len);
         const int my_u = gsm >> 1;                    // PP: use count of this group's S / P buffer
         if (PP && (gsm++ & 1) != hc) continue;        // the other warp group's step
-        // mask needed iff an in-bounds row of the tile misses a key of the step (Fig. 10 or key bounds)
-        const bool masked = cls == kPartial && step_class<BN>(st, g, j, nq, kv_len, true) == kPartial;
+        // mask needed iff an in-bounds row of the tile misses a key of the step (Fig. 10 or key
+        // bounds); one span (attend_chunk): only a ragged last key step
+        const bool masked = st.n == 1 ? (j == nkv - 1 && kv_len % BN != 0)
+                                      : step_class<BN>(st, g, j, nq, kv_len, true) == kPartial;
         if constexpr (PP) {
           ptx::mbar_wait(bar(bars->s_full[hc]), my_u & 1);
         } else {
