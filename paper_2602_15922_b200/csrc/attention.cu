@@ -592,14 +592,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int qs = st.n == 1 ? 0 : span_at(st, min(s_row, nq - 1));  // its span (rows past nq: never stored)
       const bool map_thread = tile_map != nullptr && b == 0 && h == 0 && rank == 0 && row == 0 && hc == 0;
       int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
-      for (int k = sg.k0; k < sg.k1; ++k, ++j) {
-        if (st.n != 1)
-          while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+      // fast walk (PP, one span, no tile map): every step executes, so this group's steps
+      // are every other one -- no per-step bookkeeping for the other group's steps
+      const int gsm0 = gsm;
+      const bool fast = PP && st.n == 1 && tile_map == nullptr;
+      const int kstep = fast ? 2 : 1;
+      const int k_start = sg.k0 + (fast ? ((hc - gsm0) & 1) : 0);
+      j += k_start - sg.k0;
+      for (int k = k_start; k < sg.k1; k += kstep, j += kstep) {
         const bool first = k == sg.k0;
-        // executed steps only; the host zeroes (SKIP) the map
-        if (map_thread) tile_map[g * nkv + j] = step_class<BN>(st, g, j, nq, kv_len);
-        const int my_u = gsm >> 1;                    // PP: use count of this group's S / P buffer
-        if (PP && (gsm++ & 1) != hc) continue;        // the other warp group's step
+        int my_u;                                     // PP: use count of this group's S / P buffer
+        if (fast) {
+          my_u = (gsm0 + (k - sg.k0)) >> 1;
+        } else {
+          if (st.n != 1)
+            while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+          // executed steps only; the host zeroes (SKIP) the map
+          if (map_thread) tile_map[g * nkv + j] = step_class<BN>(st, g, j, nq, kv_len);
+          my_u = gsm >> 1;
+          if (PP && (gsm++ & 1) != hc) continue;      // the other warp group's step
+        }
         // mask needed iff an in-bounds row of the tile misses a key of the step (Fig. 10 or key
         // bounds); one span (attend_chunk): only a ragged last key step
         const bool masked = st.n == 1 ? (j == nkv - 1 && kv_len % BN != 0)
@@ -713,6 +725,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (tr) trace[j * 8 + 5] = (uint32_t)clock();
         SCHED_POINT();
       }
+      if (fast) gsm = gsm0 + (sg.k1 - sg.k0);
       first_seg = false;
       if (tl && n_seg < kTlSegs) tline[9 + 4 * n_seg] = (uint32_t)clock();
       // total row sum over both key halves
