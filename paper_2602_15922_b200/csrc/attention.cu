@@ -798,9 +798,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int q = pf; q <= pl; ++q) n_pieces += pair_lo(sched0.W, ncl, q) < pair_lo(sched0.W, ncl, q + 1);
       int* cnt_ptr = ws_cnt + (((int64_t)b * H + h) * n_groups + g) * 2 + rank;
       if (threadIdx.x == 0) {
-        __threadfence();
-        const bool last_piece = atomicAdd(cnt_ptr, 1) == n_pieces - 1;
-        if (last_piece) __threadfence();  // acquire the other pieces before the barrier releases the readers
+        // acq_rel RMW at GPU scope: releases this CTA's piece (the barrier above made every
+        // softmax thread's stores precede it; release is cumulative) and, for the last
+        // piece, acquires the others' before the barrier below releases the readers
+        const bool last_piece = ptx::atom_add_acq_rel_gpu(cnt_ptr, 1) == n_pieces - 1;
         bars->last_piece = last_piece;
       }
       ptx::named_bar_sync(kSoftmaxBar, 256);
