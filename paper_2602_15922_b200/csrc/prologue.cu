@@ -32,7 +32,14 @@ namespace dz {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxStageBytes = 96 * 1024;  // ring size cap: 2 CTAs per SM
+#ifndef DZ_PRO_CTAS
+#define DZ_PRO_CTAS 2
+#endif
+#ifndef DZ_PRO_RING_KB
+#define DZ_PRO_RING_KB 96
+#endif
+constexpr int kCtasPerSm = DZ_PRO_CTAS;
+constexpr int kMaxStageBytes = DZ_PRO_RING_KB * 1024;  // ring size cap per CTA
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -55,7 +62,7 @@ struct ProSmem {
     row_bytes = H * D * 2;
     stage_bytes = nt * row_bytes;
     S = kMaxStageBytes / stage_bytes;
-    S = S < 2 ? 2 : (S > 4 ? 4 : S);
+    S = S < 2 ? 2 : (S > 6 ? 6 : S);
   }
   __host__ __device__ int cs_off() const { return S * stage_bytes; }           // float2 [S][D/2]
   __host__ __device__ int row_off(int D) const { return cs_off() + S * (D / 2) * 8; }  // int64 [H]
@@ -64,7 +71,7 @@ struct ProSmem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 2) prologue_kernel(const PrologueArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const PrologueArgs a) {
   constexpr int G = D / 8;               // threads per row (one 16-byte vector each)
   constexpr int kGroups = kThreads / G;  // rows processed side by side
   constexpr int kPer = 3;                // heads per thread in one pass (H <= 48 at D = 128: one pass)
@@ -227,7 +234,7 @@ cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int items = a.B * a.n;
-  const int grid = items < 2 * sms ? items : 2 * sms;
+  const int grid = items < kCtasPerSm * sms ? items : kCtasPerSm * sms;
   k<<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
