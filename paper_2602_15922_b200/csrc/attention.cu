@@ -694,6 +694,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t pk[32];
+#ifdef DZ_DIAG_NOEXP  // diagnostics build only: P = packed scores, no exponentials (results are garbage)
+          if (true) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) pk[i] = ptx::pack_bf16x2(s[64 * half + 2 * i], s[64 * half + 2 * i + 1]);
+          } else
+#endif
           if (plain)
             exp_half<true>(s + 64 * half, nb2, pk, acc);
           else
