@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="warm L2 (secondary measurement)")
+    ap.add_argument("--flush-read", action="store_true",
+                    help="after the 512 MB flush write, read 256 MB of it so no dirty flush lines stay in L2")
     return ap.parse_args()
 
 
@@ -282,6 +284,8 @@ def main():
         for i in range(args.steps):
             if not args.no_flush:
                 flush.zero_()
+                if args.flush_read:
+                    flush_sum = flush[: flush.numel() // 2].sum()  # noqa: F841
             ev[i][0].record()
             step()
             ev[i][1].record()

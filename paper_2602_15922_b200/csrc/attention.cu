@@ -109,16 +109,24 @@ struct Cfg {
   static constexpr int kQBoxes = D / 64;                  // 64-column SW128 boxes per Q / K row
   static constexpr int kQTileBytes = BM * D * 2;          // one CTA's query tile (fp16)
   static constexpr int kStageBytes = kBN * D;             // K (kBN/2 keys x D) or V (kBN keys x D/2) per CTA
-  static constexpr int kStages = (PP || D == 64) ? 12 : 6;
+#ifndef DZ_KST
+#define DZ_KST 5   // measured on C1 (K/V stages): 7/5 192.7 us, 6/4 190.3, 5/4 191.0, 5/3 190.0
+#endif
+#ifndef DZ_VST
+#define DZ_VST 3
+#endif
   // separate K and V rings: a V stage is held until its PV completes, several steps after
   // its QK, so a shared in-order ring would let V recycling throttle the K prefetch
-  static constexpr int kKStages = kStages == 12 ? 7 : 3;
-  static constexpr int kVStages = kStages - kKStages;
+  static constexpr int kKStages = (PP || D == 64) ? DZ_KST : 3;
+  static constexpr int kVStages = (PP || D == 64) ? DZ_VST : 2;
+  static constexpr int kStages = kKStages + kVStages;
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = kQTileBytes;
   static constexpr int kRedOff = kKVOff + kStages * kStageBytes;  // row max / row sum exchange [2][BM]
-  static constexpr int kBarOff = kRedOff + 2 * BM * 4;
+  static constexpr int kOOff = kRedOff + 2 * BM * 4;              // epilogue O staging: 8 warps x 32 rows x D/2 bf16
+  static constexpr int kBarOff = kOOff + 8 * 32 * D;
   static constexpr int kSmem = kBarOff + 576 + 1024;              // + barriers/schedule + alignment slack
+  static_assert(kSmem <= 232448, "shared memory per CTA");
   static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, 2 * BM, BN / 2);  // f16 x f16, K-major, per half
   static constexpr uint32_t kIdescPV = ptx::idesc_f16(1, 1, 0, 1, 2 * BM, D);   // P (TMEM) x V (MN-major)
   static constexpr int kVRowBytes = D;                      // V half row: D/2 bf16
@@ -299,7 +307,8 @@ __device__ __forceinline__ int step_of(const SpanTable& st, int g, int k, int nq
 template <int D, bool PP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ out, int64_t o_bstride,
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                    __nv_bfloat16* __restrict__ out, int64_t o_bstride,
                     int64_t o_tstride, float* __restrict__ lse, uint8_t* __restrict__ tile_map, int B, int H,
                     int nq, int kv_len, float m_static, int dbg, float* __restrict__ ws, int* __restrict__ ws_cnt,
                     const __grid_constant__ SpanTable st) {
@@ -570,6 +579,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t pair_bar = 1 + quad;         // named barrier: the two warps of these rows
     constexpr uint32_t kSoftmaxBar = 5;         // named barrier: all 8 softmax warps
     const bool online = m_static <= 0.f;
+    // Epilogue store of this thread's row (D/2 bf16 = D/4 packed pairs, this warp's column half):
+    // through the warp's swizzled shared-memory staging tile and one TMA tensor store per warp
+    // (32 rows x D bytes), so the output leaves in whole 128-byte lines; rows past nq are clipped.
+    const uint32_t sOw = base + C::kOOff + warp * 32 * D;
+    auto store_o = [&](const uint32_t* pk, int b_, int h_, int qt_) {
+      constexpr int NC = D / 16;  // 16-byte chunks per staged row (D/2 bf16)
+      if (lane == 0) ptx::bulk_wait_read_all();  // the previous store has read the staging tile
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        ptx::st_shared_v4(sOw + lane * D + ((c ^ ((lane * D >> 7) & (NC - 1))) * 16), pk[4 * c], pk[4 * c + 1],
+                          pk[4 * c + 2], pk[4 * c + 3]);
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_4d(&tm_o, sOw, hc * (D / 2), h_, qt_ * BM + quad * 32, b_);
+        ptx::bulk_commit_group();
+      }
+    };
     uint32_t s_phase = 0, pe_phase = 0, of_phase = 0;
     int gsm = 0;  // executed steps so far (PP: this warp group takes the steps with gsm % 2 == hc)
     Sched sc = sched0;
@@ -744,32 +772,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       if (tl && n_seg < kTlSegs) tline[10 + 4 * n_seg] = (uint32_t)clock();
       const int s_idx = qt * BM + row;
-      __nv_bfloat16* orow = out + b * o_bstride + (int64_t)s_idx * o_tstride + (int64_t)h * D + hc * (D / 2);
       if (sg.k0 == 0 && sg.k1 == sg.cnt) {
-        // whole unit: O / l -> bf16 -> HBM (this warp's D/2 columns)
+        // whole unit: O / l -> bf16 -> HBM (this warp's D/2 columns).  O leaves TMEM first and is
+        // released at once, so the next unit's first PV does not wait for the global stores.
         const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
+        uint32_t r[D / 2];
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          uint32_t r[32];
-          __syncwarp();  // reconverge after the row-dependent store below
-          ptx::tmem_ld32(tO + c * 32, r);
-          ptx::tmem_wait_ld();
-          uint32_t pk[16];
+        for (int c = 0; c < D / 64; ++c) ptx::tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[c * 32]));
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));
+        {
+          uint32_t pk[D / 4];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
+          for (int i = 0; i < D / 4; ++i)
             pk[i] = ptx::pack_bf16x2(__uint_as_float(r[2 * i]) * inv_l, __uint_as_float(r[2 * i + 1]) * inv_l);
-          if (s_idx < nq) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              ptx::st_global_v4(orow + c * 32 + v * 8, pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
-          }
+          store_o(pk, b, h, qt);
         }
         if (lse != nullptr && hc == 0 && s_idx < nq)
           lse[((int64_t)b * H + h) * nq + s_idx] =
               (lt > 0.f) ? (m_used + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));
         if (tl && n_seg < kTlSegs) tline[11 + 4 * n_seg] = (uint32_t)clock();
         ++n_seg;
         continue;
@@ -779,38 +802,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // layout per (slot, rank): O [D][128] fp32 column-major (coalesced per column), l [128], m [128]
       constexpr int kSlotFloats = (D + 2) * BM;
       float* mine = ws + ((size_t)(2 * cid + (sg.k0 > 0 ? 0 : 1)) * 2 + rank) * kSlotFloats;
-#pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld32(tO + c * 32, r);
-        ptx::tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) __stcg(mine + (hc * (D / 2) + c * 32 + i) * BM + row, __uint_as_float(r[i]));
-      }
-      if (hc == 0) {
-        __stcg(mine + D * BM + row, lt);
-        __stcg(mine + (D + 1) * BM + row, m_used);
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));  // TMEM O has been read
-      if (tl && n_part < 2) tline[50 + 5 * n_part] = (uint32_t)clock();
-      // publish: every thread's stores precede the barrier; one thread fences (cumulative) and counts
-      ptx::named_bar_sync(kSoftmaxBar, 256);
       const int ustart = (b * H + h) * sched0.wbh + gpre[g];
       const int pf = pair_of(sched0.W, ncl, ustart), pl = pair_of(sched0.W, ncl, ustart + sg.cnt - 1);
       // pieces = pairs in [pf, pl] with a non-empty range (a pair's range may be empty when W < P)
       int n_pieces = 0;
       for (int q = pf; q <= pl; ++q) n_pieces += pair_lo(sched0.W, ncl, q) < pair_lo(sched0.W, ncl, q + 1);
       int* cnt_ptr = ws_cnt + (((int64_t)b * H + h) * n_groups + g) * 2 + rank;
-      if (threadIdx.x == 0) {
-        // acq_rel RMW at GPU scope: releases this CTA's piece (the barrier above made every
-        // softmax thread's stores precede it; release is cumulative) and, for the last
-        // piece, acquires the others' before the barrier below releases the readers
-        const bool last_piece = ptx::atom_add_acq_rel_gpu(cnt_ptr, 1) == n_pieces - 1;
-        bars->last_piece = last_piece;
-      }
+      // Every other piece already published (the usual case for the piece finishing last, e.g. a
+      // unit's head piece at the end of a pair's range): combine straight from TMEM, no publish.
+      if (threadIdx.x == 0) bars->last_piece = ptx::ld_acquire_gpu(cnt_ptr) == n_pieces - 1 ? 2 : 0;
       ptx::named_bar_sync(kSoftmaxBar, 256);
+      const bool direct = bars->last_piece == 2;  // (O leaves TMEM inside the combine loop below)
+#pragma unroll 1
+      for (int c = 0; c < D / 64 && !direct; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tO + c * 32, r);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) __stcg(mine + (hc * (D / 2) + c * 32 + i) * BM + row, __uint_as_float(r[i]));
+      }
+      if (!direct) {
+        if (hc == 0) {
+          __stcg(mine + D * BM + row, lt);
+          __stcg(mine + (D + 1) * BM + row, m_used);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));  // TMEM O has been read
+        if (tl && n_part < 2) tline[50 + 5 * n_part] = (uint32_t)clock();
+        // publish: every thread's stores precede the barrier; one thread fences (cumulative) and counts
+        ptx::named_bar_sync(kSoftmaxBar, 256);
+        if (threadIdx.x == 0) {
+          // acq_rel RMW at GPU scope: releases this CTA's piece (the barrier above made every
+          // softmax thread's stores precede it; release is cumulative) and, for the last
+          // piece, acquires the others' before the barrier below releases the readers
+          const bool last_piece = ptx::atom_add_acq_rel_gpu(cnt_ptr, 1) == n_pieces - 1;
+          bars->last_piece = last_piece;
+        }
+        ptx::named_bar_sync(kSoftmaxBar, 256);
+      }
       if (tl && n_part < 2) tline[51 + 5 * n_part] = (uint32_t)clock();
       if (!bars->last_piece) {
         if (tl && n_seg < kTlSegs) tline[11 + 4 * n_seg] = (uint32_t)clock();
@@ -821,12 +851,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // last piece to finish: combine all pieces of this unit in key order.  Each piece's
       // D/2 columns of this row are loaded in one batch (64 loads in flight per thread), so
       // a combine costs about one L2 round trip per piece.
+      // own piece (direct path): O from TMEM; base and total row sum are this thread's (both warps
+      // of a row hold the same m_used and lt)
+      const float m_own = m_used, l_own = lt;
       float mmax = -INFINITY;
 #pragma unroll 1
       for (int q = pf; q <= pl; ++q) {
         if (pair_lo(sched0.W, ncl, q) == pair_lo(sched0.W, ncl, q + 1)) continue;
         const float* pc = ws + ((size_t)(2 * q + (q == pf ? 1 : 0)) * 2 + rank) * kSlotFloats;
-        mmax = fmaxf(mmax, __ldcg(pc + (D + 1) * BM + row));
+        mmax = fmaxf(mmax, (direct && q == cid) ? m_own : __ldcg(pc + (D + 1) * BM + row));
       }
       float wsum = 0.f;
       float acc[D / 2];
@@ -837,25 +870,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (pair_lo(sched0.W, ncl, q) == pair_lo(sched0.W, ncl, q + 1)) continue;
         const float* pc = ws + ((size_t)(2 * q + (q == pf ? 1 : 0)) * 2 + rank) * kSlotFloats;
         float v[D / 2];
+        float mq, lq;
+        if (direct && q == cid) {
 #pragma unroll
-        for (int i = 0; i < D / 2; ++i) v[i] = __ldcg(pc + (hc * (D / 2) + i) * BM + row);
-        const float mq = __ldcg(pc + (D + 1) * BM + row);
-        const float lq = __ldcg(pc + D * BM + row);
+          for (int c = 0; c < D / 64; ++c) ptx::tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[c * 32]));
+          ptx::tmem_wait_ld();
+          mq = m_own;
+          lq = l_own;
+        } else {
+#pragma unroll
+          for (int i = 0; i < D / 2; ++i) v[i] = __ldcg(pc + (hc * (D / 2) + i) * BM + row);
+          mq = __ldcg(pc + (D + 1) * BM + row);
+          lq = __ldcg(pc + D * BM + row);
+        }
         const float wq = mq == -INFINITY ? 0.f : ptx::ex2(mq - mmax);  // fixed base: every mq = 0, wq = 1
         wsum += wq * lq;
 #pragma unroll
         for (int i = 0; i < D / 2; ++i) acc[i] = fmaf(wq, v[i], acc[i]);
       }
+      if (direct) {  // TMEM O has been read
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));
+      }
       const float inv_l = wsum > 0.f ? 1.f / wsum : 0.f;
       if (tl && n_part < 2) tline[52 + 5 * n_part] = (uint32_t)clock();
-      if (s_idx < nq) {
+      {
+        uint32_t pk[D / 4];
 #pragma unroll
-        for (int c8 = 0; c8 < D / 16; ++c8) {
-          const float* a8 = acc + c8 * 8;
-          ptx::st_global_v4(orow + c8 * 8, ptx::pack_bf16x2(a8[0] * inv_l, a8[1] * inv_l),
-                            ptx::pack_bf16x2(a8[2] * inv_l, a8[3] * inv_l), ptx::pack_bf16x2(a8[4] * inv_l, a8[5] * inv_l),
-                            ptx::pack_bf16x2(a8[6] * inv_l, a8[7] * inv_l));
-        }
+        for (int i = 0; i < D / 4; ++i) pk[i] = ptx::pack_bf16x2(acc[2 * i] * inv_l, acc[2 * i + 1] * inv_l);
+        store_o(pk, b, h, qt);
       }
       if (lse != nullptr && hc == 0 && s_idx < nq)
         lse[((int64_t)b * H + h) * nq + s_idx] =
@@ -867,6 +911,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ++n_comb;
       ++n_part;
     }
+    if (lane == 0) ptx::bulk_wait_all();  // the last epilogue stores have completed
     if (tl) {
       tline[1] = gtime();
       tline[3] = (uint32_t)clock();
@@ -887,7 +932,7 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
   auto k = attn_fwd_kernel<D, PP>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return e;
-  k<<<a.grid, kThreads, C::kSmem, s>>>(a.tm_q, a.tm_k, a.tm_v, static_cast<__nv_bfloat16*>(a.out), a.o_bstride,
+  k<<<a.grid, kThreads, C::kSmem, s>>>(a.tm_q, a.tm_k, a.tm_v, a.tm_o, static_cast<__nv_bfloat16*>(a.out), a.o_bstride,
                                        a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq, a.kv_len, a.m_static,
                                        a.debug_flags, a.ws, a.ws_cnt, a.spans);
   return cudaGetLastError();

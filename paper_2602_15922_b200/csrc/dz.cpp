@@ -343,6 +343,10 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
       !make_tmap(&a.tm_v, c->vslot(0, c->start), true, c->D, c->Hl, kv_len, c->B, bs, (uint32_t)c->D / 2,
                  (uint32_t)dz::attention_step_keys(c->m_static)))
     return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled failed");
+  // O rows are token-major with o_tstride == Hl * D (the caller's [B][n][H][D] or the SP local buffer)
+  if (o_tstride != (int64_t)c->Hl * c->D ||
+      !make_tmap(&a.tm_o, out_local, true, c->D, c->Hl, n, c->B, o_bstride, (uint32_t)c->D / 2, 32))
+    return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (O) failed");
   a.out = out_local;
   a.o_bstride = o_bstride;
   a.o_tstride = o_tstride;

@@ -54,6 +54,7 @@ struct AttnArgs {
   CUtensorMap tm_q;   // Q' fp16, dims (D, H, nq, B), box (64, 1, 128, 1), SW128
   CUtensorMap tm_k;   // K' fp16 cache, dims (D, H, kv_len, B)
   CUtensorMap tm_v;   // V  bf16 cache, dims (D, H, kv_len, B)
+  CUtensorMap tm_o;   // O  bf16 output, dims (D, H, nq, B), box (64, 1, 32, 1), SW128 (epilogue TMA stores)
   void* out = nullptr;            // bf16, row (b, s, h) at out + b*o_bstride + s*o_tstride + h*D
   int64_t o_bstride = 0, o_tstride = 0;
   float* lse = nullptr;           // optional fp32 [B][H][nq] natural-log LSE

@@ -122,6 +122,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long l
     for (int i = 0; i < 8; ++i) { float x, y; ptx::f2_unpack(v[i], x, y); sacc += a[i] + x + y + __uint_as_float(u[i]); }
     if (sacc == 1.2345f) cycles[100] = 1;
   }
+  if (ALU >= 30 && ALU < 40 && warp >= 4) {  // the K2 exponential block (exp_half<true>): poly share ALU - 30 of 8
+    constexpr int kP = ALU - 30;
+    float s[64];
+    for (int i = 0; i < 64; ++i) s[i] = ((threadIdx.x * 131 + i * 17) % 61) - 30.5f;
+    uint32_t x = 0;
+    for (int k = 0; *(volatile uint32_t*)&tbase != 0xFFFFFFFFu; ++k) {
+      uint64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        uint64_t xx = ptx::f2_pack(s[2 * i], s[2 * i + 1]);
+        uint64_t p;
+        if ((i % 8) >= 8 - kP) {
+          p = ptx::f2_exp2_poly<false>(xx);
+        } else {
+          float x0, x1;
+          ptx::f2_unpack(xx, x0, x1);
+          p = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+        }
+        acc[i % 4] = ptx::f2_add(acc[i % 4], p);
+        float p0, p1;
+        ptx::f2_unpack(p, p0, p1);
+        x ^= ptx::pack_bf16x2(p0, p1);
+      }
+      const uint64_t a = ptx::f2_add(ptx::f2_add(acc[0], acc[1]), ptx::f2_add(acc[2], acc[3]));
+      float a0, a1;
+      ptx::f2_unpack(a, a0, a1);
+      x += __float_as_uint(a0 + a1);
+      s[k & 63] = __uint_as_float(__float_as_uint(s[k & 63]) ^ (x & 1));
+    }
+    if (x == 0x12345) cycles[100] = x;
+  }
   if (TMEM_TRAFFIC && warp >= 4) {  // 8 warps: softmax-like S loads and P stores
     const uint32_t lanes = (uint32_t)((warp % 4) * 32) << 16;
     uint32_t r[32];
@@ -168,6 +199,16 @@ void run(const char* name, double instr_per_iter) {
 }
 
 int main() {
+  if (getenv("ONLY_K2")) {
+    run<2, true, false, 1, 0, 30>("TS+SS + 8 warps K2 exp (poly 0/8)", 16);
+    run<2, true, false, 1, 0, 31>("TS+SS + 8 warps K2 exp (poly 1/8)", 16);
+    run<2, true, false, 1, 0, 32>("TS+SS + 8 warps K2 exp (poly 2/8)", 16);
+    run<2, true, false, 1, 0, 33>("TS+SS + 8 warps K2 exp (poly 3/8)", 16);
+    run<2, true, false, 1, 0, 34>("TS+SS + 8 warps K2 exp (poly 4/8)", 16);
+    run<2, true, false, 1, 0, 9>("TS+SS + 8 warps poly (no clamp)", 16);
+    run<2, true, false, 1, 0, 3>("TS+SS + 8 warps FFMA", 16);
+    return 0;
+  }
   if (getenv("ONLY_ALU")) {
     run<2, true, false, 1, 0, 2>("TS+SS + 8 warps MUFU+poly math", 16);
     run<2, true, false, 1, 0, 20>("TS+SS + 6 warps MUFU+poly, SMSP0 free", 16);
