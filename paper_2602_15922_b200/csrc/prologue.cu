@@ -111,15 +111,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
                        static_cast<const uint8_t*>(a.x[w]) + src, (uint32_t)L.row_bytes, bar, pol);
   };
   // the token's D/2 rotation angles, one per 4th thread so every warp takes a share of the fp64 sincos
-  auto angles = [&](int k) {
+  // (the position is loaded one item ahead of its use, so the angle computation never waits on it)
+  const int ai = tid >> 2;  // 0 .. 63 >= D/2 - 1
+  const bool angle_thread = (tid & 3) == 0 && ai < D / 2;
+  auto load_pos = [&](int k) -> int {
     const int item = blockIdx.x + k * gridDim.x;
-    if (item >= n_items || (tid & 3) != 0) return;
-    const int ai = tid >> 2;  // 0 .. 63 >= D/2 - 1
-    if (ai >= D / 2) return;
-    const int t = item % a.n;
-    const double p = (double)__ldg(a.pos + 3 * t + a.axis[ai]);
+    if (item >= n_items || !angle_thread) return 0;
+    return __ldg(a.pos + 3 * (item % a.n) + a.axis[ai]);
+  };
+  auto angles = [&](int k, int p) {
+    const int item = blockIdx.x + k * gridDim.x;
+    if (item >= n_items || !angle_thread) return;
     double sn, cn;
-    sincos(p * a.omega[ai], &sn, &cn);
+    sincos((double)p * a.omega[ai], &sn, &cn);
     cs[(k % L.S) * (D / 2) + ai] = make_float2((float)cn, (float)sn);
   };
   __syncthreads();  // barriers initialised, row offsets visible
@@ -137,18 +141,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
       gk[i][e] = (gains_in_regs && h < H && a.gain[1]) ? __ldg(a.gain[1] + h * D + li * 8 + e) : 0.f;
     }
   }
-  angles(0);
+  angles(0, load_pos(0));
+  int pos_next = load_pos(1);
 
   for (int k = 0;; ++k) {
     const int item = blockIdx.x + k * gridDim.x;
     if (item >= n_items) break;
     const int b = item / a.n, t = item - b * a.n;
     const int st = k % L.S;
+    const int pos_k1 = pos_next;
+    pos_next = load_pos(k + 2);
     if (tid == 0) issue(k + L.S - 1);  // its stage was released by the __syncthreads ending item k - 1
     ptx::mbar_wait(bar0 + 8 * st, (uint32_t)((k / L.S) & 1));
     __syncthreads();  // angles of item k visible (written before the barrier that ended item k - 1)
     const uint8_t* stage = sm + st * L.stage_bytes;
-    const float2* csk = cs + st * (D / 2);
+    float2 csr[4];  // this thread's 4 rotation pairs (the same for every head and tensor of the item)
+    {
+      const float4* c4 = reinterpret_cast<const float4*>(cs + st * (D / 2) + li * 4);
+      const float4 c0 = c4[0], c1 = c4[1];
+      csr[0] = make_float2(c0.x, c0.y);
+      csr[1] = make_float2(c0.z, c0.w);
+      csr[2] = make_float2(c1.x, c1.y);
+      csr[3] = make_float2(c1.z, c1.w);
+    }
 #pragma unroll
     for (int w = 0; w < 3; ++w) {
       if (slot_of[w] < 0) continue;  // block-uniform
@@ -203,14 +218,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
           for (int e = 0; e < 4; ++e) {
             const float u = f[i][2 * e] * inv * gg[2 * e];
             const float x = f[i][2 * e + 1] * inv * gg[2 * e + 1];
-            const float2 c = csk[li * 4 + e];
+            const float2 c = csr[e];
             pk[e] = pack_half2((u * c.x - x * c.y) * sc, (u * c.y + x * c.x) * sc);
           }
           reinterpret_cast<uint4*>(o.base)[(base + rowoff[h]) / 8 + li] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
       }
     }
-    angles(k + 1);    // next item's angles into its own slot, off the critical path of the copies
+    angles(k + 1, pos_k1);  // next item's angles into its own slot, off the critical path of the copies
     __syncthreads();  // stage and angles of item k may be refilled
   }
 }

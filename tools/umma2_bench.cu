@@ -8,6 +8,8 @@
 
 using namespace dz;
 
+__device__ uint8_t g_src[1 << 20];  // L2-resident TMA source (ALU 41..44)
+
 template <int MODE, bool RANDOM, bool TMEM_TRAFFIC, int COMMIT_EVERY = 0, int FENCE = 0, int ALU = 0>  // 0: SS N=128 (QK-like), 1: TS N=128 (PV-like), 2: TS+SS 8+8
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long long* cycles, int iters) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -93,7 +95,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long l
     }
     if (acc == 0x12345) cycles[100] = acc;
   }
-  if (ALU >= 3 && warp >= 4) {  // 8 warps of one instruction kind only (which pipes interfere with the MMA?)
+  if (ALU >= 3 && ALU < 30 && warp >= 4) {  // 8 warps of one instruction kind only (which pipes interfere with the MMA?)
     float a[16];
     uint64_t v[8];
     uint32_t u[8];
@@ -153,6 +155,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long l
     }
     if (x == 0x12345) cycles[100] = x;
   }
+  if (ALU >= 41 && ALU <= 44 && warp == 5) {  // TMA bulk loads (16 KB each, ALU - 40 in flight) into smem [64K, 96K)
+    constexpr int kIn = ALU - 40;
+    __shared__ uint64_t tbar[4];
+    if ((threadIdx.x % 32) == 0) {
+      for (int i = 0; i < 4; ++i) ptx::mbar_init(ptx::smem_u32(&tbar[i]), 1);
+      ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t k = 0, ph[4] = {0, 0, 0, 0};
+    const uint64_t pol = ptx::l2_policy_evict_last();
+    while (*(volatile uint32_t*)&tbase != 0xFFFFFFFFu) {
+      const int sl = k % kIn;
+      if ((threadIdx.x % 32) == 0) {
+        if (k >= (uint32_t)kIn) { ptx::mbar_wait(ptx::smem_u32(&tbar[sl]), ph[sl]); ph[sl] ^= 1; }
+        ptx::mbar_arrive_expect_tx(ptx::smem_u32(&tbar[sl]), 16384);
+        ptx::bulk_load(base + 65536 + (sl % 2) * 16384, g_src + ((k * 16384u) & ((1u << 20) - 1)), 16384,
+                       ptx::smem_u32(&tbar[sl]), pol);
+      }
+      __syncwarp();
+      ++k;
+    }
+    if ((threadIdx.x % 32) == 0 && k > 0) {
+      for (int i = 0; i < kIn && i < (int)k; ++i) { const int sl = (k - 1 - i) % kIn; ptx::mbar_wait(ptx::smem_u32(&tbar[sl]), ph[sl]); ph[sl] ^= 1; }
+    }
+    if ((threadIdx.x % 32) == 0) atomicMax((unsigned long long*)&cycles[101], (unsigned long long)k);
+  }
   if (TMEM_TRAFFIC && warp >= 4) {  // 8 warps: softmax-like S loads and P stores
     const uint32_t lanes = (uint32_t)((warp % 4) * 32) << 16;
     uint32_t r[32];
@@ -172,7 +200,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long l
 template <int MODE, bool RANDOM, bool TT, int CE = 0, int FE = 0, int AL = 0>
 void run(const char* name, double instr_per_iter) {
   long long* d;
-  cudaMalloc(&d, 74 * sizeof(long long));
+  cudaMalloc(&d, 128 * sizeof(long long));
+  cudaMemset(d, 0, 128 * sizeof(long long));
   const int iters = 4096;
   auto k = bench<MODE, RANDOM, TT, CE, FE, AL>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
@@ -193,12 +222,24 @@ void run(const char* name, double instr_per_iter) {
   avg /= 74;
   const double instrs = iters * instr_per_iter;
   const double flop = 74.0 * instrs * 2.0 * 256 * 128 * 16;
+  long long tma_loads = 0;
+  cudaMemcpy(&tma_loads, d + 101, sizeof tma_loads, cudaMemcpyDeviceToHost);
+  if (tma_loads) printf("[TMA: %.1f B/clk per CTA] ", tma_loads * 16384.0 / avg);
   printf("%-30s cyc/instr %7.2f (ideal 64)  %8.1f TFLOP/s  err=%s\n", name, avg / instrs, flop / (ms * 1e-3) / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 
 int main() {
+  if (getenv("ONLY_TMA")) {
+    run<0, true, false, 1, 0, 41>("SS + TMA 16KB x1 in flight", 8);
+    run<0, true, false, 1, 0, 42>("SS + TMA 16KB x2 in flight", 8);
+    run<0, true, false, 1, 0, 44>("SS + TMA 16KB x4 in flight", 8);
+    run<2, true, false, 1, 0, 42>("TS+SS + TMA 16KB x2", 16);
+    run<2, true, false, 1, 0, 44>("TS+SS + TMA 16KB x4", 16);
+    run<1, true, false, 1, 0, 44>("TS + TMA 16KB x4", 8);
+    return 0;
+  }
   if (getenv("ONLY_K2")) {
     run<2, true, false, 1, 0, 30>("TS+SS + 8 warps K2 exp (poly 0/8)", 16);
     run<2, true, false, 1, 0, 31>("TS+SS + 8 warps K2 exp (poly 1/8)", 16);
