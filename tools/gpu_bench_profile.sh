@@ -11,3 +11,6 @@ timeout 300 $SHORT > $OUT/short.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $SHORT > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 4 -c 1 -o $OUT/attn_full -f $SHORT > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
 tail -5 $OUT/ncu_full.log
+# K1 prologue (attend: Q, K, V) and K4 append: one full capture each (launches 5 and 6 of the short run)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:prologue -s 4 -c 2 -o $OUT/pro_full -f $SHORT > $OUT/ncu_pro.log 2>&1; echo "ncu prologue rc=$?"
+timeout 300 python tools/copy_bench.py > $OUT/copy_bench.txt 2>&1; cat $OUT/copy_bench.txt
