@@ -249,11 +249,32 @@ struct Sched {
   int lo, hi, wbh, W;  // stream-K: this pair's range, steps per (b, h), total steps (host keeps W * P < 2^31)
   int P;               // pairs
   int u;               // round-robin: next unit
+  int rr_end;          // hybrid (one span): units [0, rr_end) are dealt whole, unit u to pair u % P
+  int x0;              // ... and stream-K covers the executed steps [x0, W) of the remaining units
 };
+// stream-K range boundary of pair p (ranges split [x0, W) evenly)
+__device__ __forceinline__ int pair_lo(const Sched& sc, int p) { return sc.x0 + (sc.W - sc.x0) * p / sc.P; }
+__device__ __forceinline__ int pair_of(const Sched& sc, int x) {
+  int p = (int)((int64_t)(x - sc.x0) * sc.P / (sc.W - sc.x0));
+  while (p + 1 < sc.P && pair_lo(sc, p + 1) <= x) ++p;
+  while (p > 0 && pair_lo(sc, p) > x) --p;
+  return p;
+}
 template <int TK>
 __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_groups, int n_units, int H,
                                       const SpanTable& st, int nq, int kv_len, int nkv, Seg& sg) {
   if (sc.streamk) {
+    if (sc.u < sc.rr_end) {  // hybrid: whole units, dealt round-robin (all query groups of a head at once)
+      const int u = sc.u;
+      sc.u += sc.P;
+      sg.g = u % n_groups;
+      const int bh = u / n_groups;
+      sg.h = bh % H;
+      sg.b = bh / H;
+      sg.k0 = 0;
+      sg.k1 = sg.cnt = nkv;
+      return true;
+    }
     if (sc.lo >= sc.hi) return false;
     const int bh = sc.lo / sc.wbh;
     const int r = sc.lo - bh * sc.wbh;
@@ -283,14 +304,6 @@ __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_g
   }
   sg.k1 = sg.cnt = cnt;
   return true;
-}
-// stream-K range boundary of pair p
-__device__ __forceinline__ int pair_lo(int W, int P, int p) { return W * p / P; }
-__device__ __forceinline__ int pair_of(int W, int P, int x) {
-  int p = x * P / W;
-  while (p + 1 < P && pair_lo(W, P, p + 1) <= x) ++p;
-  while (p > 0 && pair_lo(W, P, p) > x) --p;
-  return p;
 }
 // key step of the k-th executed step of group g (k counted from the group's first executed step)
 template <int TK>
@@ -398,11 +411,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   sched0.streamk = streamk;
   sched0.P = ncl;
   sched0.u = cid;
+  sched0.rr_end = 0;
+  sched0.x0 = 0;
   if (streamk) {
     sched0.wbh = gpre[n_groups];
     sched0.W = B * H * sched0.wbh;
-    sched0.lo = pair_lo(sched0.W, ncl, cid);
-    sched0.hi = pair_lo(sched0.W, ncl, cid + 1);
+    // One span (uniform units): all but the last ~1.x waves of units are dealt whole, round-robin,
+    // so the query groups of a head run side by side and its K/V is read from HBM about once;
+    // stream-K balances the rest.  (Pure stream-K would spread each head's groups over the
+    // whole launch, and the K/V of every head would have to stay in L2 from start to end.)
+    if (st.n == 1 && n_units >= 2 * ncl) {
+      sched0.rr_end = (n_units / ncl - 1) * ncl;
+      sched0.x0 = sched0.rr_end * nkv;
+    }
+    sched0.lo = pair_lo(sched0, cid);
+    sched0.hi = pair_lo(sched0, cid + 1);
   }
 
   if (warp >= 8) {
@@ -803,10 +826,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       constexpr int kSlotFloats = (D + 2) * BM;
       float* mine = ws + ((size_t)(2 * cid + (sg.k0 > 0 ? 0 : 1)) * 2 + rank) * kSlotFloats;
       const int ustart = (b * H + h) * sched0.wbh + gpre[g];
-      const int pf = pair_of(sched0.W, ncl, ustart), pl = pair_of(sched0.W, ncl, ustart + sg.cnt - 1);
+      const int pf = pair_of(sched0, ustart), pl = pair_of(sched0, ustart + sg.cnt - 1);
       // pieces = pairs in [pf, pl] with a non-empty range (a pair's range may be empty when W < P)
       int n_pieces = 0;
-      for (int q = pf; q <= pl; ++q) n_pieces += pair_lo(sched0.W, ncl, q) < pair_lo(sched0.W, ncl, q + 1);
+      for (int q = pf; q <= pl; ++q) n_pieces += pair_lo(sched0, q) < pair_lo(sched0, q + 1);
       int* cnt_ptr = ws_cnt + (((int64_t)b * H + h) * n_groups + g) * 2 + rank;
       // Every other piece already published (the usual case for the piece finishing last, e.g. a
       // unit's head piece at the end of a pair's range): combine straight from TMEM, no publish.
@@ -857,7 +880,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       float mmax = -INFINITY;
 #pragma unroll 1
       for (int q = pf; q <= pl; ++q) {
-        if (pair_lo(sched0.W, ncl, q) == pair_lo(sched0.W, ncl, q + 1)) continue;
+        if (pair_lo(sched0, q) == pair_lo(sched0, q + 1)) continue;
         const float* pc = ws + ((size_t)(2 * q + (q == pf ? 1 : 0)) * 2 + rank) * kSlotFloats;
         mmax = fmaxf(mmax, (direct && q == cid) ? m_own : __ldcg(pc + (D + 1) * BM + row));
       }
@@ -867,7 +890,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int i = 0; i < D / 2; ++i) acc[i] = 0.f;
 #pragma unroll 1
       for (int q = pf; q <= pl; ++q) {
-        if (pair_lo(sched0.W, ncl, q) == pair_lo(sched0.W, ncl, q + 1)) continue;
+        if (pair_lo(sched0, q) == pair_lo(sched0, q + 1)) continue;
         const float* pc = ws + ((size_t)(2 * q + (q == pf ? 1 : 0)) * 2 + rank) * kSlotFloats;
         float v[D / 2];
         float mq, lq;
