@@ -55,9 +55,31 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="warm L2 (secondary measurement)")
+    ap.add_argument("--tf-chunks", type=int, default=4, help="tf mode: M clean + M noisy chunks")
+    ap.add_argument("--mode", choices=["chunk", "denoise", "tf"], default="chunk",
+                    help="chunk: attend + evict + append per step; denoise: the denoising steps of one "
+                         "chunk over a fixed cache (Alg. 2 update=False; C3: 4 steps x CFG batch 2); tf: the "
+                         "teacher-forcing training layout [C0..C_{M-1}; Z1..Z_M] of Fig. 10(a) in one attend_spans")
+    ap.add_argument("--denoise-steps", type=int, default=None, help="denoise mode: steps per chunk "
+                    "(default: the workload's, C3 = 4)")
+    ap.add_argument("--graph", action="store_true", help="denoise mode: replay the steps as one CUDA graph")
     ap.add_argument("--flush-read", action="store_true",
                     help="after the 512 MB flush write, read 256 MB of it so no dirty flush lines stay in L2")
     return ap.parse_args()
+
+
+def visible_pairs(spans) -> int:
+    """Visible (query, key) pairs of a span layout under the Fig. 10 rule (PAPER.md l.505,
+    DESIGN.md R3): a NOISY query of chunk k sees CLEAN keys of chunks < k and its own span;
+    a CLEAN query of chunk j sees CLEAN keys of chunks <= j.  (Checked against the oracle's
+    pair enumeration in tests/test_bench_host.py.)"""
+    total = 0
+    for i, qs in enumerate(spans):
+        qth = qs.chunk if qs.kind == synth.NOISY else qs.chunk + 1
+        for j, ks in enumerate(spans):
+            if i == j or (ks.kind == synth.CLEAN and ks.chunk < qth):
+                total += qs.n_tokens * ks.n_tokens
+    return total
 
 
 def peaks():
@@ -250,7 +272,8 @@ def main():
     def dev_chunk(x):   # [B][n][H][D] bf16 -> this rank's tokens on the device
         return x[:, sl].contiguous().to(dev)
 
-    streams = [synth.draw_stream(w, b, steps=2) for b in range(w.batch)]
+    S = (args.denoise_steps or w.steps) if args.mode == "denoise" else 1
+    streams = [synth.draw_stream(w, b, steps=max(2, S)) for b in range(w.batch)]
     stack = lambda key, c: torch.stack([getattr(s, key)[c] for s in streams])
     for c in range(C):
         cache.append(dev_chunk(stack("cache_k", c)), dev_chunk(stack("cache_v", c)),
@@ -269,12 +292,53 @@ def main():
         cache.append(kkc, vvc, pp, cid)    # ... and the ground-truth chunk enters
         chunk_id[0] += 1
 
+    graph = None
+    flop_one = w.useful_flop()
+    if args.mode == "tf":
+        # Fig. 10(a) teacher forcing at the Wan shape: M clean chunks then M noisy chunks, one call
+        tf_spans = synth.teacher_forcing_spans(args.tf_chunks, n)
+        n_tf = sum(sp.n_tokens for sp in tf_spans)
+        tq, tk, tv, tpos = synth.span_inputs(w, tf_spans)
+        tf_cache = dz.ChunkKVCache(w.batch, H, D, 0, n_tf, w.rope_dims, gq.to(dev), gk.to(dev),
+                                   rope_theta=w.rope_theta, rms_eps=w.rms_eps, flags=dz.FLAG_PROFILE, device=dev)
+        tq, tk, tv = (x[None].expand(w.batch, -1, -1, -1).contiguous().to(dev) for x in (tq, tk, tv))
+        tpos = tpos.to(dev)
+        tout = torch.empty_like(tq)
+        span_list = [(sp.chunk, sp.kind, sp.n_tokens) for sp in tf_spans]
+        flop_one = 4.0 * D * w.batch * H * visible_pairs(tf_spans)
+        cache = tf_cache
+
+        def tf_step():
+            tf_cache.attend_spans(tq, tk, tv, tpos, span_list, out=tout)
+
+        step = tf_step
+    if args.mode == "denoise":
+        # S denoising steps of chunk C over the fixed cache: new Q, K, V per step (Alg. 2 l.584-585)
+        qs = [[dev_chunk(stack(x, st)) for x in ("cur_q", "cur_k", "cur_v")] for st in range(S)]
+        outs = [torch.empty_like(q) for _ in range(S)]
+
+        def denoise():
+            for st in range(S):
+                cache.attend(*qs[st], pos, C, out=outs[st])
+
+        step = denoise
+        if args.graph:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                denoise()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                denoise()
+            step = graph.replay
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
 
     # ---------------- timed region: per-step CUDA events, L2 flushed between steps
-    flop_step = w.useful_flop()                      # global useful FLOP of one step
+    flop_step = flop_one * S                         # global useful FLOP of one step
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     attn_ms, pro_ms, app_ms = [], [], []
     if pg:
@@ -289,10 +353,11 @@ def main():
             ev[i][0].record()
             step()
             ev[i][1].record()
-            prof = cache.profile_last()             # host-syncs on the library's events
-            attn_ms.append(prof["attention"])
-            pro_ms.append(prof["prologue"])
-            app_ms.append(prof["append"])
+            if graph is None:
+                prof = cache.profile_last()         # host-syncs on the library's events (last call)
+                attn_ms.append(prof["attention"])
+                pro_ms.append(prof["prologue"])
+                app_ms.append(prof["append"])
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
@@ -305,7 +370,7 @@ def main():
 
     # ---------------- end to end through the public API with host buffers
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and args.mode == "chunk":  # (other modes: device-resident only)
         pin = lambda x: x.cpu().pin_memory()
         hq, hk, hv, hkc, hvc, hpos = (pin(x) for x in (q, k, v, kc, vc, pos))
         hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
@@ -334,8 +399,11 @@ def main():
                "path": "pinned host -> ChunkKVCache.attend/append/evict -> pinned host"}
 
     peak, peak_sus, hbm, src = peaks()
+    if graph is not None:   # no per-kernel events inside a graph: K1 + K2 of every step together
+        attn_ms = [m / S for m in step_ms]
+        pro_ms, app_ms = [float("nan")], [float("nan")]
     attn_mean = statistics.mean(attn_ms)
-    flop_launch = flop_step / N
+    flop_launch = flop_step / N / S
     achieved = flop_launch / (attn_mean * 1e-3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_attention_traffic.json")
@@ -343,7 +411,8 @@ def main():
         d = json.load(open(tp))
         if d.get("workload") == w.name:
             traffic = d.get("dram_bytes_per_launch")
-    pro_bytes = 2 * 3 * w.batch * n_loc * H * D * 2     # read q,k,v + write q',k',v (bf16/fp16)
+    n_new = n_tf if args.mode == "tf" else n_loc
+    pro_bytes = 2 * 3 * w.batch * n_new * H * D * 2     # read q,k,v + write q',k',v (bf16/fp16)
     app_bytes = 2 * 2 * w.batch * n_loc * H * D * 2     # read k,v + write k',v
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": N, "steps": args.steps,
@@ -352,21 +421,27 @@ def main():
         "config": {"workload": w.name, "batch": w.batch, "heads": H, "head_dim": D, "chunk_tokens": n,
                    "cache_tokens": w.cache_tokens, "kv_tokens": w.kv_tokens, "useful_flop_per_step": flop_step,
                    "parallelism": "single GPU" if N == 1 else f"ulysses sp{N}",
-                   "step": "attend (K1+K2) + append (K4) + evict, sliding window",
+                   "step": ("attend (K1+K2) + append (K4) + evict, sliding window" if args.mode == "chunk" else
+                            f"teacher forcing [C0..C{args.tf_chunks - 1}; Z1..Z{args.tf_chunks}] x {n} tokens, "
+                            "one attend_spans (K1+K2, SKIP tiles never loaded)" if args.mode == "tf" else
+                            f"{S} denoising steps of one chunk (K1+K2 each) over a fixed cache"
+                            + (", one CUDA graph replay" if graph is not None else ", eager")),
                    "l2": "flushed before every timed step (512 MB write)" if not args.no_flush else "warm",
                    "qk_storage": "fp16 (post-RMSNorm)", "pv": "bf16", "accumulate": "fp32"},
         "pct_peak": value / (N * peak), "pct_peak_sustained": value / (N * peak_sus),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "attn_fwd_kernel (K2)",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "attn_fwd_kernel (K2)" if graph is None else "K1 + K2 per denoise step (graph replay)",
                      "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({src}, burst)",
                      "frac_vs_sustained": achieved / peak_sus, "attn_ms_mean": attn_mean,
                      "flop_per_launch": flop_launch},
-        "kernels": {"prologue_ms": statistics.mean(pro_ms),
+        "kernels": {"prologue_ms": statistics.mean(pro_ms),  # (denoise mode: the last step's; graph: n/a)
                     "prologue_gbs": pro_bytes / (statistics.mean(pro_ms) * 1e-3) / 1e9,
                     "append_ms": statistics.mean(app_ms),
-                    "append_gbs": app_bytes / (statistics.mean(app_ms) * 1e-3) / 1e9 if N == 1 else None,
+                    "append_gbs": (app_bytes / (statistics.mean(app_ms) * 1e-3) / 1e9
+                                   if N == 1 and args.mode == "chunk" and statistics.mean(app_ms) > 0 else None),
                     "hbm_peak_gbs": hbm},
-        "gpu_launches": args.steps * (3 if N == 1 else 4),
+        "gpu_launches": args.steps * ((3 if N == 1 else 4) if args.mode == "chunk" else 2 * S),  # K1, K2 (K4)
         "clocks": clk.summary(),
         "e2e": e2e,
         "parity": "tests/test_gpu_parity.py (pytest -m gpu); bench.py runs no oracle on the GPU arm",

@@ -64,7 +64,10 @@ constexpr float kRescaleLog2 = 8.0f;
 constexpr int kPolyPairs = DZ_POLY;  // of every 8 exp2 pairs, this many go to the FMA-pipe polynomial (measured on the ping-pong kernel: 0/2/3/4 -> 234/205/212/218 us)
 constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr int kWarpMma = 11, kWarpTma = 10, kWarpPv = 9, kWarpTmem = 8;
-constexpr uint32_t kRegsLight = 88, kRegsSoftmax = 208;  // setmaxnreg: 128*88 + 256*208 = 384*168 (launch)
+// setmaxnreg split, 128 * light + 256 * softmax = 384 * 168 (launch): ping-pong 104/200 (measured on
+// C1: 88/208 182.8 us, 104/200 178.0, 120/192 179.7), lock-step 88/208 (its softmax holds more state)
+template <bool PP> __host__ __device__ constexpr uint32_t regs_light() { return PP ? 104 : 88; }
+template <bool PP> __host__ __device__ constexpr uint32_t regs_softmax() { return PP ? 200 : 208; }
 
 // Cycle trace of cluster 0's first unit (diagnostics, dz_debug_trace), per CTA
 // rank r at [r * 16 * kTraceSteps]: per step j [8j+0,1] QK wait/issue,
@@ -103,6 +106,8 @@ __device__ __forceinline__ uint32_t gtime() {
 // PP (ping-pong, fixed softmax base): 128-key steps, S and P double-buffered, the two
 // softmax warp groups take alternate steps.  !PP (online base): 256-key steps, each step
 // split in two key halves between the two warp groups.
+constexpr int kClsWords = kMaxStepTiles / 16;  // step-class table (several spans): 16 KB static shared memory
+
 template <int D, bool PP>
 struct Cfg {
   static constexpr int kBN = PP ? 128 : 256;               // keys per step
@@ -124,9 +129,10 @@ struct Cfg {
   static constexpr int kKVOff = kQTileBytes;
   static constexpr int kRedOff = kKVOff + kStages * kStageBytes;  // row max / row sum exchange [2][BM]
   static constexpr int kOOff = kRedOff + 2 * BM * 4;              // epilogue O staging: 8 warps x 32 rows x D/2 bf16
+  static constexpr bool kTab = PP || D == 64;                     // static step-class table fits beside
   static constexpr int kBarOff = kOOff + 8 * 32 * D;
   static constexpr int kSmem = kBarOff + 576 + 1024;              // + barriers/schedule + alignment slack
-  static_assert(kSmem <= 232448, "shared memory per CTA");
+  static_assert(kSmem + (kTab ? kClsWords * 4 : 0) <= 232448, "shared memory per CTA");
   static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, 2 * BM, BN / 2);  // f16 x f16, K-major, per half
   static constexpr uint32_t kIdescPV = ptx::idesc_f16(1, 1, 0, 1, 2 * BM, D);   // P (TMEM) x V (MN-major)
   static constexpr int kVRowBytes = D;                      // V half row: D/2 bf16
@@ -211,6 +217,19 @@ __device__ __forceinline__ uint8_t step_class(const SpanTable& st, int g, int j,
   }
   return !any ? kSkip : (all ? kFull : kPartial);
 }
+// Executed-step classes of the (query group, key step) tiles with several spans: 2 bits per tile
+// (the rows_in_bounds class: SKIP, PARTIAL = needs a mask, FULL), built once per CTA in static
+// shared memory so the single-thread roles (MMA issuers, TMA producers) never evaluate span loops
+// on their critical path.  With one span, or a table too large, the class is evaluated on the fly.
+__shared__ uint32_t s_cls_tab[kClsWords];
+template <int TK, bool kTab>
+__device__ __forceinline__ uint8_t cls_get(const SpanTable& st, int g, int j, int nq, int kv_len, int nkv) {
+  if (kTab) {  // (the host rejects span layouts whose table would not fit: dz_attend_spans -> DZ_ESHAPE)
+    const int x = g * nkv + j;
+    return (uint8_t)((s_cls_tab[x >> 4] >> (2 * (x & 15))) & 3u);
+  }
+  return step_class<TK>(st, g, j, nq, kv_len, true);
+}
 // set bits [lo, hi) of a 128-bit mask
 __device__ __forceinline__ void set_bits(uint32_t (&m)[4], int lo, int hi) {
 #pragma unroll
@@ -260,7 +279,7 @@ __device__ __forceinline__ int pair_of(const Sched& sc, int x) {
   while (p > 0 && pair_lo(sc, p) > x) --p;
   return p;
 }
-template <int TK>
+template <int TK, bool kTab>
 __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_groups, int n_units, int H,
                                       const SpanTable& st, int nq, int kv_len, int nkv, Seg& sg) {
   if (sc.streamk) {
@@ -300,18 +319,18 @@ __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_g
   int cnt = nkv;  // whole unit: all of its executed steps
   if (st.n != 1) {
     cnt = 0;
-    for (int j = 0; j < nkv; ++j) cnt += step_class<TK>(st, sg.g, j, nq, kv_len) != kSkip;
+    for (int j = 0; j < nkv; ++j) cnt += cls_get<TK, kTab>(st, sg.g, j, nq, kv_len, nkv) != kSkip;
   }
   sg.k1 = sg.cnt = cnt;
   return true;
 }
 // key step of the k-th executed step of group g (k counted from the group's first executed step)
-template <int TK>
+template <int TK, bool kTab>
 __device__ __forceinline__ int step_of(const SpanTable& st, int g, int k, int nq, int kv_len, int nkv) {
   if (st.n == 1) return k;
   int j = 0;
   for (;; ++j) {
-    if (step_class<TK>(st, g, j, nq, kv_len) == kSkip) continue;
+    if (cls_get<TK, kTab>(st, g, j, nq, kv_len, nkv) == kSkip) continue;
     if (k-- == 0) return j;
   }
 }
@@ -363,6 +382,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   // executed steps per query group -> prefix sums (every role walks the same schedule)
   const bool streamk = ws != nullptr && n_groups <= kMaxGroups;
+  constexpr bool kTab = C::kTab;
+  if (kTab && st.n != 1) {
+    for (int i = threadIdx.x; i < (n_groups * nkv + 15) / 16; i += kThreads) s_cls_tab[i] = 0u;
+    __syncthreads();
+    for (int x = threadIdx.x; x < n_groups * nkv; x += kThreads) {
+      const uint32_t c = step_class<BN>(st, x / nkv, x % nkv, nq, kv_len, true);
+      if (c != 0u) atomicOr(&s_cls_tab[x >> 4], c << (2 * (x & 15)));
+    }
+    __syncthreads();
+  }
   if (streamk) {
     if (st.n == 1) {
       for (int g = threadIdx.x; g <= n_groups; g += kThreads) bars->gpre[g] = g * nkv;
@@ -370,7 +399,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int g = threadIdx.x; g <= n_groups; g += kThreads) bars->gpre[g] = 0;
       __syncthreads();
       for (int x = threadIdx.x; x < n_groups * nkv; x += kThreads)
-        if (step_class<BN>(st, x / nkv, x % nkv, nq, kv_len) != kSkip) atomicAdd(&bars->gpre[x / nkv + 1], 1);
+        if (cls_get<BN, kTab>(st, x / nkv, x % nkv, nq, kv_len, nkv) != kSkip)
+          atomicAdd(&bars->gpre[x / nkv + 1], 1);
       __syncthreads();
       if (threadIdx.x == 0)
         for (int g = 1; g <= n_groups; ++g) bars->gpre[g] += bars->gpre[g - 1];
@@ -429,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 
   if (warp >= 8) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsLight));
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(regs_light<PP>()));
   if (warp == kWarpTma || warp == kWarpTmem) {
     // ------------------------------------------------ TMA producers (K + Q, V) --
     // warp kWarpTma loads each piece's Q tiles and the K tiles into the K ring; warp
@@ -441,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     Sched sc = sched0;
     Seg sg;
     bool first_seg = true;
-    while (next_seg<BN>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+    while (next_seg<BN, kTab>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
       const int b = sg.b, h = sg.h, g = sg.g;
       if (do_k) {
         ptx::mbar_wait(bar(bars->q_empty), q_phase ^ 1);
@@ -454,10 +484,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * 64, h, qt * BM, b, pol_q);
         }
       }
-      int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
+      int j = step_of<BN, kTab>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j, ++ld) {
         if (st.n != 1)
-          while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+          while (cls_get<BN, kTab>(st, g, j, nq, kv_len, nkv) == kSkip) ++j;
         uint32_t sl, ph;
         if (do_k)
           kslot(ld, sl, ph);
@@ -500,12 +530,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     Sched sc = sched0;
     Seg sg;
     bool first_seg = true;
-    while (next_seg<BN>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+    while (next_seg<BN, kTab>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
       const int g = sg.g;
-      int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
+      int j = step_of<BN, kTab>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j) {
         if (st.n != 1)
-          while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+          while (cls_get<BN, kTab>(st, g, j, nq, kv_len, nkv) == kSkip) ++j;
         const bool first = k == sg.k0, last = k == sg.k1 - 1;
         const bool tr = trace_on && first_seg && j < kTraceSteps && lane == 0;
         if (do_qk) {
@@ -590,7 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(regs_softmax<PP>()));
     // ---------------------------------------------- softmax + epilogue --
     const int quad = warp % 4;                  // TMEM lane quadrant (query rows)
     const int hc = warp / 4;                    // key half of S / column half of O
@@ -633,7 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tline[0] = gtime();
       tline[2] = (uint32_t)clock();
     }
-    while (next_seg<BN>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
+    while (next_seg<BN, kTab>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
       const int b = sg.b, h = sg.h, g = sg.g;
       const int qt = 2 * g + (int)rank;
       if (tl && n_seg < kTlSegs) tline[8 + 4 * n_seg] = (uint32_t)clock();
@@ -642,7 +672,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int s_row = qt * BM + row;            // this thread's query (row of the new tokens)
       const int qs = st.n == 1 ? 0 : span_at(st, min(s_row, nq - 1));  // its span (rows past nq: never stored)
       const bool map_thread = tile_map != nullptr && b == 0 && h == 0 && rank == 0 && row == 0 && hc == 0;
-      int j = step_of<BN>(st, g, sg.k0, nq, kv_len, nkv);
+      int j = step_of<BN, kTab>(st, g, sg.k0, nq, kv_len, nkv);
       // fast walk (PP, one span, no tile map): every step executes, so this group's steps
       // are every other one -- no per-step bookkeeping for the other group's steps
       const int gsm0 = gsm;
@@ -657,7 +687,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           my_u = (gsm0 + (k - sg.k0)) >> 1;
         } else {
           if (st.n != 1)
-            while (step_class<BN>(st, g, j, nq, kv_len) == kSkip) ++j;
+            while (cls_get<BN, kTab>(st, g, j, nq, kv_len, nkv) == kSkip) ++j;
           // executed steps only; the host zeroes (SKIP) the map
           if (map_thread) tile_map[g * nkv + j] = step_class<BN>(st, g, j, nq, kv_len);
           my_u = gsm >> 1;
@@ -666,7 +696,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // mask needed iff an in-bounds row of the tile misses a key of the step (Fig. 10 or key
         // bounds); one span (attend_chunk): only a ragged last key step
         const bool masked = st.n == 1 ? (j == nkv - 1 && kv_len % BN != 0)
-                                      : step_class<BN>(st, g, j, nq, kv_len, true) == kPartial;
+                                      : cls_get<BN, kTab>(st, g, j, nq, kv_len, nkv) == kPartial;
         if constexpr (PP) {
           ptx::mbar_wait(bar(bars->s_full[hc]), my_u & 1);
         } else {
@@ -994,5 +1024,9 @@ cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s) {
 }
 
 int attention_step_keys(float m_static) { return m_static > 0.f ? 128 : 256; }
+
+bool attention_has_step_table(int32_t D, float m_static) {
+  return D == 128 ? Cfg<128, true>::kTab && m_static > 0.f : true;  // Cfg<D, PP>::kTab
+}
 
 }  // namespace dz

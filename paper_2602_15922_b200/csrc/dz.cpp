@@ -581,6 +581,13 @@ dz_status dz_attend_spans(dz_ctx* c, const void* q_raw, const void* k_raw, const
   if (n % c->N) return fail(c, DZ_ESHAPE, "%lld tokens not a multiple of world_size %d", (long long)n, c->N);
   if (n > c->cfg.max_chunk_tokens)
     return fail(c, DZ_ECAPACITY, "%lld span tokens exceed max_chunk_tokens %d", (long long)n, c->cfg.max_chunk_tokens);
+  if (n_spans > 1) {  // K2 keeps the (query group, key step) classes of a span layout in a 65536-tile table
+    const int step_keys = dz::attention_step_keys(c->m_static);
+    const int64_t tiles = ((n + dz::kTileQ - 1) / dz::kTileQ) * ((c->valid + n + step_keys - 1) / step_keys);
+    if (dz::attention_has_step_table(c->D, c->m_static) && tiles > dz::kMaxStepTiles)
+      return fail(c, DZ_ESHAPE, "span layout of %lld query groups x key steps exceeds %d tiles", (long long)tiles,
+                  dz::kMaxStepTiles);
+  }
   return attend_impl(c, q_raw, k_raw, v_raw, pos_thw, n, t, out, static_cast<cudaStream_t>(stream));
 }
 

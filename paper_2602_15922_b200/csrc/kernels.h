@@ -73,6 +73,10 @@ int attention_units(int32_t B, int32_t H, int32_t nq);
 constexpr int kTileQ = 256;  // skip / mask decision granularity: query rows of a CTA pair x the keys of a step
 // keys per K2 step: 128 with the fixed softmax base (ping-pong kernel), 256 with the online base
 int attention_step_keys(float m_static);
+// span layouts (several spans): the kernel's step-class table holds at most kMaxStepTiles
+// (256-row query group, key step) tiles when attention_has_step_table(D, m_static)
+constexpr int kMaxStepTiles = 65536;
+bool attention_has_step_table(int32_t D, float m_static);
 cudaError_t read_watchdog(uint32_t* host8);   // {fired, block, warp, bar addr, parity, smid, bars base, 0}
 cudaError_t reset_watchdog();
 cudaError_t trace_control(int enable, uint32_t* host, size_t n);  // K2 cycle trace (CTA 0, first unit)  // work units (b, h, q-tile pair)
