@@ -139,7 +139,11 @@ DZ_API dz_status dz_append_kv(dz_ctx* ctx, const void* k_raw, const void* v_raw,
  * K'/V are computed here (K1 prologue) and staged after the committed slots;
  * the committed cache is never modified.  chunk_id must exceed every committed
  * id (else DZ_ESTATE); n <= max_chunk_tokens (else DZ_ECAPACITY).
- * out: bf16 [batch][n_local][heads][head_dim]. */
+ * out: bf16 [batch][n_local][heads][head_dim].
+ * Capture-safe: no host synchronisation, every launch on `stream`, so the
+ * denoising steps of one chunk can be recorded once into a CUDA graph and
+ * replayed; a replay reads the committed state of the
+ * capture, so re-capture after dz_append_kv / dz_evict_front / dz_commit_staged. */
 DZ_API dz_status dz_attend_chunk(dz_ctx* ctx, const void* q_raw, const void* k_raw, const void* v_raw,
                           const dz_span* chunk, void* out, void* stream);
 
@@ -154,11 +158,14 @@ DZ_API dz_status dz_attend_chunk(dz_ctx* ctx, const void* q_raw, const void* k_r
  * every span id must exceed the last committed id (else DZ_ESTATE), visible to
  * every query.  Examples: the training layout [C0 .. C_{M-1}; Z1 .. Z_M] of
  * Fig. 10(a) with an empty cache; attend_chunk is the one-span case.
- * Key tiles of 256 keys whose (query group of 256 rows, key tile) pairs are
- * all invisible are skipped (never loaded, never multiplied); partially
- * visible tiles are masked per element.  1 <= n_spans <= 64; the total token
- * count must be <= max_chunk_tokens (else DZ_ECAPACITY) and a multiple of
- * world_size.  Nothing is staged for dz_commit_staged.
+ * Key steps (128 keys with the fixed softmax base, 256 with the online one)
+ * whose (query group of 256 rows, key step) pairs are all invisible are
+ * skipped (never loaded, never multiplied); partially visible ones are masked
+ * per element.  1 <= n_spans <= 64; the total token count must be <=
+ * max_chunk_tokens (else DZ_ECAPACITY) and a multiple of world_size; with
+ * several spans, ceil(n / 256) query groups x key steps over committed + new
+ * keys must not exceed 65536 (the kernel's tile-class table; else DZ_ESHAPE).
+ * Nothing is staged for dz_commit_staged.
  * out: bf16 [batch][n_local_total][heads][head_dim]. */
 DZ_API dz_status dz_attend_spans(dz_ctx* ctx, const void* q_raw, const void* k_raw, const void* v_raw,
                                  const int32_t* pos_thw, const dz_span* spans, int32_t n_spans, void* out,
