@@ -194,3 +194,20 @@ def test_spans_validation():
     with pytest.raises(dz.DzError, match="DZ_ESTATE"):      # nothing staged by attend_spans
         cache.attend_spans(q, q, q, pos, [(1, CLEAN, 128), (2, NOISY, 128)])
         cache.commit_staged(1)
+
+
+def test_spans_tile_table_limit():
+    # several spans: ceil(n/256) query groups x 128-key steps must fit the kernel's 65536-tile table
+    import paper_2602_15922_b200 as dz
+    w = synth.scaled(synth.workload("C0"), heads=1)
+    n = 2 * 40000                                   # 313 groups x 625 steps > 65536
+    cache, _, _ = _cache(w, 0, n, flags=0)
+    dev = torch.device("cuda")
+    q = torch.zeros(1, n, 1, w.head_dim, dtype=torch.bfloat16, device=dev)
+    pos = torch.zeros(n, 3, dtype=torch.int32, device=dev)
+    with pytest.raises(dz.DzError, match="DZ_ESHAPE"):
+        cache.attend_spans(q, q, q, pos, [(0, CLEAN, n // 2), (1, NOISY, n // 2)])
+    # one span of the same size has no table: it runs
+    out = cache.attend_spans(q, q, q, pos, [(1, NOISY, n)])
+    torch.cuda.synchronize()
+    assert out.shape == q.shape
