@@ -210,6 +210,13 @@ DZ_API dz_status dz_get_tile_map(const dz_ctx* ctx, uint8_t* host, size_t cap, i
  * recorded events (host sync).  Entries not yet recorded are 0. */
 DZ_API dz_status dz_profile_last(dz_ctx* ctx, float* ms6);
 
+/* Switches the DZ_FLAG_PROFILE event recording on (default) or off.  An event
+ * recorded between two kernels ends their programmatic overlap (each kernel
+ * is launched with programmatic stream serialization and may start while its
+ * predecessor drains), so throughput runs switch it off and measure the
+ * kernels in a separate profiled pass.  DZ_ESTATE without DZ_FLAG_PROFILE. */
+DZ_API dz_status dz_profile_enable(dz_ctx* ctx, int32_t on);
+
 /* Releases the context's host state and device workspace (not the caller's
  * buffers).  Safe on NULL. */
 DZ_API dz_status dz_destroy(dz_ctx* ctx);

@@ -95,6 +95,7 @@ SIGNATURES = [
     ("dz_debug_sp_unpack", I32, [P, P, I32, I32, I32, I32, I32, P]),
     ("dz_debug_watchdog", I32, [P, I32]),
     ("dz_profile_last", I32, [P, P]),
+    ("dz_profile_enable", I32, [P, I32]),
     ("dz_debug_trace", I32, [I32, P, SZ]),
 ]
 
@@ -338,6 +339,10 @@ class ChunkKVCache:
         self._check(lib().dz_profile_last(self._ctx, ctypes.cast(buf, P)), "dz_profile_last")
         keys = ("prologue", "exchange_pre", "attention", "exchange_post", "attend_total", "append")
         return dict(zip(keys, list(buf)))
+
+    def profile_enable(self, on: bool):
+        """Record per-kernel events (FLAG_PROFILE) or not (kernels then overlap programmatically)."""
+        self._check(lib().dz_profile_enable(self._ctx, 1 if on else 0), "dz_profile_enable")
 
     def attention_units(self, n_tokens: int) -> int:
         return int(lib().dz_attention_units(self._ctx, n_tokens))

@@ -346,6 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const __grid_constant__ SpanTable st) {
   using C = Cfg<D, PP>;
   constexpr int BN = C::kBN;  // keys per step (shadows the file-level 256)
+  ptx::pdl_launch_dependents();  // the next kernel may take SMs as our CTAs finish (it waits for us)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;           // SW128 tiles need 1024-byte alignment
@@ -434,6 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   ptx::cluster_sync();  // both CTAs' barriers initialised and TMEM allocated before any remote traffic
   ptx::tc_fence_after();
+  ptx::pdl_wait();      // the prologue's Q' / K' / V (and everything before it) are complete
   const uint32_t tmem = bars->tmem_base;
   const int32_t* gpre = bars->gpre;
 
@@ -985,10 +987,9 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
   auto k = attn_fwd_kernel<D, PP>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return e;
-  k<<<a.grid, kThreads, C::kSmem, s>>>(a.tm_q, a.tm_k, a.tm_v, a.tm_o, static_cast<__nv_bfloat16*>(a.out), a.o_bstride,
-                                       a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq, a.kv_len, a.m_static,
-                                       a.debug_flags, a.ws, a.ws_cnt, a.spans);
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(a.grid), dim3(kThreads), C::kSmem, s, a.tm_q, a.tm_k, a.tm_v, a.tm_o,
+                    static_cast<__nv_bfloat16*>(a.out), a.o_bstride, a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq,
+                    a.kv_len, a.m_static, a.debug_flags, a.ws, a.ws_cnt, a.spans);
 }
 
 }  // namespace

@@ -149,6 +149,7 @@ struct dz_ctx {
   // DZ_FLAG_PROFILE: events e[0..4] around the attend phases, a[0..1] around the append
   cudaEvent_t ev[5] = {}, ev_app[2] = {};
   bool have_attend_ev = false, have_append_ev = false;
+  bool prof_on = true;  // dz_profile_enable: events are recorded only while on
   std::string err;
 
   void* kslot(int b, int64_t slot) const {
@@ -471,7 +472,7 @@ dz_status dz_append_kv(dz_ctx* c, const void* k_raw, const void* v_raw, const dz
     return fail(c, DZ_ECAPACITY, "cache full: %lld + %d > %lld", (long long)c->valid, s->n_tokens,
                 (long long)c->cfg.cache_capacity_tokens);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool prof = c->ev_app[0] != nullptr;
+  const bool prof = c->ev_app[0] != nullptr && c->prof_on;
   if (prof) cudaEventRecord(c->ev_app[0], st);
   if ((r = run_prologue(c, nullptr, k_raw, v_raw, s->pos_thw, s->n_tokens, st))) return r;
   if (c->N > 1 && (r = exchange_pre(c, false, s->n_tokens, st))) return r;
@@ -494,7 +495,7 @@ dz_status attend_impl(dz_ctx* c, const void* q_raw, const void* k_raw, const voi
                       int64_t n, const dz::SpanTable& spans, void* out, cudaStream_t st) {
   dz_status r;
   c->staged = false;
-  const bool prof = c->ev[0] != nullptr;
+  const bool prof = c->ev[0] != nullptr && c->prof_on;
   auto mark = [&](int i) { if (prof) cudaEventRecord(c->ev[i], st); };
   mark(0);
   if ((r = run_prologue(c, q_raw, k_raw, v_raw, pos, n, st))) return r;
@@ -660,6 +661,14 @@ dz_status dz_get_tile_map(const dz_ctx* c, uint8_t* host, size_t cap, int32_t* n
   if (cap < need) return DZ_EINVAL;
   // synchronous device read of the kernel-written debug map (tests only)
   if (cudaMemcpy(host, c->base + c->L.map_off, need, cudaMemcpyDeviceToHost) != cudaSuccess) return DZ_ECUDA;
+  return DZ_OK;
+}
+
+dz_status dz_profile_enable(dz_ctx* c, int32_t on) {
+  if (!c) return DZ_EINVAL;
+  if (!c->ev[0]) return fail(c, DZ_ESTATE, "created without DZ_FLAG_PROFILE");
+  c->prof_on = on != 0;
+  if (!c->prof_on) c->have_attend_ev = c->have_append_ev = false;
   return DZ_OK;
 }
 

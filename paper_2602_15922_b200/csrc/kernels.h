@@ -10,6 +10,24 @@ namespace dz {
 
 constexpr int kMaxHeadDim = 128;
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while the previous
+// kernel of the stream drains; it calls griddepcontrol.wait before touching global memory.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---- K1 / K4: fused per-head RMSNorm + 3D RoPE (+ V copy) -----------------
 // One output tensor slot.  Address of output row (b, t, h):
 //   base + b*bstride + (h / heads_per_dest)*dstride + t*tstride + (h % heads_per_dest)*D

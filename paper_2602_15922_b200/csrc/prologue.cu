@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
   constexpr int G = D / 8;               // threads per row (one 16-byte vector each)
   constexpr int kGroups = kThreads / G;  // rows processed side by side
   constexpr int kPer = 3;                // heads per thread in one pass (H <= 48 at D = 128: one pass)
+  ptx::pdl_launch_dependents();  // the next kernel may take SMs as our CTAs finish (it waits for us)
   extern __shared__ __align__(128) uint8_t sm[];
   const int H = a.H, tid = threadIdx.x;
   const int g = tid / G, li = tid % G;
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
     cs[(k % L.S) * (D / 2) + ai] = make_float2((float)cn, (float)sn);
   };
   __syncthreads();  // barriers initialised, row offsets visible
+  ptx::pdl_wait();  // the previous kernel of the stream (e.g. the last attention reading the staging slot) is done
   if (tid == 0)
     for (int k = 0; k < L.S - 1; ++k) issue(k);
   // gains of this thread's heads (h = g + kGroups * i) and column slice, kept in registers
@@ -250,8 +252,7 @@ cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
   }
   const int items = a.B * a.n;
   const int grid = items < kCtasPerSm * sms ? items : kCtasPerSm * sms;
-  k<<<grid, kThreads, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(grid), dim3(kThreads), (size_t)smem, s, a);
 }
 
 cudaError_t launch_prologue(const PrologueArgs& a, cudaStream_t s) {

@@ -156,6 +156,12 @@ __device__ __forceinline__ void tma_load_4d_2cta(uint32_t dst, const void* tmap,
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cluster), "l"(policy)
       : "memory");
 }
+// Programmatic dependent launch: let the next kernel of the stream be scheduled now (its CTAs take
+// SMs as ours leave) / wait until the previous kernel of the stream has completed and its memory
+// is visible.  Every kernel of the library waits before its first global access, so ordering
+// stays transitive along the stream.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // TMA tensor store shared -> global (bulk async-group completion).
 __device__ __forceinline__ void tma_store_4d(const void* tmap, uint32_t src, int32_t c0, int32_t c1, int32_t c2,
                                              int32_t c3) {
