@@ -462,7 +462,10 @@ def main():
         if d.get("workload") == w.name:
             traffic = d.get("dram_bytes_per_launch")
     n_new = n_tf if args.mode == "tf" else n_loc
-    pro_bytes = 2 * 3 * w.batch * n_new * H * D * 2     # read q,k,v + write q',k',v (bf16/fp16)
+    # attend prologue: read q, k (+ v) and write q', k' (+ the V staging copy); with one GPU and the
+    # new keys starting at a 128-key step the attention reads V in place (dz.h), no V copy
+    v_in_place = N == 1 and (0 if args.mode == "tf" else w.cache_tokens) % 128 == 0
+    pro_bytes = 2 * (2 if v_in_place else 3) * w.batch * n_new * H * D * 2
     app_bytes = 2 * 2 * w.batch * n_loc * H * D * 2     # read k,v + write k',v
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": N, "steps": args.steps,

@@ -331,7 +331,7 @@ dz_status exchange_post(dz_ctx* c, int64_t n, cudaStream_t st) { return run_exch
 
 // K2 over local heads and the full sequence: committed slots + the staged chunk.
 dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* out_local, int64_t o_bstride,
-                        int64_t o_tstride, cudaStream_t st) {
+                        int64_t o_tstride, const void* v_new, cudaStream_t st) {
   dz::AttnArgs a;
   a.spans = spans;
   a.spans.valid = (int32_t)c->valid;
@@ -348,6 +348,13 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   if (o_tstride != (int64_t)c->Hl * c->D ||
       !make_tmap(&a.tm_o, out_local, true, c->D, c->Hl, n, c->B, o_bstride, (uint32_t)c->D / 2, 32))
     return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (O) failed");
+  if (v_new != nullptr) {  // the new tokens' V straight from the caller's [B][n][H][D] input
+    const int step_keys = dz::attention_step_keys(c->m_static);
+    if (!make_tmap(&a.tm_v2, v_new, true, c->D, c->Hl, n, c->B, n * c->Hl * c->D, (uint32_t)c->D / 2,
+                   (uint32_t)step_keys))
+      return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (V in place) failed");
+    a.v2_step = (int32_t)(c->valid / step_keys);
+  }
   a.out = out_local;
   a.o_bstride = o_bstride;
   a.o_tstride = o_tstride;
@@ -492,22 +499,29 @@ namespace {
 // One attention call (K1 prologue [+ exchange] + K2 [+ exchange + unpack]) over
 // n new tokens described by `spans`; keys = committed chunks + the new tokens.
 dz_status attend_impl(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const int32_t* pos,
-                      int64_t n, const dz::SpanTable& spans, void* out, cudaStream_t st) {
+                      int64_t n, const dz::SpanTable& spans, void* out, bool may_commit, cudaStream_t st) {
   dz_status r;
   c->staged = false;
+  // V of the new tokens is only copied into the staging slot when the chunk may be committed
+  // (attend_chunk of a CLEAN chunk) or the exchange needs it (SP) or the new keys do not start at
+  // a key step; otherwise the attention reads it in place from the caller's input.
+  const bool v_in_place = c->N == 1 && !may_commit && c->valid % dz::attention_step_keys(c->m_static) == 0;
   const bool prof = c->ev[0] != nullptr && c->prof_on;
   auto mark = [&](int i) { if (prof) cudaEventRecord(c->ev[i], st); };
   mark(0);
-  if ((r = run_prologue(c, q_raw, k_raw, v_raw, pos, n, st))) return r;
+  if ((r = run_prologue(c, q_raw, k_raw, v_in_place ? nullptr : v_raw, pos, n, st))) return r;
   mark(1);
   if (c->N == 1) {
     mark(2);
-    if ((r = run_attention(c, n, spans, out, n * c->H * c->D, (int64_t)c->H * c->D, st))) return r;
+    if ((r = run_attention(c, n, spans, out, n * c->H * c->D, (int64_t)c->H * c->D, v_in_place ? v_raw : nullptr,
+                           st)))
+      return r;
     mark(3);
   } else {
     if ((r = exchange_pre(c, true, n, st))) return r;
     mark(2);
-    if ((r = run_attention(c, n, spans, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, st)))
+    if ((r = run_attention(c, n, spans, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, nullptr,
+                           st)))
       return r;
     mark(3);
     if ((r = exchange_post(c, n, st))) return r;
@@ -549,7 +563,8 @@ dz_status dz_attend_chunk(dz_ctx* c, const void* q_raw, const void* k_raw, const
   dz::SpanTable t;
   t.n = 1;
   set_span(t, 0, s->chunk_id, s->kind, 0, s->n_tokens);
-  if ((r = attend_impl(c, q_raw, k_raw, v_raw, s->pos_thw, s->n_tokens, t, out, static_cast<cudaStream_t>(stream))))
+  if ((r = attend_impl(c, q_raw, k_raw, v_raw, s->pos_thw, s->n_tokens, t, out, s->kind == DZ_CLEAN,
+                       static_cast<cudaStream_t>(stream))))
     return r;
   c->staged = true;
   c->staged_id = s->chunk_id;
@@ -589,7 +604,7 @@ dz_status dz_attend_spans(dz_ctx* c, const void* q_raw, const void* k_raw, const
       return fail(c, DZ_ESHAPE, "span layout of %lld query groups x key steps exceeds %d tiles", (long long)tiles,
                   dz::kMaxStepTiles);
   }
-  return attend_impl(c, q_raw, k_raw, v_raw, pos_thw, n, t, out, static_cast<cudaStream_t>(stream));
+  return attend_impl(c, q_raw, k_raw, v_raw, pos_thw, n, t, out, false, static_cast<cudaStream_t>(stream));
 }
 
 dz_status dz_commit_staged(dz_ctx* c, int32_t chunk_id, void* stream) {

@@ -20,7 +20,16 @@ def _small(name="C1", **kw):
 # ---------------------------------------------------------------- append --
 @pytest.mark.parametrize("wname", ["C0", "C1"])
 def test_append_parity(wname):
-    w = synth.workload(wname)
+    _append_parity(synth.workload(wname))
+
+
+def test_append_parity_many_heads_ring_prologue():
+    # 56 heads at D = 128 exceed one pass of the one-token-per-CTA prologue (48 heads): the
+    # persistent TMA-ring prologue runs instead; same checks
+    _append_parity(synth.scaled(synth.workload("C1"), heads=56, cached_chunks=2))
+
+
+def _append_parity(w):
     run = GpuRun(w)
     run.fill()
     torch.cuda.synchronize()
