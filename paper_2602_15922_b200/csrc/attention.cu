@@ -59,9 +59,11 @@ constexpr int BN = 256;           // keys per KV step
 constexpr int kThreads = 384;     // 12 warps
 constexpr float kRescaleLog2 = 8.0f;
 #ifndef DZ_POLY
-#define DZ_POLY 2
+#define DZ_POLY 1
 #endif
-constexpr int kPolyPairs = DZ_POLY;  // of every 8 exp2 pairs, this many go to the FMA-pipe polynomial (measured on the ping-pong kernel: 0/2/3/4 -> 234/205/212/218 us)
+// of every 8 exp2 pairs, this many go to the FMA-pipe polynomial (measured on the current ping-pong
+// kernel at C1: 0/1/2/3 of 8 -> 179.5/174.3/176.1/179.1 us)
+constexpr int kPolyPairs = DZ_POLY;
 constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr int kWarpMma = 11, kWarpTma = 10, kWarpPv = 9, kWarpTmem = 8;
 // setmaxnreg split, 128 * light + 256 * softmax = 384 * 168 (launch): ping-pong 104/200 (measured on
