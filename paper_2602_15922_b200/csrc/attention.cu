@@ -1,48 +1,40 @@
 // attention.cu -- K2: block-causal chunk attention on tcgen05 tensor cores, CTA pairs.
 //
-// Computes, for every (b, h, query s) of the current chunk,
+// Computes, for every (b, h, query s) of the new tokens,
 //     O_s = sum_j softmax_j(<q'_s, k'_j> * scale) v_j
-// over the visible keys j = the committed clean chunks plus the current chunk
-// (Fig. 10 / l.505; Alg. 2 l.584-585; BJ:5).  For attend_chunk every
-// committed key and every own-chunk key is visible, so the only masked pairs
-// are out-of-bounds columns of the last KV tile.
+// over the visible keys j: the committed clean chunks plus the new tokens under the
+// Fig. 10 rule (Alg. 2 l.584-585; BJ:5).  For attend_chunk every
+// committed key and every own-chunk key is visible, so the only masked pairs are the
+// out-of-bounds columns of the last key step.
 //
-// Work unit: a cluster of two CTAs (one SM each, same TPC) owns (batch, head,
-// two consecutive 128-row query tiles); CTA r keeps q-tile 2g + r in shared
-// memory.  Per KV step of 256 keys the leader CTA issues two cta_group::2
-// tcgen05.mma groups (M = 256 rows: 128 per CTA):
-//   S = Q K_j^T      SS, f16 x f16 -> f32, N = 256 keys; each CTA supplies its
-//                    128 query rows and 128 of the step's keys
-//   O += P V_j       TS, P bf16 from TMEM, K = 256 keys, N = D; each CTA
-//                    supplies D/2 of V's columns
-// so each byte of K and V in shared memory is read by one SM, and the shared
-// memory traffic per SM stays under 100 B/clk (the port is 128 B/clk; a 1-CTA
-// M=128 N=128 SS MMA alone saturates it).
+// Work unit: a cluster of two CTAs (one SM each, same TPC) owns (batch, head, query
+// group of 256 rows); CTA r keeps q-tile 2g + r in shared memory.  Every MMA is
+// tcgen05.mma.cta_group::2 (M = 256: 128 rows per CTA), issued by one thread of the
+// leader CTA, fp32 accumulators in TMEM:
+//   S = Q K_j^T   SS, f16 x f16 -> f32; each CTA supplies its 128 query rows and half
+//                 of the step's keys
+//   O += P V_j    TS, P bf16 from TMEM; each CTA supplies D/2 of V's columns
+// so each byte of K and V in shared memory is read by one SM.
 //
-// TMEM per CTA (512 columns): S [0,256) fp32, P [256,384) bf16 pairs, O
-// [384,512).  The pipeline (issue order QK(j) PV(j-1) QK(j+1) PV(j) ...):
-//   * S is released ("S free") as soon as the softmax has copied it into
-//     registers, so QK(j+1) is gated only by that copy, never by the softmax's
-//     exponentials;
-//   * P has its own buffer, so PV(j) runs behind QK(j+1) and overlaps the
-//     softmax of step j+1.
-// Each handshake (commit -> mbarrier -> wake, ~400 clk on this part, measured
-// with tools/handoff_bench.cu) is paid once per 1024 clk of QK work; with
-// 128-key steps and two query tiles per CTA the same handshakes cost ~35% of
-// the tensor pipe (measured: 2750 clk per 2048 clk of MMA work).
+// Two variants:
+//   * ping-pong (fixed softmax base, the production path): 128-key steps; TMEM per CTA
+//     S[2] [0,256) fp32, P[2] [256,384) bf16 pairs, O [384,512).  The two softmax warp
+//     groups take alternate steps; S is released as soon as it is in registers, P has
+//     its own double buffer, so the tensor pipe holds the next QK and the previous PV.
+//   * lock-step (online base): 256-key steps split in two 128-key halves between the
+//     groups, which exchange row maxima and rescale O lazily.
 //
-// Warps per CTA (12; schedulers favour high warp ids, so the single-thread
-// roles sit on top):
+// Warps per CTA (12):
 //   11     QK issuer (leader CTA)
+//   10     K (+Q) TMA producer (both CTAs; bytes counted on the leader's barriers)
 //   9      PV issuer (leader CTA)
-//   10     TMA producer (both CTAs; bytes counted on the leader's barriers)
-//   8      TMEM allocator (cta_group::2)
-//   0..7   softmax + epilogue: warp w owns TMEM lanes 32*(w%4).. (query rows)
-//          and S columns 128*(w/4)..+128 (keys), O columns (w/4)*D/2..+D/2.
-//          Fixed softmax base from the QK-norm bound (or a running max with
-//          lazy rescaling, exchanged between the two warps of a row, when the
-//          bound is large); exp2 on MUFU with 3 of every 8 pairs on an
-//          FMA-pipe polynomial.
+//   8      TMEM allocator, then V TMA producer
+//   0..7   softmax + epilogue: warp w owns TMEM lanes 32*(w%4).. (query rows); ping-pong:
+//          every other step (group w/4), lock-step: key half w/4; O columns (w/4)*D/2..
+//          exp2 on MUFU.EX2 with 1 of every 8 pairs on an FMA-pipe polynomial.
+// Schedule: stream-K over executed steps (one span: the first units dealt whole,
+// round-robin), pieces of split units combined in key order by the last to finish.
+// Epilogue: O through swizzled shared memory and one TMA tensor store per warp.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
