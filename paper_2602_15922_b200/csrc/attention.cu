@@ -125,7 +125,7 @@ struct Cfg {
   static constexpr int kOOff = kRedOff + 2 * BM * 4;              // epilogue O staging: 8 warps x 32 rows x D/2 bf16
   static constexpr bool kTab = PP || D == 64;                     // static step-class table fits beside
   static constexpr int kBarOff = kOOff + 8 * 32 * D;
-  static constexpr int kSmem = kBarOff + 576 + 1024;              // + barriers/schedule + alignment slack
+  static constexpr int kSmem = kBarOff + 1024 + 1024;             // + barriers/schedule + alignment slack
   static_assert(kSmem + (kTab ? kClsWords * 4 : 0) <= 232448, "shared memory per CTA");
   static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, 2 * BM, BN / 2);  // f16 x f16, K-major, per half
   static constexpr uint32_t kIdescPV = ptx::idesc_f16(1, 1, 0, 1, 2 * BM, D);   // P (TMEM) x V (MN-major)
@@ -140,8 +140,9 @@ struct Bars {
   uint32_t tmem_base;
   int32_t last_piece;               // combine election result (softmax warps)
   int32_t gpre[kMaxGroups + 1];     // prefix sums of executed steps per query group
+  int32_t plo[kMaxPairs + 1];       // stream-K range boundaries of the CTA pairs (executed-step index)
 };
-static_assert(sizeof(Bars) <= 576, "Bars must fit its shared-memory slot");
+static_assert(sizeof(Bars) <= 1024, "Bars must fit its shared-memory slot");
 
 // p = 2^(x + nb) for 32 pairs of scores (already in log2 units); row-sum
 // partials in acc, bf16 pairs in pk.
@@ -262,13 +263,14 @@ struct Sched {
   int lo, hi, wbh, W;  // stream-K: this pair's range, steps per (b, h), total steps (host keeps W * P < 2^31)
   int P;               // pairs
   int u;               // round-robin: next unit
-  int rr_end;          // hybrid (one span): units [0, rr_end) are dealt whole, unit u to pair u % P
+  int rr_end;          // hybrid: units [0, rr_end) are dealt whole, unit u to pair u % P
   int x0;              // ... and stream-K covers the executed steps [x0, W) of the remaining units
+  const int32_t* plo;  // range boundaries [P + 1] (shared memory)
 };
-// stream-K range boundary of pair p (ranges split [x0, W) evenly)
-__device__ __forceinline__ int pair_lo(const Sched& sc, int p) { return sc.x0 + (sc.W - sc.x0) * p / sc.P; }
+// stream-K range boundary of pair p
+__device__ __forceinline__ int pair_lo(const Sched& sc, int p) { return sc.plo[p]; }
 __device__ __forceinline__ int pair_of(const Sched& sc, int x) {
-  int p = (int)((int64_t)(x - sc.x0) * sc.P / (sc.W - sc.x0));
+  int p = sc.W > sc.x0 ? (int)((int64_t)(x - sc.x0) * sc.P / (sc.W - sc.x0)) : 0;  // a guess; the walks fix it
   while (p + 1 < sc.P && pair_lo(sc, p + 1) <= x) ++p;
   while (p > 0 && pair_lo(sc, p) > x) --p;
   return p;
@@ -285,7 +287,7 @@ __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_g
       sg.h = bh % H;
       sg.b = bh / H;
       sg.k0 = 0;
-      sg.k1 = sg.cnt = nkv;
+      sg.k1 = sg.cnt = gpre[sg.g + 1] - gpre[sg.g];  // the group's executed steps
       return true;
     }
     if (sc.lo >= sc.hi) return false;
@@ -434,24 +436,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::pdl_wait();      // the prologue's Q' / K' / V (and everything before it) are complete
   const uint32_t tmem = bars->tmem_base;
   const int32_t* gpre = bars->gpre;
+  // Hybrid schedule: all but the last ~1.x waves of units are dealt whole, round-robin (unit u
+  // to pair u mod P), so the query groups of a head run side by side and its K/V is read from
+  // HBM about once; stream-K splits the executed steps of the remaining units so that every
+  // pair's total (its whole units + its range) matches W / P as closely as the unit lengths
+  // allow.  (Pure stream-K spreads each head's groups over the whole launch, and the K/V of
+  // every head must then stay in L2 from start to end.)
+  int rr_end = 0, x0 = 0;
+  if (streamk) {
+    const int wbh = gpre[n_groups], W = B * H * wbh;
+    if (n_units >= 2 * ncl) {
+      rr_end = (n_units / ncl - 1) * ncl;
+      x0 = (rr_end / n_groups) * wbh + gpre[rr_end % n_groups];  // executed steps of units [0, rr_end)
+    }
+    int32_t* plo = bars->plo;
+    // linear index of the first executed step of unit u
+    auto lin = [&](int u) { return (u / n_groups) * wbh + gpre[u % n_groups]; };
+    for (int p = threadIdx.x; p < ncl; p += kThreads) {
+      // whole-unit steps of pairs 0..p: units w*P .. w*P + p of every round-robin wave w
+      int rr = 0;
+      for (int w0 = 0; w0 < rr_end; w0 += ncl) rr += lin(w0 + p + 1) - lin(w0);
+      // pairs 0..p end where their whole-unit steps plus their ranges reach W (p + 1) / P
+      plo[p + 1] = p + 1 == ncl ? W : min(W, max(x0, x0 + W * (p + 1) / ncl - rr));  // (host: W * P < 2^31)
+    }
+    if (threadIdx.x == 0) plo[0] = x0;
+    __syncthreads();
+    if (threadIdx.x == 0)  // keep the boundaries non-decreasing (uneven unit lengths)
+      for (int p = 1; p <= ncl; ++p) plo[p] = max(plo[p], plo[p - 1]);
+    __syncthreads();
+  }
 
   Sched sched0;
   sched0.streamk = streamk;
   sched0.P = ncl;
   sched0.u = cid;
-  sched0.rr_end = 0;
-  sched0.x0 = 0;
+  sched0.rr_end = rr_end;
+  sched0.x0 = x0;
+  sched0.plo = bars->plo;
   if (streamk) {
     sched0.wbh = gpre[n_groups];
     sched0.W = B * H * sched0.wbh;
-    // One span (uniform units): all but the last ~1.x waves of units are dealt whole, round-robin,
-    // so the query groups of a head run side by side and its K/V is read from HBM about once;
-    // stream-K balances the rest.  (Pure stream-K would spread each head's groups over the
-    // whole launch, and the K/V of every head would have to stay in L2 from start to end.)
-    if (st.n == 1 && n_units >= 2 * ncl) {
-      sched0.rr_end = (n_units / ncl - 1) * ncl;
-      sched0.x0 = sched0.rr_end * nkv;
-    }
     sched0.lo = pair_lo(sched0, cid);
     sched0.hi = pair_lo(sched0, cid + 1);
   }

@@ -211,3 +211,21 @@ def test_spans_tile_table_limit():
     out = cache.attend_spans(q, q, q, pos, [(1, NOISY, n)])
     torch.cuda.synchronize()
     assert out.shape == q.shape
+
+
+def test_teacher_forcing_wan_shape_all_heads_hybrid_schedule():
+    # all 40 heads: 1680 units, so the hybrid schedule deals whole units of unequal executed
+    # length round-robin and stream-K splits the rest; heads 0 and 39 against the oracle
+    w = synth.workload("C1")
+    spans = synth.teacher_forcing_spans(4, w.chunk_tokens)
+    q, k, v, pos = synth.span_inputs(w, spans)
+    n = q.shape[0]
+    cache, gq, gk = _cache(w, 0, n, flags=0)
+    out = _run(cache, spans, q, k, v, pos)
+    again = _run(cache, spans, q, k, v, pos)
+    assert torch.equal(out, again), "the schedule must be deterministic"
+    for h in (0, 39):
+        sl = lambda x: x[:, h:h + 1].contiguous()
+        w1 = synth.scaled(w, heads=1)
+        want, _, _ = _oracle_spans(w1, gq[h:h + 1], gk[h:h + 1], spans, sl(q), sl(k), sl(v), pos)
+        assert_parity(out[:, h:h + 1].cpu().double().numpy(), want, f"teacher forcing 40 heads, head {h}")
