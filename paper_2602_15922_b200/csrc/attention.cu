@@ -109,8 +109,8 @@ struct Cfg {
   static constexpr int kQTileBytes = BM * D * 2;          // one CTA's query tile (fp16)
   static constexpr int kStageBytes = kBN * D;             // K (kBN/2 keys x D) or V (kBN keys x D/2) per CTA
 #ifndef DZ_KST
-#define DZ_KST 5   // measured on C1 (K/V stages): 7/5 192.7 us, 6/4 190.3, 5/4 191.0, 5/3 190.0
-#endif
+#define DZ_KST 4   // measured on C1 (K/V stages), first kernel: 7/5 192.7 us, 6/4 190.3, 5/4 191.0, 5/3 190.0;
+#endif               // current kernel: 6/3 176.5, 5/4 177.5, 5/3 175.4, 4/3 174.2, 4/2 176.8, 3/3 174.8, 3/2 176.9
 #ifndef DZ_VST
 #define DZ_VST 3
 #endif
