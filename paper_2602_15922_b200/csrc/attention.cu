@@ -51,10 +51,10 @@ constexpr int BN = 256;           // keys per KV step
 constexpr int kThreads = 384;     // 12 warps
 constexpr float kRescaleLog2 = 8.0f;
 #ifndef DZ_POLY
-#define DZ_POLY 1
+#define DZ_POLY 2
 #endif
-// of every 8 exp2 pairs, this many go to the FMA-pipe polynomial (measured on the current ping-pong
-// kernel at C1: 0/1/2/3 of 8 -> 179.5/174.3/176.1/179.1 us)
+// of every 16 exp2 pairs, this many go to the FMA-pipe polynomial (measured on the current ping-pong
+// kernel at C1: 0/1/2/3/4/6 of 16 -> 179.5/174.1/174.1/175.5/176.1/179.1 us)
 constexpr int kPolyPairs = DZ_POLY;
 constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr int kWarpMma = 11, kWarpTma = 10, kWarpPv = 9, kWarpTmem = 8;
@@ -147,7 +147,7 @@ static_assert(sizeof(Bars) <= 1024, "Bars must fit its shared-memory slot");
 // p = 2^(x + nb) for 32 pairs of scores (already in log2 units); row-sum
 // partials in acc, bf16 pairs in pk.
 //   kMixed (fixed base, unmasked step: every x in [-40, 40], nb = 0): kPolyPairs
-//     of every 8 pairs through the FMA-pipe polynomial, the rest through MUFU.EX2;
+//     of every 16 pairs through the FMA-pipe polynomial, the rest through MUFU.EX2;
 //   !kMixed (online base or masked step: x may be -inf): every pair through
 //     MUFU.EX2 after adding nb (ex2(-inf) = +0 exactly, so masked keys add 0).
 // Two variants only, to keep the softmax loop inside the instruction cache.
@@ -157,7 +157,7 @@ __device__ __forceinline__ void exp_half(const float* s, uint64_t nb2, uint32_t 
   for (int i = 0; i < 32; ++i) {
     uint64_t x = ptx::f2_pack(s[2 * i], s[2 * i + 1]);
     uint64_t p;
-    if (kMixed && (i % 8) >= 8 - kPolyPairs) {
+    if (kMixed && (i % 16) >= 16 - kPolyPairs) {
       p = ptx::f2_exp2_poly<false>(x);
     } else {
       if (!kMixed) x = ptx::f2_add(x, nb2);
