@@ -64,6 +64,7 @@ def parse():
                     "(default: the workload's, C3 = 4)")
     ap.add_argument("--graph", action="store_true", help="denoise mode: replay the steps as one CUDA graph")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events in the library (diagnostics)")
+    ap.add_argument("--online", action="store_true", help="force the online-softmax (running max) kernel")
     ap.add_argument("--flush-read", action="store_true",
                     help="after the 512 MB flush write, read 256 MB of it so no dirty flush lines stay in L2")
     return ap.parse_args()
@@ -267,7 +268,9 @@ def main():
     slack = 16 * n
     cache = dz.ChunkKVCache(w.batch, H, D, w.cache_tokens, n, w.rope_dims, gq.to(dev), gk.to(dev),
                             rope_theta=w.rope_theta, rms_eps=w.rms_eps, window_slack=slack, world_size=N,
-                            rank=rank, nccl_comm=comm, flags=0 if args.no_profile else dz.FLAG_PROFILE, device=dev)
+                            rank=rank, nccl_comm=comm,
+                            flags=(0 if args.no_profile else dz.FLAG_PROFILE) | (dz.FLAG_ONLINE_SOFTMAX if args.online else 0),
+                            device=dev)
     sl = slice(rank * n_loc, (rank + 1) * n_loc)
 
     def dev_chunk(x):   # [B][n][H][D] bf16 -> this rank's tokens on the device
