@@ -120,7 +120,7 @@ DZ_API size_t dz_cache_bytes(const dz_config* cfg);
  * caller's cache_storage (dz_cache_bytes counts it); the context allocates no
  * device memory.  Also derives the QK-norm logit bound
  *   |<q',k'>| * scale * log2(e) <= head_dim * max_abs_gain^2 * scale * log2(e)
- * (RMSNorm makes ||x'|| <= sqrt(head_dim) * max|g|); when it is <= 40 the
+ * (RMSNorm makes ||x'|| <= sqrt(head_dim) * max|g|); when it is <= 60 the
  * attention uses it as a fixed softmax base instead of a running row max
  * (DZ_FLAG_ONLINE_SOFTMAX disables this).  *out is owned by the caller until
  * dz_destroy. */

@@ -146,7 +146,7 @@ static_assert(sizeof(Bars) <= 1024, "Bars must fit its shared-memory slot");
 
 // p = 2^(x + nb) for 32 pairs of scores (already in log2 units); row-sum
 // partials in acc, bf16 pairs in pk.
-//   kMixed (fixed base, unmasked step: every x in [-40, 40], nb = 0): kPolyPairs
+//   kMixed (fixed base, unmasked step: every x in [-60, 60], nb = 0): kPolyPairs
 //     of every 16 pairs through the FMA-pipe polynomial, the rest through MUFU.EX2;
 //   !kMixed (online base or masked step: x may be -inf): every pair through
 //     MUFU.EX2 after adding nb (ex2(-inf) = +0 exactly, so masked keys add 0).
@@ -789,7 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (grow) m_used = mx;
         }
         // Scores are in log2 units (Q' was pre-scaled by scale*log2e).  Fixed base (QK-norm
-        // bound, m_static <= 40): p = 2^s directly, every p in [2^-40, 2^40], so neither an
+        // bound, m_static <= 60): p = 2^s directly, every p in [2^-60, 2^60], so neither an
         // offset nor a clamp is needed; online base: p = 2^(s - m).
         const float nbase = (!online || m_used == -INFINITY) ? 0.f : -m_used;
         const uint64_t nb2 = ptx::f2_pack(nbase, nbase);

@@ -457,7 +457,7 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   {
     const double bound = (double)cfg->head_dim * cfg->max_abs_gain * cfg->max_abs_gain * c->scale *
                          1.4426950408889634 * 1.005;
-    c->m_static = (!(cfg->flags & DZ_FLAG_ONLINE_SOFTMAX) && bound <= 40.0) ? (float)std::max(bound, 1.0) : 0.f;  // > 0 selects the fixed base
+    c->m_static = (!(cfg->flags & DZ_FLAG_ONLINE_SOFTMAX) && bound <= 60.0) ? (float)std::max(bound, 1.0) : 0.f;  // > 0 selects the fixed base
   }
   if (cfg->flags & DZ_FLAG_PROFILE) {
     for (auto& e : c->ev)

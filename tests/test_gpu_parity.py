@@ -220,6 +220,25 @@ def test_online_softmax_path_c1():
         assert_parity(out[:, h:h + 1], run.oracle_out(heads=(h, h + 1)), f"online C1 head {h}")
 
 
+def test_fixed_base_near_its_limit():
+    # gains x1.25 (max|g| ~ 1.87): QK-norm bound ~57.7 log2 units, still the fixed softmax base
+    # (p = 2^s in [2^-58, 2^58]); must meet the BASELINE tolerance like the online path
+    w = synth.scaled(synth.workload("C1"), heads=4, cached_chunks=2)
+    run = GpuRun(w)
+    run.gq, run.gk = run.gq * 1.25, run.gk * 1.25
+    import paper_2602_15922_b200 as dz
+    run.cache = dz.ChunkKVCache(w.batch, w.heads, w.head_dim, w.cache_tokens, w.chunk_tokens, w.rope_dims,
+                                run.gq.to(run.dev), run.gk.to(run.dev), flags=8, device=run.dev)  # tile map
+    run.fill()
+    out = run.attend().cpu().double().numpy()[0]
+    _, bm, bn = run.cache.tile_map(with_tiles=True)
+    assert bn == 128, "expected the fixed-base (ping-pong, 128-key step) kernel"
+    max_abs, rel_fro = errors(out, run.oracle_out())
+    scale = max(1.0, float(np.abs(run.oracle_out()).max()))
+    assert np.isfinite(out).all()
+    assert rel_fro <= 5e-3 and max_abs <= 2e-2 * scale, (max_abs, rel_fro, scale)
+
+
 def test_large_gains_stress_online_path():
     # gains x3 (scores up to ~50, reading A19's stress case): the QK-norm bound exceeds
     # the fixed-base limit, so the kernel tracks the running max and rescales
