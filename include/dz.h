@@ -136,11 +136,12 @@ DZ_API dz_status dz_append_kv(dz_ctx* ctx, const void* k_raw, const void* v_raw,
 /* One denoising step of the current chunk (Alg. 2 l.584-585, update=False):
  * out = softmax(Q' K'^T * scale) V over keys = committed chunks (all have id <
  * chunk_id) plus the chunk itself (bidirectional, Fig. 10).  Q' and the chunk's
- * K' are computed here (K1 prologue) and staged after the committed slots, with
- * V; for a NOISY chunk on one GPU whose keys start at a key step (valid a
- * multiple of 128 with the fixed softmax base, 256 otherwise) V is not copied:
- * the attention reads it in place from v_raw.  The committed cache is never
- * modified.  chunk_id must exceed every committed
+ * K' are computed here (K1 prologue).  A CLEAN chunk (which dz_commit_staged may
+ * commit), SP, or new keys not starting at a key step (valid not a multiple of
+ * 128 with the fixed softmax base, 256 otherwise): K' and V are staged after the
+ * committed slots.  Otherwise (a NOISY chunk on one GPU) K' goes to a
+ * current-chunk buffer, V is read in place from v_raw, and the call only reads
+ * the cache.  The committed cache is never modified.  chunk_id must exceed every committed
  * id (else DZ_ESTATE); n <= max_chunk_tokens (else DZ_ECAPACITY).
  * out: bf16 [batch][n_local][heads][head_dim].
  * Capture-safe: no host synchronisation, every launch on `stream`, so the

@@ -335,8 +335,8 @@ __device__ __forceinline__ int step_of(const SpanTable& st, int g, int k, int nq
 template <int D, bool PP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_v2,
-                    const __grid_constant__ CUtensorMap tm_o, int v2_step,
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_k2,
+                    const __grid_constant__ CUtensorMap tm_v2, const __grid_constant__ CUtensorMap tm_o, int cur_step,
                     __nv_bfloat16* __restrict__ out, int64_t o_bstride,
                     int64_t o_tstride, float* __restrict__ lse, uint8_t* __restrict__ tile_map, int B, int H,
                     int nq, int kv_len, float m_static, int dbg, float* __restrict__ ws, int* __restrict__ ws_cnt,
@@ -426,7 +426,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
-    if (v2_step != 0x7fffffff) ptx::tma_prefetch_desc(&tm_v2);
+    if (cur_step != 0x7fffffff) {
+      ptx::tma_prefetch_desc(&tm_k2);
+      ptx::tma_prefetch_desc(&tm_v2);
+    }
   }
   if (warp == kWarpTmem) ptx::tmem_alloc_2cta<512>(ptx::smem_u32(&bars->tmem_base));
   if (blockIdx.x == 0 && threadIdx.x == 0) ptx::g_dz_watchdog[6] = ptx::smem_u32(bars);
@@ -525,13 +528,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (do_k) {
             // S half hh (keys 128hh..128hh+127 of the step) takes 64 keys from each CTA:
             // this CTA loads keys 128hh + 64*rank .. +63 into [hh][dim box] of 64 x 128 B
+            // the new tokens' K' (j >= cur_step) come from the current-chunk buffer
+            const bool cur = j >= cur_step;
+            const CUtensorMap* tk = cur ? &tm_k2 : &tm_k;
+            const int row0 = (cur ? j - cur_step : j) * BN + 64 * (int)rank;
             for (int hh = 0; hh < BN / 128; ++hh)
               for (int x = 0; x < C::kQBoxes; ++x)
-                ptx::tma_load_4d_2cta(dst + (hh * C::kQBoxes + x) * 64 * 128, &tm_k, lbar(bars->kv_full[sl]),
-                                      x * 64, h, j * BN + 128 * hh + 64 * (int)rank, b, pol_kv);
+                ptx::tma_load_4d_2cta(dst + (hh * C::kQBoxes + x) * 64 * 128, tk, lbar(bars->kv_full[sl]),
+                                      x * 64, h, row0 + 128 * hh, b, pol_kv);
           } else {
-            if (j >= v2_step)  // the new tokens' V, read in place from the caller's input (no staging copy)
-              ptx::tma_load_4d_2cta(dst, &tm_v2, lbar(bars->kv_full[sl]), (int)rank * (D / 2), h, (j - v2_step) * BN,
+            if (j >= cur_step)  // the new tokens' V, read in place from the caller's input (no staging copy)
+              ptx::tma_load_4d_2cta(dst, &tm_v2, lbar(bars->kv_full[sl]), (int)rank * (D / 2), h, (j - cur_step) * BN,
                                     b, pol_kv);
             else
               ptx::tma_load_4d_2cta(dst, &tm_v, lbar(bars->kv_full[sl]), (int)rank * (D / 2), h, j * BN, b, pol_kv);
@@ -1011,7 +1018,8 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
   auto k = attn_fwd_kernel<D, PP>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k, dim3(a.grid), dim3(kThreads), C::kSmem, s, a.tm_q, a.tm_k, a.tm_v, a.tm_v2, a.tm_o, a.v2_step,
+  return launch_pdl(k, dim3(a.grid), dim3(kThreads), C::kSmem, s, a.tm_q, a.tm_k, a.tm_v, a.tm_k2, a.tm_v2, a.tm_o,
+                    a.cur_step,
                     static_cast<__nv_bfloat16*>(a.out), a.o_bstride, a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq,
                     a.kv_len, a.m_static, a.debug_flags, a.ws, a.ws_cnt, a.spans);
 }

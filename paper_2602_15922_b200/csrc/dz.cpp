@@ -31,7 +31,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {  // byte offsets inside the caller's storage
   int64_t slots = 0;
-  size_t k_off = 0, v_off = 0, q_off = 0, lse_off = 0, sq_off = 0, sk_off = 0, sv_off = 0, ol_off = 0,
+  size_t k_off = 0, v_off = 0, q_off = 0, kc_off = 0, lse_off = 0, sq_off = 0, sk_off = 0, sv_off = 0, ol_off = 0,
          or_off = 0, map_off = 0, ws_off = 0, cnt_off = 0, cnt_bytes = 0, total = 0;
 };
 
@@ -72,6 +72,7 @@ Layout make_layout(const dz_config* c) {
   L.k_off = take((size_t)B * L.slots * Hl * D * 2);
   L.v_off = take((size_t)B * L.slots * Hl * D * 2);
   L.q_off = take((size_t)B * mc * Hl * D * 2);                       // Q' fp16
+  L.kc_off = take(N == 1 ? (size_t)B * mc * Hl * D * 2 : 0);         // K' fp16 of a noisy chunk (not staged)
   L.lse_off = take((c->flags & DZ_FLAG_WRITE_LSE) ? (size_t)B * Hl * mc * 4 : 0);
   L.map_off = take((c->flags & DZ_FLAG_TILE_MAP) ? map_bytes(c) : 0);
   // K2 stream-K workspace: per pair a head and a tail piece, per CTA rank (D + 2) x 128 fp32
@@ -135,6 +136,9 @@ struct dz_ctx {
   int32_t last_id = -1;
   // staged chunk (written by the last attend)
   bool staged = false;
+  // the last attention read the new tokens' K'/V from the staging slots after the committed ones
+  // (they are only staged there when the chunk may be committed, under SP, or unaligned)
+  bool staging_read = false;
   int32_t staged_id = 0, staged_kind = 0;
   int64_t staged_n = 0;
   // last attend geometry (tile map / lse)
@@ -287,7 +291,7 @@ void fill_prologue_common(dz_ctx* c, dz::PrologueArgs& a, const int32_t* pos, in
 // K1 prologue for the current chunk: Q' and the chunk's K'/V, written either
 // straight into the staging slot (N == 1) or into the all-to-all send layout.
 dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, const int32_t* pos, int64_t n,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool cur_separate = false, bool wait_late = false) {
   const int64_t n_loc = n / c->N;
   dz::PrologueArgs a;
   fill_prologue_common(c, a, pos, n_loc);
@@ -299,7 +303,10 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
     a.heads_per_dest = c->H;
     a.y[0] = {c->base + c->L.q_off, n * c->H * c->D, (int64_t)c->H * c->D, 0};
     const int64_t slot = c->start + c->valid;
-    a.y[1] = {c->kslot(0, slot), c->L.slots * c->H * c->D, (int64_t)c->H * c->D, 0};
+    if (cur_separate)  // a noisy chunk's K' goes to its own buffer; the committed cache is only read
+      a.y[1] = {c->base + c->L.kc_off, n * c->H * c->D, (int64_t)c->H * c->D, 0};
+    else
+      a.y[1] = {c->kslot(0, slot), c->L.slots * c->H * c->D, (int64_t)c->H * c->D, 0};
     a.y[2] = {c->vslot(0, slot), c->L.slots * c->H * c->D, (int64_t)c->H * c->D, 0};
   } else {
     a.heads_per_dest = c->Hl;
@@ -308,6 +315,7 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
     a.y[1] = {c->base + c->L.sk_off, bst, tst, dst};
     a.y[2] = {c->base + c->L.sv_off, bst, tst, dst};
   }
+  a.wait_late = wait_late ? 1 : 0;
   return cuda_check(c, dz::launch_prologue(a, st), "prologue launch");
 }
 
@@ -331,7 +339,7 @@ dz_status exchange_post(dz_ctx* c, int64_t n, cudaStream_t st) { return run_exch
 
 // K2 over local heads and the full sequence: committed slots + the staged chunk.
 dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* out_local, int64_t o_bstride,
-                        int64_t o_tstride, const void* v_new, cudaStream_t st) {
+                        int64_t o_tstride, const void* k_new, const void* v_new, cudaStream_t st) {
   dz::AttnArgs a;
   a.spans = spans;
   a.spans.valid = (int32_t)c->valid;
@@ -348,12 +356,13 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   if (o_tstride != (int64_t)c->Hl * c->D ||
       !make_tmap(&a.tm_o, out_local, true, c->D, c->Hl, n, c->B, o_bstride, (uint32_t)c->D / 2, 32))
     return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (O) failed");
-  if (v_new != nullptr) {  // the new tokens' V straight from the caller's [B][n][H][D] input
+  if (v_new != nullptr) {  // the new tokens: K' from the current-chunk buffer, V from the caller's input
     const int step_keys = dz::attention_step_keys(c->m_static);
-    if (!make_tmap(&a.tm_v2, v_new, true, c->D, c->Hl, n, c->B, n * c->Hl * c->D, (uint32_t)c->D / 2,
+    if (!make_tmap(&a.tm_k2, k_new, false, c->D, c->Hl, n, c->B, n * c->Hl * c->D, 64, 64) ||
+        !make_tmap(&a.tm_v2, v_new, true, c->D, c->Hl, n, c->B, n * c->Hl * c->D, (uint32_t)c->D / 2,
                    (uint32_t)step_keys))
-      return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (V in place) failed");
-    a.v2_step = (int32_t)(c->valid / step_keys);
+      return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (new tokens) failed");
+    a.cur_step = (int32_t)(c->valid / step_keys);
   }
   a.out = out_local;
   a.o_bstride = o_bstride;
@@ -481,7 +490,12 @@ dz_status dz_append_kv(dz_ctx* c, const void* k_raw, const void* v_raw, const dz
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool prof = c->ev_app[0] != nullptr && c->prof_on;
   if (prof) cudaEventRecord(c->ev_app[0], st);
-  if ((r = run_prologue(c, nullptr, k_raw, v_raw, s->pos_thw, s->n_tokens, st))) return r;
+  // With one GPU the append writes slots [valid, valid + n) that an attention still in flight on
+  // this stream only reads if it staged its new tokens there: otherwise K4 starts without waiting
+  // for its predecessor (it can run in the attention's tail) and waits before it completes.
+  const bool wait_late = c->N == 1 && !c->staging_read;
+  if ((r = run_prologue(c, nullptr, k_raw, v_raw, s->pos_thw, s->n_tokens, st, false, wait_late))) return r;
+  c->staging_read = false;
   if (c->N > 1 && (r = exchange_pre(c, false, s->n_tokens, st))) return r;
   if (prof) cudaEventRecord(c->ev_app[1], st);
   c->have_append_ev = prof;
@@ -502,26 +516,28 @@ dz_status attend_impl(dz_ctx* c, const void* q_raw, const void* k_raw, const voi
                       int64_t n, const dz::SpanTable& spans, void* out, bool may_commit, cudaStream_t st) {
   dz_status r;
   c->staged = false;
-  // V of the new tokens is only copied into the staging slot when the chunk may be committed
-  // (attend_chunk of a CLEAN chunk) or the exchange needs it (SP) or the new keys do not start at
-  // a key step; otherwise the attention reads it in place from the caller's input.
-  const bool v_in_place = c->N == 1 && !may_commit && c->valid % dz::attention_step_keys(c->m_static) == 0;
+  // The new tokens' K'/V are only staged after the committed slots when the chunk may be committed
+  // (attend_chunk of a CLEAN chunk), the exchange needs them (SP) or the new keys do not start at a
+  // key step; otherwise K' goes to the current-chunk buffer, V is read in place from the caller's
+  // input, and the attention only reads the committed cache.
+  const bool cur_sep = c->N == 1 && !may_commit && c->valid % dz::attention_step_keys(c->m_static) == 0;
+  c->staging_read = !cur_sep;
   const bool prof = c->ev[0] != nullptr && c->prof_on;
   auto mark = [&](int i) { if (prof) cudaEventRecord(c->ev[i], st); };
   mark(0);
-  if ((r = run_prologue(c, q_raw, k_raw, v_in_place ? nullptr : v_raw, pos, n, st))) return r;
+  if ((r = run_prologue(c, q_raw, k_raw, cur_sep ? nullptr : v_raw, pos, n, st, cur_sep))) return r;
   mark(1);
   if (c->N == 1) {
     mark(2);
-    if ((r = run_attention(c, n, spans, out, n * c->H * c->D, (int64_t)c->H * c->D, v_in_place ? v_raw : nullptr,
-                           st)))
+    if ((r = run_attention(c, n, spans, out, n * c->H * c->D, (int64_t)c->H * c->D,
+                           cur_sep ? c->base + c->L.kc_off : nullptr, cur_sep ? v_raw : nullptr, st)))
       return r;
     mark(3);
   } else {
     if ((r = exchange_pre(c, true, n, st))) return r;
     mark(2);
     if ((r = run_attention(c, n, spans, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, nullptr,
-                           st)))
+                           nullptr, st)))
       return r;
     mark(3);
     if ((r = exchange_post(c, n, st))) return r;

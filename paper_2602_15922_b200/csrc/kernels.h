@@ -45,6 +45,9 @@ struct PrologueArgs {
   int32_t B = 0, n = 0, H = 0, D = 0, heads_per_dest = 0;
   float eps = 1e-6f;
   float q_scale = 1.f;                             // extra factor on Q' (softmax_scale * log2e)
+  int32_t wait_late = 0;                           // 1: griddepcontrol.wait at the end, not the start
+                                                   // (the writes cannot conflict with an in-flight
+                                                   // predecessor; see dz_append_kv)
   double omega[kMaxHeadDim / 2];                   // per pair j: theta^(-2i/d_a), fp64 (host)
   int8_t axis[kMaxHeadDim / 2];                    // per pair j: 0 t, 1 h, 2 w
 };
@@ -72,7 +75,8 @@ struct AttnArgs {
   CUtensorMap tm_q;   // Q' fp16, dims (D, H, nq, B), box (64, 1, 128, 1), SW128
   CUtensorMap tm_k;   // K' fp16 cache, dims (D, H, kv_len, B)
   CUtensorMap tm_v;   // V  bf16 cache, dims (D, H, kv_len, B)
-  CUtensorMap tm_v2;  // V of the new tokens straight from the caller's input, dims (D, H, nq, B) (see v2_step)
+  CUtensorMap tm_k2;  // K' of the new tokens in the current-chunk buffer, dims (D, H, nq, B) (see cur_step)
+  CUtensorMap tm_v2;  // V of the new tokens straight from the caller's input, dims (D, H, nq, B) (see cur_step)
   CUtensorMap tm_o;   // O  bf16 output, dims (D, H, nq, B), box (64, 1, 32, 1), SW128 (epilogue TMA stores)
   void* out = nullptr;            // bf16, row (b, s, h) at out + b*o_bstride + s*o_tstride + h*D
   int64_t o_bstride = 0, o_tstride = 0;
@@ -85,7 +89,7 @@ struct AttnArgs {
   int32_t grid = 0;               // persistent CTAs (<= #SMs)
   float* ws = nullptr;            // stream-K piece workspace: [2 * pairs][2 ranks][(D + 2) * 128] fp32 (nullptr: no split)
   int32_t* ws_cnt = nullptr;      // per (unit, rank) piece counters, zero between launches
-  int32_t v2_step = 0x7fffffff;   // key steps >= v2_step read V from tm_v2 (row (j - v2_step) * step), else tm_v
+  int32_t cur_step = 0x7fffffff;  // key steps >= cur_step read K'/V from tm_k2/tm_v2 (row (j - cur_step) * step)
 };
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);
 constexpr int kMaxPairs = 80;  // CTA pairs of the persistent grid (B200: 74)

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
     cs[(k % L.S) * (D / 2) + ai] = make_float2((float)cn, (float)sn);
   };
   __syncthreads();  // barriers initialised, row offsets visible
-  ptx::pdl_wait();  // the previous kernel of the stream (e.g. the last attention reading the staging slot) is done
+  if (!a.wait_late) ptx::pdl_wait();  // the previous kernel of the stream (e.g. the last attention) is done
   if (tid == 0)
     for (int k = 0; k < L.S - 1; ++k) issue(k);
   // gains of this thread's heads (h = g + kGroups * i) and column slice, kept in registers
@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
     angles(k + 1, pos_k1);  // next item's angles into its own slot, off the critical path of the copies
     __syncthreads();  // stage and angles of item k may be refilled
   }
+  if (a.wait_late) ptx::pdl_wait();  // complete only after the previous kernel (ordering stays transitive)
 }
 
 // ---- one token per CTA: every load of the token issued at once, no ring --------------
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(256) prologue_tok_kernel(const PrologueArgs a)
   const int H = a.H;
   const int item = blockIdx.x;
   const int b = item / a.n, t = item - b * a.n;
-  ptx::pdl_wait();  // the previous kernel of the stream is done
+  if (!a.wait_late) ptx::pdl_wait();  // the previous kernel of the stream is done
   // 1. all loads of this token
   uint4 v[3][kPer];
   const int64_t src = (int64_t)b * a.x_bstride + (int64_t)t * H * D + li * 8;
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(256) prologue_tok_kernel(const PrologueArgs a)
       reinterpret_cast<uint4*>(o.base)[off] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
   }
+  if (a.wait_late) ptx::pdl_wait();  // complete only after the previous kernel (ordering stays transitive)
 }
 
 }  // namespace
