@@ -209,6 +209,44 @@ def test_sliding_window_evict_equals_fresh_cache():
     assert torch.equal(a, b)
 
 
+def test_pipelined_bench_steps_match_fresh_caches():
+    # the bench's step, back to back without host syncs: attend(noisy c) -> evict -> append(clean c)
+    # -> attend(noisy c + 1) ...  The append kernel starts before the attention completes (it
+    # writes slots the attention does not read) and the kernels overlap programmatically; every
+    # attention must equal, bit for bit, the same attention on a cache built from scratch
+    w = _small(heads=4, cached_chunks=3)
+    steps = 4
+    run = GpuRun(w, slack=8 * w.chunk_tokens, steps=steps)
+    run.fill()
+    C, n = w.cached_chunks, w.chunk_tokens
+    s0 = run.streams[0]
+    extra = [synth.draw_qkv(w, 0, C + i) for i in range(steps + 1)]          # (q, k, v) of chunks C..
+    outs = []
+    for i in range(steps):
+        c = C + i
+        q, k, v = extra[i]
+        pos = synth.chunk_positions(w, c).to(run.dev)
+        outs.append(run.cache.attend(q[None].to(run.dev), k[None].to(run.dev), v[None].to(run.dev), pos, c))
+        run.cache.evict_front(1)
+        run.cache.append(k[None].to(run.dev), v[None].to(run.dev), pos, c)   # the chunk enters, clean
+    torch.cuda.synchronize()
+    for i in range(steps):
+        c = C + i
+        fresh = GpuRun(w, capacity=C * n)
+        for j in range(c - C, c):   # the window of C chunks the i-th attention saw
+            if j < C:
+                kk, vv = s0.cache_k[j], s0.cache_v[j]
+            else:
+                _, kk, vv = extra[j - C]
+            fresh.cache.append(kk[None].to(fresh.dev), vv[None].to(fresh.dev),
+                               synth.chunk_positions(w, j).to(fresh.dev), j)
+        q, k, v = extra[i]
+        want = fresh.cache.attend(q[None].to(fresh.dev), k[None].to(fresh.dev), v[None].to(fresh.dev),
+                                  synth.chunk_positions(w, c).to(fresh.dev), c)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[i], want), f"step {i}"
+
+
 def test_online_softmax_path_c1():
     # the running-max (lazy rescale) path, forced on C1, must meet the same bar
     import paper_2602_15922_b200 as dz
