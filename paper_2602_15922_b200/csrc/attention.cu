@@ -597,12 +597,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             if (lane == 0) {
               const uint32_t ka = sKV + k_st * C::kStageBytes + hh * C::kQBoxes * 64 * 128;
+              const uint64_t dq0 = ptx::sdesc_sw128(sQ, 16, 1024), dk0 = ptx::sdesc_sw128(ka, 16, 1024);
 #pragma unroll
               for (int kk = 0; kk < D / 16; ++kk) {
                 const uint32_t qoff = (kk / 4) * (128 * 128) + (kk % 4) * 32;  // Q: 128 rows per box
                 const uint32_t koff = (kk / 4) * (64 * 128) + (kk % 4) * 32;   // K half: 64 rows per box
-                ptx::mma_ss_2cta(tmem + kColS + sb * 128, ptx::sdesc_sw128(sQ + qoff, 16, 1024),
-                                 ptx::sdesc_sw128(ka + koff, 16, 1024), C::kIdescQK, kk > 0);
+                // descriptors: the start address field is addr >> 4 in the low bits, offsets add
+                ptx::mma_ss_2cta(tmem + kColS + sb * 128, dq0 + (qoff >> 4), dk0 + (koff >> 4), C::kIdescQK, kk > 0);
                 if (tr && j == 9) trace[kTraceSteps * 8 + hh * 8 + kk] = (uint32_t)clock();
               }
               ptx::tc_commit_2cta(bar(bars->s_full[sb]), kBoth);
@@ -633,12 +634,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t va = sKV + v_st * C::kStageBytes;
+            const uint64_t dv0 = D == 128 ? ptx::sdesc_sw128(va, 16, 1024) : ptx::sdesc_sw64(va, 16, 512);
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk) {
-              const uint64_t bd = D == 128 ? ptx::sdesc_sw128(va + kk * 16 * C::kVRowBytes, 16, 1024)
-                                           : ptx::sdesc_sw64(va + kk * 16 * C::kVRowBytes, 16, 512);
-              ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + pb * 64 + kk * 8, bd, C::kIdescPV,
-                               (!first || kk > 0) ? 1u : 0u);
+              ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + pb * 64 + kk * 8, dv0 + ((kk * 16 * C::kVRowBytes) >> 4),
+                               C::kIdescPV, (!first || kk > 0) ? 1u : 0u);
               if (tr && j == 9) trace[kTraceSteps * 8 + 16 + kk] = (uint32_t)clock();
             }
             ptx::tc_commit_2cta(bar(bars->p_empty[pb]), kBoth);              // P may be overwritten
