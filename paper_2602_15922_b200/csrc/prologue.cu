@@ -9,7 +9,8 @@
 // multiplied by softmax_scale * log2(e), so the attention kernel's scores come
 // out of the tensor core already in log2 units (one FMA per score saved).
 //
-// Layout: a persistent grid (2 CTAs per SM) walks the (batch, token) items.
+// Two kernels.  H <= 48 at D = 128 (the paper's 40 heads): prologue_loop_kernel, see there.
+// More heads: prologue_kernel, a persistent grid (2 CTAs per SM) that walks the (batch, token) items.
 // Each item's Q, K, V rows are contiguous H x D blocks in the [B][n][H][D]
 // input, so one thread issues three 1D bulk copies (cp.async.bulk, TMA) per
 // item into a kStages-deep shared-memory ring, kStages - 1 items ahead of the
@@ -37,6 +38,12 @@ constexpr int kThreads = 256;
 #endif
 #ifndef DZ_PRO_RING_KB
 #define DZ_PRO_RING_KB 96
+#endif
+#ifndef DZ_PRO_LOOP_MINB
+#define DZ_PRO_LOOP_MINB 2
+#endif
+#ifndef DZ_PRO_LOOP_WAVES
+#define DZ_PRO_LOOP_WAVES 1
 #endif
 constexpr int kCtasPerSm = DZ_PRO_CTAS;
 constexpr int kMaxStageBytes = DZ_PRO_RING_KB * 1024;  // ring size cap per CTA
@@ -233,55 +240,88 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
   if (a.wait_late) ptx::pdl_wait();  // complete only after the previous kernel (ordering stays transitive)
 }
 
-// ---- one token per CTA: every load of the token issued at once, no ring --------------
-// CTA = (batch, token); thread (g, li) owns column slice li (8 elements) of heads g, g + G', ...
-// of every present tensor.  All of the token's loads (<= 9 x 16 B per thread) are in flight
-// before the first use; the token's D/2 angles are computed once (fp64, one thread each) and
-// shared through shared memory.  Many small CTAs (3 per SM by registers) replace the
-// persistent ring: the ring's per-item barriers and its short pipelines (4.5 items per CTA at
-// C1) left the kernel latency-bound.
-template <int D>
-__global__ void __launch_bounds__(256) prologue_tok_kernel(const PrologueArgs a) {
-  constexpr int G = D / 8;                // threads per row
-  constexpr int kRows = 256 / G;          // rows side by side (16 at D = 128)
-  constexpr int kPer = 3;                 // heads per thread per tensor (H <= 48 at D = 128)
+// ---- token loop: registers instead of a ring --------------------------------------------
+// Thread (g, li) owns column slice li (8 elements) of heads g, g + G', g + 2G' of every present
+// tensor.  The persistent ring above (its per-item barriers, 4.5 items per CTA at C1) and a
+// one-token-per-CTA variant both left the kernel latency- or instruction-bound.
+// Token loop (H <= 48 at D = 128, the default): the per-row arithmetic of prologue_kernel
+// with a row per D/8 threads straight from registers; a CTA walks tokens item, item + grid,
+// ... and keeps the next token's loads and rotation angles in flight while it processes the
+// current one.  The tensors present are a template
+// mask (bit w: x[w] given), so only their registers exist; the per-thread head offsets
+// (including the SP destination split h / heads_per_dest) are computed once per CTA.
+// (It replaced a one-token-per-CTA kernel that ncu showed instruction-bound -- 7060 warp
+// instructions per token, mostly per-token address and division arithmetic: attend prologue
+// 24.2 -> 22.4 us, append 19.7 -> 17.1 us at C1.)
+template <int D, int MASK>
+__global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(const PrologueArgs a) {
+  constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
   ptx::pdl_launch_dependents();
-  __shared__ float2 cs[D / 2];
+  __shared__ float2 cs[2][D / 2];
   const int tid = threadIdx.x, g = tid / G, li = tid % G;
-  const int H = a.H;
-  const int item = blockIdx.x;
-  const int b = item / a.n, t = item - b * a.n;
-  if (!a.wait_late) ptx::pdl_wait();  // the previous kernel of the stream is done
-  // 1. all loads of this token
-  uint4 v[3][kPer];
-  const int64_t src = (int64_t)b * a.x_bstride + (int64_t)t * H * D + li * 8;
+  const int H = a.H, items = a.B * a.n;
+  const int64_t tokD = (int64_t)H * D;
+  // per (tensor, head slot): output offset inside the token's block, in elements
+  int64_t ooff[3][kPer];
+  bool hv[kPer];
 #pragma unroll
-  for (int w = 0; w < 3; ++w)
+  for (int i = 0; i < kPer; ++i) {
+    const int h = g + kRows * i;
+    hv[i] = h < H;
+    const int dest = h / a.heads_per_dest;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const int h = g + kRows * i;
-      if (a.x[w] != nullptr && h < H)
-        v[w][i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.x[w]) + src + h * D));
-    }
-  // 2. the token's rotation angles
-  if (tid < D / 2) {
-    double sn, cn;
-    sincos((double)__ldg(a.pos + 3 * t + a.axis[tid]) * a.omega[tid], &sn, &cn);
-    cs[tid] = make_float2((float)cn, (float)sn);
+    for (int w = 0; w < 3; ++w)
+      if (MASK >> w & 1) ooff[w][i] = (int64_t)dest * a.y[w].dstride + (int64_t)(h - dest * a.heads_per_dest) * D + li * 8;
   }
-  __syncthreads();
-  float2 csr[4];
+  auto load = [&](int item, uint4 (&v)[3][kPer]) {
+    const int b = item / a.n, t = item - b * a.n;
+    const int64_t src = (int64_t)b * a.x_bstride + (int64_t)t * tokD + g * D + li * 8;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) csr[e] = cs[li * 4 + e];
-  // 3. V copies, Q / K RMSNorm + RoPE
+    for (int w = 0; w < 3; ++w)
+      if (MASK >> w & 1)
 #pragma unroll
-  for (int w = 0; w < 3; ++w) {
-    if (a.x[w] == nullptr) continue;
-    const OutSlot& o = a.y[w];
-    const int64_t base = (int64_t)b * o.bstride + (int64_t)t * o.tstride;
-    float ss[kPer];
-    float f[kPer][8];
-    if (w != 2) {
+        for (int i = 0; i < kPer; ++i)
+          if (hv[i])
+            v[w][i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.x[w]) + src +
+                                                          (int64_t)kRows * i * D));
+  };
+  auto angles = [&](int item, int buf) {
+    if (tid < D / 2) {
+      const int t = item % a.n;
+      double sn, cn;
+      sincos((double)__ldg(a.pos + 3 * t + a.axis[tid]) * a.omega[tid], &sn, &cn);
+      cs[buf][tid] = make_float2((float)cn, (float)sn);
+    }
+  };
+  if (!a.wait_late) ptx::pdl_wait();
+  uint4 v[3][kPer], vn[3][kPer];
+  int item = blockIdx.x;
+  if (item < items) {
+    load(item, v);
+    angles(item, 0);
+  }
+  for (int it = 0; item < items; item += gridDim.x, ++it) {
+    const int nxt = item + gridDim.x;
+    if (nxt < items) load(nxt, vn);  // in flight while this token is processed
+    __syncthreads();                 // cs[it & 1] written; cs[(it + 1) & 1] no longer read
+    if (nxt < items) angles(nxt, (it + 1) & 1);
+    float2 csr[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) csr[e] = cs[it & 1][li * 4 + e];
+    const int b = item / a.n, t = item - b * a.n;
+#pragma unroll
+    for (int w = 0; w < 3; ++w) {
+      if (!(MASK >> w & 1)) continue;
+      const OutSlot& o = a.y[w];
+      const int64_t base = (int64_t)b * o.bstride + (int64_t)t * o.tstride;
+      if (w == 2) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i)
+          if (hv[i]) reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(o.base) + base + ooff[w][i])[0] = v[w][i];
+        continue;
+      }
+      float ss[kPer];
+      float f[kPer][8];
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         bf16x8_to_f32(v[w][i], f[i]);
@@ -293,43 +333,66 @@ __global__ void __launch_bounds__(256) prologue_tok_kernel(const PrologueArgs a)
       for (int m = G / 2; m >= 1; m >>= 1)
 #pragma unroll
         for (int i = 0; i < kPer; ++i) ss[i] += __shfl_xor_sync(0xffffffffu, ss[i], m);
-    }
-    const float sc = w == 0 ? a.q_scale : 1.f;
+      const float sc = w == 0 ? a.q_scale : 1.f;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      const int h = g + kRows * i;
-      if (h >= H) continue;
-      const int dest = h / a.heads_per_dest;
-      const int64_t off = (base + (int64_t)dest * o.dstride + (int64_t)(h - dest * a.heads_per_dest) * D) / 8 + li;
-      if (w == 2) {
-        reinterpret_cast<uint4*>(o.base)[off] = v[w][i];
-        continue;
-      }
-      const float inv = rsqrtf(ss[i] * (1.0f / D) + a.eps);
-      const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
-      const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      uint32_t pk[4];
+      for (int i = 0; i < kPer; ++i) {
+        if (!hv[i]) continue;
+        const int h = g + kRows * i;
+        const float inv = rsqrtf(ss[i] * (1.0f / D) + a.eps);
+        const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
+        const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        uint32_t pk[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float u = f[i][2 * e] * inv * gg[2 * e];
-        const float x = f[i][2 * e + 1] * inv * gg[2 * e + 1];
-        pk[e] = pack_half2((u * csr[e].x - x * csr[e].y) * sc, (u * csr[e].y + x * csr[e].x) * sc);
+        for (int e = 0; e < 4; ++e) {
+          const float u = f[i][2 * e] * inv * gg[2 * e];
+          const float x = f[i][2 * e + 1] * inv * gg[2 * e + 1];
+          pk[e] = pack_half2((u * csr[e].x - x * csr[e].y) * sc, (u * csr[e].y + x * csr[e].x) * sc);
+        }
+        reinterpret_cast<uint4*>(static_cast<__half*>(o.base) + base + ooff[w][i])[0] =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-      reinterpret_cast<uint4*>(o.base)[off] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
+#pragma unroll
+    for (int w = 0; w < 3; ++w)
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) v[w][i] = vn[w][i];
   }
-  if (a.wait_late) ptx::pdl_wait();  // complete only after the previous kernel (ordering stays transitive)
+  if (a.wait_late) ptx::pdl_wait();
 }
 
 }  // namespace
 
+template <int D, int MASK>
+cudaError_t launch_loop(const PrologueArgs& a, cudaStream_t s) {
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_loop_kernel<D, MASK>, 256, 0);
+    grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
+  }
+  const int items = a.B * a.n;
+  return launch_pdl(prologue_loop_kernel<D, MASK>, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s, a);
+}
+
 template <int D>
 cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
-  // one token per CTA when a token's heads fit one pass of the CTA (H <= 48 at D = 128), else the
-  // persistent ring (measured at C1: append 19.3 vs 20.5 us, attend prologue 23.7 vs 23.8 us)
-  if (a.H <= 3 * (256 / (D / 8)))
-    return launch_pdl(prologue_tok_kernel<D>, dim3((unsigned)(a.B * a.n)), dim3(256), 0, s, a);
+  if (a.H <= 3 * (256 / (D / 8))) {
+    const int mask = (a.x[0] ? 1 : 0) | (a.x[1] ? 2 : 0) | (a.x[2] ? 4 : 0);
+    switch (mask) {
+      case 1: return launch_loop<D, 1>(a, s);
+      case 2: return launch_loop<D, 2>(a, s);
+      case 3: return launch_loop<D, 3>(a, s);
+      case 4: return launch_loop<D, 4>(a, s);
+      case 5: return launch_loop<D, 5>(a, s);
+      case 6: return launch_loop<D, 6>(a, s);
+      case 7: return launch_loop<D, 7>(a, s);
+      default: return cudaSuccess;
+    }
+  }
+  // more heads than one pass of the CTA: the persistent ring
   int nt = 0;
   for (int w = 0; w < 3; ++w) nt += a.x[w] != nullptr;
   const ProSmem L(a.H, D, nt);
