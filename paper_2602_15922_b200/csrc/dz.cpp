@@ -32,7 +32,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct Layout {  // byte offsets inside the caller's storage
   int64_t slots = 0;
   size_t k_off = 0, v_off = 0, q_off = 0, kc_off = 0, lse_off = 0, sq_off = 0, sk_off = 0, sv_off = 0, ol_off = 0,
-         or_off = 0, map_off = 0, ws_off = 0, cnt_off = 0, cnt_bytes = 0, total = 0;
+         or_off = 0, map_off = 0, ws_off = 0, cnt_off = 0, cnt_bytes = 0, rope_off = 0, total = 0;
 };
 
 bool basic_cfg_ok(const dz_config* c) {
@@ -79,6 +79,7 @@ Layout make_layout(const dz_config* c) {
   L.ws_off = take((size_t)2 * dz::kMaxPairs * 2 * (D + 2) * 128 * 4);
   L.cnt_bytes = (size_t)B * Hl * ((mc + dz::kTileQ - 1) / dz::kTileQ) * 2 * 4;
   L.cnt_off = take(L.cnt_bytes);
+  L.rope_off = take((size_t)dz::kRopeLen * (D / 2) * 8);             // RoPE (cos, sin) table, fp32
   if (N > 1) {
     const size_t sb = (size_t)B * (mc / N) * c->heads * D * 2;       // [N][B][n_loc][Hl][D]
     L.sq_off = take(sb);
@@ -150,6 +151,7 @@ struct dz_ctx {
   ncclComm_t comm = nullptr;
   bool poisoned = false;
   bool ws_zeroed = false;  // stream-K piece counters initialised
+  bool rope_ready = false;  // RoPE table written (first prologue)
   // DZ_FLAG_PROFILE: events e[0..4] around the attend phases, a[0..1] around the append
   cudaEvent_t ev[5] = {}, ev_app[2] = {};
   bool have_attend_ev = false, have_append_ev = false;
@@ -314,6 +316,15 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
     a.y[0] = {c->base + c->L.sq_off, bst, tst, dst};
     a.y[1] = {c->base + c->L.sk_off, bst, tst, dst};
     a.y[2] = {c->base + c->L.sv_off, bst, tst, dst};
+  }
+  a.rope_tab = reinterpret_cast<const float2*>(c->base + c->L.rope_off);
+  a.rope_len = dz::kRopeLen;
+  if (!c->rope_ready) {  // first prologue: fill the table; this prologue waits for it before reading
+    dz_status r = cuda_check(c, dz::launch_rope_table(reinterpret_cast<float2*>(c->base + c->L.rope_off),
+                                                      dz::kRopeLen, a, st), "rope table launch");
+    if (r) return r;
+    c->rope_ready = true;
+    wait_late = false;
   }
   a.wait_late = wait_late ? 1 : 0;
   return cuda_check(c, dz::launch_prologue(a, st), "prologue launch");

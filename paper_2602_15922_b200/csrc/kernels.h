@@ -48,10 +48,16 @@ struct PrologueArgs {
   int32_t wait_late = 0;                           // 1: griddepcontrol.wait at the end, not the start
                                                    // (the writes cannot conflict with an in-flight
                                                    // predecessor; see dz_append_kv)
+  const float2* rope_tab = nullptr;                // [rope_len][D/2] (cos, sin) of p * omega_j, or null
+  int32_t rope_len = 0;                            // positions 0 .. rope_len-1 tabulated (others computed)
   double omega[kMaxHeadDim / 2];                   // per pair j: theta^(-2i/d_a), fp64 (host)
   int8_t axis[kMaxHeadDim / 2];                    // per pair j: 0 t, 1 h, 2 w
 };
 cudaError_t launch_prologue(const PrologueArgs& a, cudaStream_t s);
+// RoPE table: tab[p][j] = (cos, sin)(p * omega_j) for p < len, fp64 sincos rounded to fp32
+// (the same values the prologue would compute per token)
+constexpr int kRopeLen = 4096;
+cudaError_t launch_rope_table(float2* tab, int32_t len, const PrologueArgs& a, cudaStream_t s);
 
 // ---- K2: block-causal flash attention (tcgen05 + TMEM + TMA) --------------
 // Fig. 10 visibility in span form (R3).  Queries are

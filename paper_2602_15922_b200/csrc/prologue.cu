@@ -62,6 +62,13 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// (cos, sin) of the angle p * omega in fp64, rounded to fp32 (table fill, untabulated positions)
+__device__ __noinline__ float2 rope_cs(int p, double omega) {
+  double sn, cn;
+  sincos((double)p * omega, &sn, &cn);
+  return make_float2((float)cn, (float)sn);
+}
+
 // shared-memory carve-up for H heads, nt tensors present, S stages
 struct ProSmem {
   int row_bytes, stage_bytes, S;
@@ -257,7 +264,6 @@ template <int D, int MASK>
 __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(const PrologueArgs a) {
   constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
   ptx::pdl_launch_dependents();
-  __shared__ float2 cs[2][D / 2];
   const int tid = threadIdx.x, g = tid / G, li = tid % G;
   const int H = a.H, items = a.B * a.n;
   const int64_t tokD = (int64_t)H * D;
@@ -285,29 +291,42 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
             v[w][i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.x[w]) + src +
                                                           (int64_t)kRows * i * D));
   };
-  auto angles = [&](int item, int buf) {
-    if (tid < D / 2) {
-      const int t = item % a.n;
-      double sn, cn;
-      sincos((double)__ldg(a.pos + 3 * t + a.axis[tid]) * a.omega[tid], &sn, &cn);
-      cs[buf][tid] = make_float2((float)cn, (float)sn);
-    }
+  // this thread's 4 rotation pairs j = 4 li + e: their axis is fixed, their angle depends on the
+  // token's position on that axis; (cos, sin) come from the table (positions two tokens ahead,
+  // table entries one token ahead of their use), or are computed for untabulated positions
+  int ax[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) ax[e] = a.axis[li * 4 + e];
+  auto positions = [&](int item, int (&p)[4]) {
+    if (item >= items) return;
+    const int t = item % a.n;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = __ldg(a.pos + 3 * t + ax[e]);
+  };
+  auto angles = [&](const int (&p)[4], float2 (&c)[4]) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      c[e] = (unsigned)p[e] < (unsigned)a.rope_len ? __ldg(a.rope_tab + (size_t)p[e] * (D / 2) + li * 4 + e)
+                                                   : rope_cs(p[e], a.omega[li * 4 + e]);
   };
   if (!a.wait_late) ptx::pdl_wait();
   uint4 v[3][kPer], vn[3][kPer];
+  float2 csr[4], csn[4];
+  int pn[4] = {0, 0, 0, 0};
   int item = blockIdx.x;
   if (item < items) {
     load(item, v);
-    angles(item, 0);
+    positions(item, pn);
+    angles(pn, csr);
+    positions(item + gridDim.x, pn);
   }
-  for (int it = 0; item < items; item += gridDim.x, ++it) {
+  for (; item < items; item += gridDim.x) {
     const int nxt = item + gridDim.x;
-    if (nxt < items) load(nxt, vn);  // in flight while this token is processed
-    __syncthreads();                 // cs[it & 1] written; cs[(it + 1) & 1] no longer read
-    if (nxt < items) angles(nxt, (it + 1) & 1);
-    float2 csr[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) csr[e] = cs[it & 1][li * 4 + e];
+    if (nxt < items) {  // in flight while this token is processed
+      load(nxt, vn);
+      angles(pn, csn);
+      positions(nxt + gridDim.x, pn);
+    }
     const int b = item / a.n, t = item - b * a.n;
 #pragma unroll
     for (int w = 0; w < 3; ++w) {
@@ -357,8 +376,18 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
     for (int w = 0; w < 3; ++w)
 #pragma unroll
       for (int i = 0; i < kPer; ++i) v[w][i] = vn[w][i];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) csr[e] = csn[e];
   }
   if (a.wait_late) ptx::pdl_wait();
+}
+
+template <int D>
+__global__ void rope_table_kernel(float2* __restrict__ tab, int32_t len, const PrologueArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)len * (D / 2)) return;
+  const int p = (int)(i / (D / 2)), j = (int)(i % (D / 2));
+  tab[i] = rope_cs(p, a.omega[j]);
 }
 
 }  // namespace
@@ -410,6 +439,15 @@ cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
   const int items = a.B * a.n;
   const int grid = items < kCtasPerSm * sms ? items : kCtasPerSm * sms;
   return launch_pdl(k, dim3(grid), dim3(kThreads), (size_t)smem, s, a);
+}
+
+cudaError_t launch_rope_table(float2* tab, int32_t len, const PrologueArgs& a, cudaStream_t s) {
+  const int64_t n = (int64_t)len * (a.D / 2);
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  if (a.D == 128) rope_table_kernel<128><<<grid, 256, 0, s>>>(tab, len, a);
+  else if (a.D == 64) rope_table_kernel<64><<<grid, 256, 0, s>>>(tab, len, a);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_prologue(const PrologueArgs& a, cudaStream_t s) {
