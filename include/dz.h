@@ -112,11 +112,14 @@ typedef struct {
 
 /* Bytes of cache storage the caller must provide for cfg:
  *   2 tensors (K' fp16, V bf16) x batch x (capacity + max_chunk + slack) x
- *   (heads / world_size) x head_dim x 2 B, rounded up to 256 B. 0 if cfg is invalid. */
+ *   (heads / world_size) x head_dim x 2 B, plus the device workspace below (Q' and
+ *   the noisy chunk's K' fp16, the stream-K partials, a 4096 x head_dim/2 fp32 RoPE
+ *   (cos, sin) table written by the first prologue, SP buffers), each rounded up to
+ *   256 B. 0 if cfg is invalid. */
 DZ_API size_t dz_cache_bytes(const dz_config* cfg);
 
 /* Validates cfg and computes the RoPE frequencies (fp64, host).  The device
- * workspace (Q', the all-to-all buffers under SP, debug maps) lives inside the
+ * workspace (Q', the RoPE table, the all-to-all buffers under SP, debug maps) lives inside the
  * caller's cache_storage (dz_cache_bytes counts it); the context allocates no
  * device memory.  Also derives the QK-norm logit bound
  *   |<q',k'>| * scale * log2(e) <= head_dim * max_abs_gain^2 * scale * log2(e)
