@@ -24,13 +24,28 @@ def test_append_parity(wname):
 
 
 def test_append_parity_many_heads_ring_prologue():
-    # 56 heads at D = 128 exceed one pass of the one-token-per-CTA prologue (48 heads): the
+    # 56 heads at D = 128 exceed one pass of the token-loop prologue (48 heads): the
     # persistent TMA-ring prologue runs instead; same checks
     _append_parity(synth.scaled(synth.workload("C1"), heads=56, cached_chunks=2))
 
 
-def _append_parity(w):
+def test_positions_beyond_rope_table():
+    # the prologue takes (cos, sin) from a table of positions 0..4095 and computes the others in
+    # place: t straddles the table's end inside the cache (4094..4097), h and w lie far beyond it
+    w = synth.workload("C0")
     run = GpuRun(w)
+    for s in run.streams:
+        for p in list(s.cache_pos) + [s.cur_pos]:
+            p[:, 0] += 4094
+            p[:, 1] += 70000
+            p[:, 2] += 123456
+    _append_parity(w, run)
+    out = run.attend().cpu().double().numpy()[0]
+    assert_parity(out, run.oracle_out(), "positions beyond the table")
+
+
+def _append_parity(w, run=None):
+    run = run or GpuRun(w)
     run.fill()
     torch.cuda.synchronize()
     valid, nch, last = run.cache.state()
