@@ -323,7 +323,9 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
     dz_status r = cuda_check(c, dz::launch_rope_table(reinterpret_cast<float2*>(c->base + c->L.rope_off),
                                                       dz::kRopeLen, a, st), "rope table launch");
     if (r) return r;
-    c->rope_ready = true;
+    // a fill recorded into a graph being captured has not run yet: fill again on the next eager call
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) c->rope_ready = true;
     wait_late = false;
   }
   a.wait_late = wait_late ? 1 : 0;
@@ -401,7 +403,8 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
     dz_status r = cuda_check(c, cudaMemsetAsync(a.ws_cnt, 0, c->L.cnt_bytes, st),
                              "counter init");
     if (r) return r;
-    c->ws_zeroed = true;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;  // (a captured clear runs at replay only)
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) c->ws_zeroed = true;
   }
   const int ngr = (int)n_groups, nst = (int)n_steps;
   if ((c->cfg.flags & DZ_FLAG_TILE_MAP) && (size_t)ngr * nst <= map_bytes(&c->cfg)) {

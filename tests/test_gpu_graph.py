@@ -73,3 +73,25 @@ def test_graph_replay_follows_new_inputs():
     for s in range(w.steps):
         want = run.cache.attend(*saved[(s + 1) % w.steps], pos, C)
         assert torch.equal(outs[s], want), f"replay with new inputs differs at step {s}"
+
+
+def test_graph_capture_as_the_first_call():
+    # capture before any eager call: the context's one-time device setup (piece counters, RoPE
+    # table) is recorded into the graph, so an eager call before the first replay must still
+    # set it up itself, and the replay must reproduce that call
+    w = synth.scaled(synth.workload("C1"), heads=4, cached_chunks=0)
+    run = GpuRun(w, capacity=w.chunk_tokens)
+    pos = run.streams[0].cur_pos.to(run.dev)
+    q, k, v = [run.stack(key, 0).clone() for key in ("cur_q", "cur_k", "cur_v")]
+    out = torch.empty_like(q)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, capture_error_mode="thread_local"):
+        run.cache.attend(q, k, v, pos, 0, out=out)
+    eager = run.cache.attend(q, k, v, pos, 0).clone()
+    torch.cuda.synchronize()
+    assert_parity(eager[0].cpu().double().numpy(), run.oracle_out(), "eager after capture")
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager), "first-call graph replay differs from the eager call"
