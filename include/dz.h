@@ -150,7 +150,10 @@ DZ_API dz_status dz_append_kv(dz_ctx* ctx, const void* k_raw, const void* v_raw,
  * Capture-safe: no host synchronisation, every launch on `stream`, so the
  * denoising steps of one chunk can be recorded once into a CUDA graph and
  * replayed; a replay reads the committed state of the
- * capture, so re-capture after dz_append_kv / dz_evict_front / dz_commit_staged. */
+ * capture, so re-capture after dz_append_kv / dz_evict_front / dz_commit_staged.
+ * The context's one-time device setup (stream-K piece counters, RoPE table) runs
+ * in the first call; if that call is captured, the setup is part of the graph and
+ * the next eager call performs it again. */
 DZ_API dz_status dz_attend_chunk(dz_ctx* ctx, const void* q_raw, const void* k_raw, const void* v_raw,
                           const dz_span* chunk, void* out, void* stream);
 
