@@ -77,7 +77,15 @@ enum {
   DZ_FLAG_PROFILE = 2,   /* record CUDA events around every kernel/exchange (dz_profile_last) */
   DZ_FLAG_ONLINE_SOFTMAX = 4, /* always track the running row max, even when the QK-norm bound
                                  D*max|g|^2*scale would allow a fixed softmax base (see dz_create) */
-  DZ_FLAG_TILE_MAP = 8        /* record the attention kernel's tile decisions (dz_get_tile_map; tests) */
+  DZ_FLAG_TILE_MAP = 8,       /* record the attention kernel's tile decisions (dz_get_tile_map; tests) */
+  DZ_FLAG_EXTERNAL_EXCHANGE = 16, /* world_size > 1 without NCCL: calls stop at each all-to-all, the
+                                     caller moves the bytes dz_sp_pending lists, then dz_sp_resume */
+  DZ_FLAG_WHOLE_UNITS = 32,   /* no stream-K split: each (batch, head, 256-row query group) is computed
+                                 whole by one CTA pair, so its bits do not depend on the unit count
+                                 (identical results at every world size, reading A21) */
+  DZ_FLAG_HOST_ONLY = 64      /* planning context: never touches the device (gains unread, the caller's
+                                 max_abs_gain is taken as given); compute calls validate, then
+                                 return DZ_ESTATE without enqueuing; dz_sp_plan works (host tests) */
 };
 
 typedef struct {
@@ -93,10 +101,11 @@ typedef struct {
   int32_t window_slack_tokens;   /* extra slots so dz_evict_front rarely compacts; 0 = none */
   const float* q_gain;           /* device fp32 [heads*head_dim]; must outlive the ctx      */
   const float* k_gain;           /* device fp32 [heads*head_dim]; must outlive the ctx      */
-  float max_abs_gain;            /* host-side bound on |gain| (checked: DZ_ERANGE)           */
+  float max_abs_gain;            /* optional bound on |gain|: 0 = none; if > 0 it must be >= the
+                                    true max (dz_create reads the gains; else DZ_ERANGE)       */
   void* cache_storage;           /* device buffer of >= dz_cache_bytes(cfg) bytes, 256-B aligned */
   size_t cache_bytes;
-  void* nccl_comm;               /* ncclComm_t when world_size > 1, else NULL               */
+  void* nccl_comm;               /* ncclComm_t when world_size > 1 (NULL with DZ_FLAG_EXTERNAL_EXCHANGE) */
   int32_t world_size;            /* Ulysses sequence-parallel ranks (heads % world_size == 0) */
   int32_t rank;
   int32_t flags;                 /* DZ_FLAG_*                                               */
@@ -121,17 +130,24 @@ DZ_API size_t dz_cache_bytes(const dz_config* cfg);
 /* Validates cfg and computes the RoPE frequencies (fp64, host).  The device
  * workspace (Q', the RoPE table, the all-to-all buffers under SP, debug maps) lives inside the
  * caller's cache_storage (dz_cache_bytes counts it); the context allocates no
- * device memory.  Also derives the QK-norm logit bound
- *   |<q',k'>| * scale * log2(e) <= head_dim * max_abs_gain^2 * scale * log2(e)
+ * device memory.  Reads q_gain and k_gain once (a synchronous device-to-host copy;
+ * an unreadable pointer gives DZ_EINVAL, a non-finite gain DZ_ERANGE) and takes
+ * G = max |g| from them; a caller bound max_abs_gain > 0 below G is rejected
+ * (DZ_ERANGE), and sqrt(head_dim) * G >= 6e4 would overflow fp16 Q'/K' (DZ_ERANGE).
+ * Also derives the QK-norm logit bound
+ *   |<q',k'>| * scale * log2(e) <= head_dim * G^2 * scale * log2(e)
  * (RMSNorm makes ||x'|| <= sqrt(head_dim) * max|g|); when it is <= 60 the
- * attention uses it as a fixed softmax base instead of a running row max
- * (DZ_FLAG_ONLINE_SOFTMAX disables this).  *out is owned by the caller until
- * dz_destroy. */
+ * attention uses base 0 (p = 2^s in [2^-60, 2^60]) instead of a running row max
+ * (DZ_FLAG_ONLINE_SOFTMAX disables this).  The gains are model weights: the bound
+ * is taken at create, so a caller who later enlarges them must recreate the
+ * context.  *out is owned by the caller until dz_destroy. */
 DZ_API dz_status dz_create(const dz_config* cfg, dz_ctx** out);
 
 /* Cache append of a clean chunk (Alg. 2 l.601-602, update=True): K' =
  * RoPE(RMSNorm(k_raw)) and V are written to slots [valid, valid + n) and
- * committed.  Requires chunk->kind == DZ_CLEAN, chunk_id greater than the last
+ * committed.  The append kernel may be scheduled while the previous kernel of
+ * `stream` drains, but reads k_raw / v_raw / positions only after that kernel
+ * (which may have produced them) has completed.  Requires chunk->kind == DZ_CLEAN, chunk_id greater than the last
  * committed id (else DZ_ESTATE) and valid + n <= capacity (else DZ_ECAPACITY).
  * k_raw, v_raw: bf16 [batch][n_local][heads][head_dim]. */
 DZ_API dz_status dz_append_kv(dz_ctx* ctx, const void* k_raw, const void* v_raw, const dz_span* chunk, void* stream);
@@ -207,7 +223,8 @@ DZ_API dz_status dz_copy_lse(dz_ctx* ctx, float* dst, size_t dst_elems, void* st
 
 /* Tile map of the last attend as decided by the attention kernel for (batch,
  * head) = (0, 0): host uint8 [n_q_tiles][n_kv_tiles] with tiles of *bm = 256
- * query rows (one CTA pair) x *bn = 256 keys (one KV step); 0 SKIP (not
+ * query rows (one CTA pair) x *bn keys (one KV step: 128 with the fixed softmax
+ * base, 256 with the online one); 0 SKIP (not
  * computed), 1 PARTIAL (masked per element), 2 FULL (unmasked) -- the
  * encoding of the oracle's classifier.  Synchronous device read (tests). */
 DZ_API dz_status dz_get_tile_map(const dz_ctx* ctx, uint8_t* host, size_t cap, int32_t* n_q_tiles, int32_t* n_kv_tiles,
@@ -242,11 +259,14 @@ DZ_API dz_status dz_nccl_unique_id(void* id128);
 DZ_API dz_status dz_nccl_comm_init(int32_t world_size, const void* id128, int32_t rank, void** comm);
 DZ_API dz_status dz_nccl_comm_destroy(void* comm);
 
-/* Hang diagnosis: every mbarrier wait in the attention kernel is bounded (5 s).
- * A wait that times out records {1, block, warp, barrier smem address, parity,
- * SM id, barrier-block base, 0} and makes all later waits return, so the kernel
- * finishes with garbage output instead of hanging the GPU.  Copies that record
- * (zeros if no timeout) to host8[8]; reset != 0 clears it.  Synchronous. */
+/* Hang diagnosis: every mbarrier wait in the kernels is bounded (5 s).  A wait
+ * that times out records {1, block, warp, barrier smem address, parity, SM id,
+ * barrier-block base, 0} and traps, so the launch fails with a CUDA error (seen at
+ * the next sync; the context's next call returns DZ_ECUDA and poisons it) instead
+ * of hanging the GPU or returning garbage.  In the diagnostics build
+ * (libdz_trace.so) the kernel drains instead and this call reads the record.
+ * Copies that record (zeros if no timeout) to host8[8]; reset != 0 clears it.
+ * Synchronous. */
 DZ_API dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset);
 
 /* Pipeline diagnostics: enable != 0 makes later attention launches record a
@@ -278,6 +298,21 @@ typedef struct {
  * negative dz_status.  Host only, no device access: lets host-side tests check
  * the plan with any process-group backend. */
 DZ_API int32_t dz_sp_plan(const dz_ctx* ctx, int32_t phase, int32_t n_tokens, dz_xfer* out, int32_t cap);
+
+/* Caller-driven exchange (DZ_FLAG_EXTERNAL_EXCHANGE).  Under SP, dz_attend_chunk,
+ * dz_attend_spans and dz_append_kv enqueue their work up to the first all-to-all
+ * and return DZ_OK with the exchange pending; every other call except these two
+ * returns DZ_ESTATE until the operation completes.  dz_sp_pending copies up to cap
+ * transfers of the pending exchange (the dz_sp_plan entries of *phase, offsets
+ * into cache_storage) to out and returns their count (0 and *phase = -1 if none).
+ * The caller delivers them -- this rank's send block of entry (peer p, tensor t,
+ * k-th such entry) is the receive block of p's entry (peer = this rank, t, k-th) --
+ * ordered before the next work on `stream`, then calls dz_sp_resume, which
+ * enqueues the next stage on stream (attend: the attention, then after exchange 2
+ * the unpack; append: the commit).  Lets a caller use its own transport (and the
+ * tests run N ranks on one GPU with one device copy per transfer). */
+DZ_API int32_t dz_sp_pending(const dz_ctx* ctx, int32_t* phase, dz_xfer* out, int32_t cap);
+DZ_API dz_status dz_sp_resume(dz_ctx* ctx, void* stream);
 
 /* K5 (the post-exchange unpack) on its own, for tests: recv bf16
  * [world_size][batch][n_local][heads_local][head_dim] -> out bf16

@@ -34,6 +34,9 @@ FLAG_WRITE_LSE = 1
 FLAG_PROFILE = 2
 FLAG_ONLINE_SOFTMAX = 4
 FLAG_TILE_MAP = 8
+FLAG_EXTERNAL_EXCHANGE = 16
+FLAG_WHOLE_UNITS = 32
+FLAG_HOST_ONLY = 64
 
 STATUS = {0: "DZ_OK", -1: "DZ_EINVAL", -2: "DZ_ESHAPE", -3: "DZ_ECAPACITY", -4: "DZ_ESTATE",
           -5: "DZ_ECUDA", -6: "DZ_ENCCL", -7: "DZ_ERANGE"}
@@ -92,6 +95,8 @@ SIGNATURES = [
     ("dz_nccl_comm_destroy", I32, [P]),
     ("dz_attention_units", I32, [P, I32]),
     ("dz_sp_plan", I32, [P, I32, I32, ctypes.POINTER(DzXfer), I32]),
+    ("dz_sp_pending", I32, [P, ctypes.POINTER(I32), ctypes.POINTER(DzXfer), I32]),
+    ("dz_sp_resume", I32, [P, P]),
     ("dz_debug_sp_unpack", I32, [P, P, I32, I32, I32, I32, I32, P]),
     ("dz_debug_watchdog", I32, [P, I32]),
     ("dz_profile_last", I32, [P, P]),
@@ -216,7 +221,7 @@ class ChunkKVCache:
         cfg.cache_capacity_tokens, cfg.max_chunk_tokens = capacity, max_chunk
         cfg.window_slack_tokens = window_slack
         cfg.q_gain, cfg.k_gain = q_gain.data_ptr(), k_gain.data_ptr()
-        cfg.max_abs_gain = float(max(q_gain.abs().max().item(), k_gain.abs().max().item(), 1e-30))
+        cfg.max_abs_gain = 0.0   # dz_create reads the gains and derives the bound itself
         cfg.nccl_comm = nccl_comm or None
         cfg.world_size, cfg.rank, cfg.flags = world_size, rank, flags
         nbytes = L.dz_cache_bytes(ctypes.byref(cfg))
@@ -287,6 +292,22 @@ class ChunkKVCache:
         self._check(lib().dz_attend_spans(self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), pos.data_ptr(), arr,
                                           len(spans), out.data_ptr(), _stream_ptr(stream)), "dz_attend_spans")
         return out
+
+    # -- caller-driven exchange (FLAG_EXTERNAL_EXCHANGE) ------------------------
+    def sp_pending(self):
+        """(phase, [(peer, tensor, send_off, recv_off, bytes), ...]) of the exchange the last call
+        stopped at; phase -1 and [] if none (offsets are into ``self.storage``)."""
+        ph = I32()
+        cnt = lib().dz_sp_pending(self._ctx, ctypes.byref(ph), None, 0)
+        if cnt < 0:
+            raise DzError(cnt, "dz_sp_pending")
+        arr = (DzXfer * max(cnt, 1))()
+        lib().dz_sp_pending(self._ctx, ctypes.byref(ph), arr, cnt)
+        return ph.value, [(x.peer, x.tensor, x.send_off, x.recv_off, x.bytes) for x in arr[:cnt]]
+
+    def sp_resume(self, stream: Optional[torch.cuda.Stream] = None):
+        """Continue the suspended call after its pending transfers have been delivered."""
+        self._check(lib().dz_sp_resume(self._ctx, _stream_ptr(stream)), "dz_sp_resume")
 
     def commit_staged(self, chunk_id: int, stream: Optional[torch.cuda.Stream] = None):
         self._check(lib().dz_commit_staged(self._ctx, chunk_id, _stream_ptr(stream)), "dz_commit_staged")

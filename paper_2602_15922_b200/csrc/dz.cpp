@@ -156,6 +156,22 @@ struct dz_ctx {
   cudaEvent_t ev[5] = {}, ev_app[2] = {};
   bool have_attend_ev = false, have_append_ev = false;
   bool prof_on = true;  // dz_profile_enable: events are recorded only while on
+  bool external_x = false;  // DZ_FLAG_EXTERNAL_EXCHANGE: the caller runs the all-to-all transfers
+  bool host_only = false;   // DZ_FLAG_HOST_ONLY: planning context, never touches the device
+  float max_gain = 0.f;     // max |g| over q_gain and k_gain (read from the device at create)
+  // An operation suspended at an exchange point (DZ_FLAG_EXTERNAL_EXCHANGE): the caller runs
+  // `plan` (dz_sp_pending), then dz_sp_resume enqueues the rest.
+  struct Pending {
+    int op = 0;          // 0 none, 1 attend, 2 append
+    int phase = -1;      // exchange phase of `plan` (0 attend pre, 1 append pre, 2 attend post)
+    int64_t n = 0;
+    dz::SpanTable spans;
+    void* out = nullptr;
+    bool prof = false;
+    bool stage_chunk = false;  // attend_chunk: record the staged chunk when the call completes
+    int32_t chunk_id = 0, kind = 0;
+    std::vector<dz_xfer> plan;
+  } pend;
   std::string err;
 
   void* kslot(int b, int64_t slot) const {
@@ -244,6 +260,15 @@ std::vector<dz_xfer> make_plan(const dz_ctx* c, int phase, int64_t n) {
 dz_status check_ready(dz_ctx* c) {
   if (!c) return DZ_EINVAL;
   if (c->poisoned) return fail(c, DZ_ESTATE, "context poisoned by an earlier CUDA/NCCL error: %s", c->err.c_str());
+  if (c->pend.op != 0)
+    return fail(c, DZ_ESTATE, "exchange phase %d pending: run dz_sp_pending's transfers, then dz_sp_resume",
+                c->pend.phase);
+  return DZ_OK;
+}
+
+// a planning context (DZ_FLAG_HOST_ONLY) validates a compute call, then refuses to enqueue it
+dz_status check_device(dz_ctx* c) {
+  if (c->host_only) return fail(c, DZ_ESTATE, "host-only (planning) context: nothing is enqueued");
   return DZ_OK;
 }
 
@@ -262,6 +287,10 @@ dz_status check_span(dz_ctx* c, const dz_span* s) {
 // committed window down to slot 0 when it would run past the end.
 dz_status ensure_staging_room(dz_ctx* c, cudaStream_t st) {
   if (c->start + c->valid + c->cfg.max_chunk_tokens <= c->L.slots) return DZ_OK;
+  if (c->host_only) {  // a planning context holds no data: bookkeeping only
+    c->start = 0;
+    return DZ_OK;
+  }
   const size_t row = (size_t)c->Hl * c->D * 2;
   const int64_t s0 = c->start;
   for (int b = 0; b < c->B; ++b) {
@@ -293,7 +322,7 @@ void fill_prologue_common(dz_ctx* c, dz::PrologueArgs& a, const int32_t* pos, in
 // K1 prologue for the current chunk: Q' and the chunk's K'/V, written either
 // straight into the staging slot (N == 1) or into the all-to-all send layout.
 dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, const int32_t* pos, int64_t n,
-                       cudaStream_t st, bool cur_separate = false, bool wait_late = false) {
+                       cudaStream_t st, bool cur_separate = false) {
   const int64_t n_loc = n / c->N;
   dz::PrologueArgs a;
   fill_prologue_common(c, a, pos, n_loc);
@@ -326,9 +355,7 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
     // a fill recorded into a graph being captured has not run yet: fill again on the next eager call
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) c->rope_ready = true;
-    wait_late = false;
   }
-  a.wait_late = wait_late ? 1 : 0;
   return cuda_check(c, dz::launch_prologue(a, st), "prologue launch");
 }
 
@@ -394,8 +421,10 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   // stream-K needs <= 64 query groups and 32-bit step arithmetic (W * pairs < 2^31); else whole units round-robin
   const int step_keys = dz::attention_step_keys(c->m_static);
   const int64_t n_groups = (n + dz::kTileQ - 1) / dz::kTileQ, n_steps = (kv_len + step_keys - 1) / step_keys;
+  // DZ_FLAG_WHOLE_UNITS: every unit computed whole by one CTA pair, so a unit's result depends only on
+  // its rows and keys, not on the unit count (the same bits at every world size, reading A21)
   static const bool rr_forced = getenv("DZ_SCHED_RR") != nullptr;  // diagnostics: whole units round-robin
-  const bool streamk = !rr_forced && n_groups <= 64 &&
+  const bool streamk = !rr_forced && !(c->cfg.flags & DZ_FLAG_WHOLE_UNITS) && n_groups <= 64 &&
                        (int64_t)c->B * c->Hl * n_groups * n_steps * dz::kMaxPairs < (1ll << 31);
   a.ws = streamk ? reinterpret_cast<float*>(c->base + c->L.ws_off) : nullptr;
   a.ws_cnt = reinterpret_cast<int32_t*>(c->base + c->L.cnt_off);
@@ -440,9 +469,31 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   if ((reinterpret_cast<uintptr_t>(cfg->cache_storage) & (kAlign - 1)) || !aligned16(cfg->q_gain) ||
       !aligned16(cfg->k_gain))
     return DZ_EINVAL;
+  const bool host_only = (cfg->flags & DZ_FLAG_HOST_ONLY) != 0;
+  const bool external_x = (cfg->flags & DZ_FLAG_EXTERNAL_EXCHANGE) != 0;
+  if (cfg->world_size > 1 && !cfg->nccl_comm && !external_x) return DZ_EINVAL;  // SP needs a transport
+  // max |g| from the gains themselves (one synchronous read; create is never captured): it sets the
+  // fp16 range check and the fixed softmax base below, so it is not taken on the caller's word.
+  // A caller bound (max_abs_gain > 0) below the true maximum is rejected.
+  double gmax = 0.0;
+  if (host_only) {
+    gmax = cfg->max_abs_gain;  // a planning context never reads device memory
+  } else {
+    const size_t ne = (size_t)cfg->heads * cfg->head_dim;
+    std::vector<float> h(2 * ne);
+    if (cudaMemcpy(h.data(), cfg->q_gain, ne * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(h.data() + ne, cfg->k_gain, ne * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaGetLastError();  // (an invalid pointer is not a sticky error)
+      return DZ_EINVAL;
+    }
+    for (float g : h) {
+      if (!std::isfinite(g)) return DZ_ERANGE;
+      gmax = std::max(gmax, (double)std::fabs(g));
+    }
+    if (cfg->max_abs_gain > 0.f && (double)cfg->max_abs_gain < gmax) return DZ_ERANGE;  // under-reported bound
+  }
   // fp16 Q'/K' (reading A13): |x'_i| <= sqrt(D) * |g_i| after RMSNorm
-  if (!(cfg->max_abs_gain > 0.f) || std::sqrt((double)cfg->head_dim) * cfg->max_abs_gain >= 6.0e4) return DZ_ERANGE;
-  if (cfg->world_size > 1 && !cfg->nccl_comm) return DZ_EINVAL;
+  if (!(gmax > 0.0) || std::sqrt((double)cfg->head_dim) * gmax >= 6.0e4) return DZ_ERANGE;
   Layout L = make_layout(cfg);
   if (cfg->cache_bytes < L.total) return DZ_ECAPACITY;
 
@@ -461,8 +512,12 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   c->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : 1.0f / std::sqrt((float)cfg->head_dim);
   c->base = static_cast<char*>(cfg->cache_storage);
   c->comm = static_cast<ncclComm_t>(cfg->nccl_comm);
+  c->external_x = external_x;
+  c->host_only = host_only;
+  c->max_gain = (float)gmax;
   int dev = 0;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!host_only && cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
   // RoPE frequencies per pair j (fp64): axis slice [t | h | w], omega = theta^(-2i/d_a)
   int j = 0;
   for (int ax = 0; ax < 3; ++ax)
@@ -475,14 +530,13 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   c->pro.eps = c->eps;
   // RMSNorm gives ||q'|| <= sqrt(D) max|g|, ||k'|| <= sqrt(D) max|g| (RoPE keeps norms), so
   // |score| * log2e <= D * max|g|^2 * scale * log2e (+0.5% for the fp16 rounding of Q'/K').
-  // When that bound is small the kernel uses it as a fixed softmax base: every 2^(x - m)
-  // stays within (2^-80, 1], far from fp32/bf16 underflow, and no running max is needed.
+  // When that bound is <= 60 the kernel uses base 0 instead of a running row max: every
+  // p = 2^s lies in [2^-60, 2^60], normal in fp32 and bf16, and no running max is needed.
   {
-    const double bound = (double)cfg->head_dim * cfg->max_abs_gain * cfg->max_abs_gain * c->scale *
-                         1.4426950408889634 * 1.005;
+    const double bound = (double)cfg->head_dim * gmax * gmax * c->scale * 1.4426950408889634 * 1.005;
     c->m_static = (!(cfg->flags & DZ_FLAG_ONLINE_SOFTMAX) && bound <= 60.0) ? (float)std::max(bound, 1.0) : 0.f;  // > 0 selects the fixed base
   }
-  if (cfg->flags & DZ_FLAG_PROFILE) {
+  if ((cfg->flags & DZ_FLAG_PROFILE) && !host_only) {
     for (auto& e : c->ev)
       if (cudaEventCreate(&e) != cudaSuccess) e = nullptr;
     for (auto& e : c->ev_app)
@@ -491,6 +545,34 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   *out = c;
   return DZ_OK;
 }
+
+}  // extern "C"
+
+namespace {
+
+// The append's commit (bookkeeping) once its K'/V are in the slots.
+dz_status append_commit(dz_ctx* c, int32_t chunk_id, int64_t n, bool prof, cudaStream_t st) {
+  if (prof) cudaEventRecord(c->ev_app[1], st);
+  c->have_append_ev = prof;
+  c->valid += n;
+  c->chunks.emplace_back(chunk_id, n);
+  c->last_id = chunk_id;
+  c->staged = false;
+  return ensure_staging_room(c, st);
+}
+
+// Suspend the current operation at an exchange point: the caller runs `phase`'s plan, then
+// dz_sp_resume continues (DZ_FLAG_EXTERNAL_EXCHANGE).
+void suspend(dz_ctx* c, int op, int phase, int64_t n) {
+  c->pend.op = op;
+  c->pend.phase = phase;
+  c->pend.n = n;
+  c->pend.plan = make_plan(c, phase, n);
+}
+
+}  // namespace
+
+extern "C" {
 
 dz_status dz_append_kv(dz_ctx* c, const void* k_raw, const void* v_raw, const dz_span* s, void* stream) {
   dz_status r = check_ready(c);
@@ -501,33 +583,78 @@ dz_status dz_append_kv(dz_ctx* c, const void* k_raw, const void* v_raw, const dz
   if (c->valid + s->n_tokens > c->cfg.cache_capacity_tokens)
     return fail(c, DZ_ECAPACITY, "cache full: %lld + %d > %lld", (long long)c->valid, s->n_tokens,
                 (long long)c->cfg.cache_capacity_tokens);
+  if ((r = check_device(c))) return r;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool prof = c->ev_app[0] != nullptr && c->prof_on;
   if (prof) cudaEventRecord(c->ev_app[0], st);
-  // With one GPU the append writes slots [valid, valid + n) that an attention still in flight on
-  // this stream only reads if it staged its new tokens there: otherwise K4 starts without waiting
-  // for its predecessor (it can run in the attention's tail) and waits before it completes.
-  const bool wait_late = c->N == 1 && !c->staging_read;
-  if ((r = run_prologue(c, nullptr, k_raw, v_raw, s->pos_thw, s->n_tokens, st, false, wait_late))) return r;
+  // K4 waits for its predecessor on the stream before it reads k_raw / v_raw / positions (that
+  // predecessor may be the kernel that produced them); it may still be scheduled early (PDL).
+  if ((r = run_prologue(c, nullptr, k_raw, v_raw, s->pos_thw, s->n_tokens, st, false))) return r;
   c->staging_read = false;
-  if (c->N > 1 && (r = exchange_pre(c, false, s->n_tokens, st))) return r;
-  if (prof) cudaEventRecord(c->ev_app[1], st);
-  c->have_append_ev = prof;
-  c->valid += s->n_tokens;
-  c->chunks.emplace_back(s->chunk_id, (int64_t)s->n_tokens);
-  c->last_id = s->chunk_id;
-  c->staged = false;
-  return ensure_staging_room(c, st);
+  if (c->N > 1) {
+    if (c->external_x) {
+      suspend(c, 2, 1, s->n_tokens);
+      c->pend.prof = prof;
+      c->pend.chunk_id = s->chunk_id;
+      return DZ_OK;
+    }
+    if ((r = exchange_pre(c, false, s->n_tokens, st))) return r;
+  }
+  return append_commit(c, s->chunk_id, s->n_tokens, prof, st);
 }
 
 }  // extern "C"
 
 namespace {
 
+// Stages of one attention call under SP: [prologue] -> exchange 0 -> [attention] -> exchange 2 ->
+// [unpack].  With DZ_FLAG_EXTERNAL_EXCHANGE the call stops at each exchange and dz_sp_resume
+// runs the next stage.
+void attend_mark(dz_ctx* c, bool prof, int i, cudaStream_t st) {
+  if (prof) cudaEventRecord(c->ev[i], st);
+}
+
+void attend_done(dz_ctx* c, bool prof, bool stage_chunk, int32_t chunk_id, int32_t kind, int64_t n) {
+  c->have_attend_ev = prof;
+  if (stage_chunk) {
+    c->staged = true;
+    c->staged_id = chunk_id;
+    c->staged_kind = kind;
+    c->staged_n = n;
+  }
+}
+
+dz_status attend_unpack(dz_ctx* c, int64_t n, void* out, bool prof, cudaStream_t st) {
+  dz_status r = cuda_check(c, dz::launch_sp_unpack(c->base + c->L.or_off, out, c->N, c->B, (int32_t)(n / c->N), c->Hl,
+                                                   c->D, st),
+                           "unpack launch");
+  if (r) return r;
+  attend_mark(c, prof, 4, st);
+  return DZ_OK;
+}
+
+// SP: K2 on this rank's heads over the full sequence, into the local O buffer; then exchange 2.
+dz_status attend_sp_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* out, bool prof,
+                              cudaStream_t st) {
+  attend_mark(c, prof, 2, st);
+  dz_status r = run_attention(c, n, spans, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, nullptr,
+                              nullptr, st);
+  if (r) return r;
+  attend_mark(c, prof, 3, st);
+  if (c->external_x) {
+    suspend(c, 1, 2, n);
+    c->pend.out = out;
+    return DZ_OK;
+  }
+  if ((r = exchange_post(c, n, st))) return r;
+  return attend_unpack(c, n, out, prof, st);
+}
+
 // One attention call (K1 prologue [+ exchange] + K2 [+ exchange + unpack]) over
 // n new tokens described by `spans`; keys = committed chunks + the new tokens.
 dz_status attend_impl(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const int32_t* pos,
-                      int64_t n, const dz::SpanTable& spans, void* out, bool may_commit, cudaStream_t st) {
+                      int64_t n, const dz::SpanTable& spans, void* out, bool may_commit, int32_t chunk_id,
+                      int32_t kind, cudaStream_t st) {
   dz_status r;
   c->staged = false;
   // The new tokens' K'/V are only staged after the committed slots when the chunk may be committed
@@ -537,31 +664,33 @@ dz_status attend_impl(dz_ctx* c, const void* q_raw, const void* k_raw, const voi
   const bool cur_sep = c->N == 1 && !may_commit && c->valid % dz::attention_step_keys(c->m_static) == 0;
   c->staging_read = !cur_sep;
   const bool prof = c->ev[0] != nullptr && c->prof_on;
-  auto mark = [&](int i) { if (prof) cudaEventRecord(c->ev[i], st); };
-  mark(0);
+  const bool stage_chunk = chunk_id >= 0;
+  attend_mark(c, prof, 0, st);
   if ((r = run_prologue(c, q_raw, k_raw, cur_sep ? nullptr : v_raw, pos, n, st, cur_sep))) return r;
-  mark(1);
+  attend_mark(c, prof, 1, st);
   if (c->N == 1) {
-    mark(2);
+    attend_mark(c, prof, 2, st);
     if ((r = run_attention(c, n, spans, out, n * c->H * c->D, (int64_t)c->H * c->D,
                            cur_sep ? c->base + c->L.kc_off : nullptr, cur_sep ? v_raw : nullptr, st)))
       return r;
-    mark(3);
-  } else {
-    if ((r = exchange_pre(c, true, n, st))) return r;
-    mark(2);
-    if ((r = run_attention(c, n, spans, c->base + c->L.ol_off, n * c->Hl * c->D, (int64_t)c->Hl * c->D, nullptr,
-                           nullptr, st)))
-      return r;
-    mark(3);
-    if ((r = exchange_post(c, n, st))) return r;
-    if ((r = cuda_check(c, dz::launch_sp_unpack(c->base + c->L.or_off, out, c->N, c->B, (int32_t)(n / c->N), c->Hl,
-                                                c->D, st),
-                        "unpack launch")))
-      return r;
+    attend_mark(c, prof, 3, st);
+    attend_mark(c, prof, 4, st);
+    attend_done(c, prof, stage_chunk, chunk_id, kind, n);
+    return DZ_OK;
   }
-  mark(4);
-  c->have_attend_ev = prof;
+  if (c->external_x) {
+    suspend(c, 1, 0, n);
+    c->pend.spans = spans;
+    c->pend.out = out;
+    c->pend.prof = prof;
+    c->pend.stage_chunk = stage_chunk;
+    c->pend.chunk_id = chunk_id;
+    c->pend.kind = kind;
+    return DZ_OK;
+  }
+  if ((r = exchange_pre(c, true, n, st))) return r;
+  if ((r = attend_sp_attention(c, n, spans, out, prof, st))) return r;
+  attend_done(c, prof, stage_chunk, chunk_id, kind, n);
   return DZ_OK;
 }
 
@@ -590,17 +719,12 @@ dz_status dz_attend_chunk(dz_ctx* c, const void* q_raw, const void* k_raw, const
   if (r) return r;
   if ((r = check_attend_ptrs(c, q_raw, k_raw, v_raw, out))) return r;
   if ((r = check_span(c, s))) return r;
+  if ((r = check_device(c))) return r;
   dz::SpanTable t;
   t.n = 1;
   set_span(t, 0, s->chunk_id, s->kind, 0, s->n_tokens);
-  if ((r = attend_impl(c, q_raw, k_raw, v_raw, s->pos_thw, s->n_tokens, t, out, s->kind == DZ_CLEAN,
-                       static_cast<cudaStream_t>(stream))))
-    return r;
-  c->staged = true;
-  c->staged_id = s->chunk_id;
-  c->staged_kind = s->kind;
-  c->staged_n = s->n_tokens;
-  return DZ_OK;
+  return attend_impl(c, q_raw, k_raw, v_raw, s->pos_thw, s->n_tokens, t, out, s->kind == DZ_CLEAN, s->chunk_id,
+                     s->kind, static_cast<cudaStream_t>(stream));
 }
 
 dz_status dz_attend_spans(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const int32_t* pos_thw,
@@ -634,7 +758,42 @@ dz_status dz_attend_spans(dz_ctx* c, const void* q_raw, const void* k_raw, const
       return fail(c, DZ_ESHAPE, "span layout of %lld query groups x key steps exceeds %d tiles", (long long)tiles,
                   dz::kMaxStepTiles);
   }
-  return attend_impl(c, q_raw, k_raw, v_raw, pos_thw, n, t, out, false, static_cast<cudaStream_t>(stream));
+  if ((r = check_device(c))) return r;
+  return attend_impl(c, q_raw, k_raw, v_raw, pos_thw, n, t, out, false, -1, 0, static_cast<cudaStream_t>(stream));
+}
+
+int32_t dz_sp_pending(const dz_ctx* c, int32_t* phase, dz_xfer* out, int32_t cap) {
+  if (!c || cap < 0) return DZ_EINVAL;
+  if (phase) *phase = c->pend.op ? c->pend.phase : -1;
+  if (!c->pend.op) return 0;
+  if (out)
+    for (int32_t i = 0; i < (int32_t)c->pend.plan.size() && i < cap; ++i) out[i] = c->pend.plan[i];
+  return (int32_t)c->pend.plan.size();
+}
+
+dz_status dz_sp_resume(dz_ctx* c, void* stream) {
+  if (!c) return DZ_EINVAL;
+  if (c->poisoned) return fail(c, DZ_ESTATE, "context poisoned by an earlier CUDA/NCCL error: %s", c->err.c_str());
+  if (!c->pend.op) return fail(c, DZ_ESTATE, "no exchange pending");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  dz_ctx::Pending p = c->pend;
+  c->pend = dz_ctx::Pending();
+  dz_status r = DZ_OK;
+  if (p.op == 2) return append_commit(c, p.chunk_id, p.n, p.prof, st);  // append: K'/V have landed
+  if (p.phase == 0) {  // attend: Q', K', V have landed -> attention (stops again at exchange 2)
+    if ((r = attend_sp_attention(c, p.n, p.spans, p.out, p.prof, st))) return r;
+    if (c->pend.op) {  // carry the call's finalisation to the last stage
+      c->pend.prof = p.prof;
+      c->pend.stage_chunk = p.stage_chunk;
+      c->pend.chunk_id = p.chunk_id;
+      c->pend.kind = p.kind;
+      return DZ_OK;
+    }
+  } else if ((r = attend_unpack(c, p.n, p.out, p.prof, st))) {  // phase 2: O has landed
+    return r;
+  }
+  attend_done(c, p.prof, p.stage_chunk, p.chunk_id, p.kind, p.n);
+  return DZ_OK;
 }
 
 dz_status dz_commit_staged(dz_ctx* c, int32_t chunk_id, void* stream) {
@@ -686,6 +845,7 @@ dz_status dz_copy_lse(dz_ctx* c, float* dst, size_t elems, void* stream) {
   dz_status r = check_ready(c);
   if (r) return r;
   if (!(c->cfg.flags & DZ_FLAG_WRITE_LSE)) return fail(c, DZ_ESTATE, "created without DZ_FLAG_WRITE_LSE");
+  if ((r = check_device(c))) return r;
   const size_t need = (size_t)c->B * c->Hl * c->last_nq;
   if (!dst || elems < need) return fail(c, DZ_EINVAL, "lse buffer too small (%zu < %zu)", elems, need);
   return cuda_check(c, cudaMemcpyAsync(dst, c->base + c->L.lse_off, need * 4, cudaMemcpyDeviceToDevice,

@@ -45,9 +45,6 @@ struct PrologueArgs {
   int32_t B = 0, n = 0, H = 0, D = 0, heads_per_dest = 0;
   float eps = 1e-6f;
   float q_scale = 1.f;                             // extra factor on Q' (softmax_scale * log2e)
-  int32_t wait_late = 0;                           // 1: griddepcontrol.wait at the end, not the start
-                                                   // (the writes cannot conflict with an in-flight
-                                                   // predecessor; see dz_append_kv)
   const float2* rope_tab = nullptr;                // [rope_len][D/2] (cos, sin) of p * omega_j, or null
   int32_t rope_len = 0;                            // positions 0 .. rope_len-1 tabulated (others computed)
   double omega[kMaxHeadDim / 2];                   // per pair j: theta^(-2i/d_a), fp64 (host)

@@ -142,7 +142,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
     cs[(k % L.S) * (D / 2) + ai] = make_float2((float)cn, (float)sn);
   };
   __syncthreads();  // barriers initialised, row offsets visible
-  if (!a.wait_late) ptx::pdl_wait();  // the previous kernel of the stream (e.g. the last attention) is done
+  // the previous kernel of the stream is done and its writes are visible before any input is read:
+  // that kernel may be the one that produced q/k/v or the positions
+  ptx::pdl_wait();
   if (tid == 0)
     for (int k = 0; k < L.S - 1; ++k) issue(k);
   // gains of this thread's heads (h = g + kGroups * i) and column slice, kept in registers
@@ -244,7 +246,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
     angles(k + 1, pos_k1);  // next item's angles into its own slot, off the critical path of the copies
     __syncthreads();  // stage and angles of item k may be refilled
   }
-  if (a.wait_late) ptx::pdl_wait();  // complete only after the previous kernel (ordering stays transitive)
 }
 
 // ---- token loop: registers instead of a ring --------------------------------------------
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
       c[e] = (unsigned)p[e] < (unsigned)a.rope_len ? __ldg(a.rope_tab + (size_t)p[e] * (D / 2) + li * 4 + e)
                                                    : rope_cs(p[e], a.omega[li * 4 + e]);
   };
-  if (!a.wait_late) ptx::pdl_wait();
+  ptx::pdl_wait();  // before the first read of an input (its producer may be the previous kernel)
   uint4 v[3][kPer], vn[3][kPer];
   float2 csr[4], csn[4];
   int pn[4] = {0, 0, 0, 0};
@@ -379,7 +380,6 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
 #pragma unroll
     for (int e = 0; e < 4; ++e) csr[e] = csn[e];
   }
-  if (a.wait_late) ptx::pdl_wait();
 }
 
 template <int D>

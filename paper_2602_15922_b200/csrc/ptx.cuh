@@ -60,21 +60,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Watchdog record (see dz_debug_watchdog): a wait that exceeds the time limit
-// records {block, warp, barrier smem address, parity, SM} and sets the abort
-// flag; from then on every wait returns at once, so the kernel drains with
-// garbage instead of hanging or trapping the GPU.
-static __device__ uint32_t g_dz_watchdog[8];  // one copy per translation unit (attention.cu)
+// Bounded waits.  A wait that exceeds 5 s records {1, block, warp, barrier smem address, parity,
+// SM} in this translation unit's g_dz_watchdog and then traps: the launch fails with a CUDA
+// error that surfaces at the caller's next sync, and the library's next call on the stream
+// returns DZ_ECUDA and poisons its context -- a hang never turns into silent garbage.  The
+// diagnostics build (-DDZ_TRACE, libdz_trace.so) instead lets every later wait return at once so
+// the kernel drains and dz_debug_watchdog can read the record (results are then garbage).
+static __device__ uint32_t g_dz_watchdog[8];  // one copy per translation unit; dz_debug_watchdog reads attention.cu's
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-#ifndef DZ_NO_WATCHDOG
   if (mbar_try_wait(bar, parity)) return;
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   uint32_t polls = 0;
   while (!mbar_try_wait(bar, parity)) {
     if ((++polls & 1023u) == 0) {
+#ifdef DZ_TRACE
       if (*((volatile uint32_t*)&g_dz_watchdog[0]) != 0) return;
+#endif
       uint64_t t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       if (t1 - t0 > 5000000000ull) {
@@ -88,14 +91,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
           g_dz_watchdog[5] = smid;
           __threadfence();
         }
+#ifdef DZ_TRACE
         return;
+#else
+        __trap();
+#endif
       }
     }
   }
-#else
-  while (!mbar_try_wait(bar, parity)) {
-  }
-#endif
 }
 
 // ------------------------------------------------------------ clusters (2-CTA) --

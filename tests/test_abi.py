@@ -49,6 +49,7 @@ def _cfg(**kw):
     c.q_gain = c.k_gain = 0x10000
     c.max_abs_gain = 1.5
     c.world_size, c.rank = 1, 0
+    c.flags = dz.FLAG_HOST_ONLY   # placeholder device pointers: the context never dereferences them
     for k, v in kw.items():
         setattr(c, k, v)
     return c
@@ -128,3 +129,37 @@ def test_call_validation_before_enqueue():
 def test_status_strings():
     for s in range(-7, 1):
         assert dz.status_string(s).startswith("DZ_")
+
+
+def test_host_only_context_validates_then_refuses_to_enqueue():
+    L = dz.lib()
+    c = _cfg()
+    c.cache_storage = 0x100000
+    c.cache_bytes = L.dz_cache_bytes(ctypes.byref(c))
+    ctx = ctypes.c_void_p()
+    assert L.dz_create(ctypes.byref(c), ctypes.byref(ctx)) == 0
+    try:
+        span = dz.DzSpan(0, dz.NOISY, 128, 0x200000)
+        assert L.dz_attend_chunk(ctx, 0x300000, 0x300000, 0x300000, ctypes.byref(span), 0x300000, None) == -4
+        assert b"host-only" in L.dz_last_error(ctx)
+        clean = dz.DzSpan(0, dz.CLEAN, 128, 0x200000)
+        assert L.dz_append_kv(ctx, 0x300000, 0x300000, ctypes.byref(clean), None) == -4
+        assert L.dz_cache_state(ctx, None, None, None) == 0
+        # nothing pending: dz_sp_pending lists no transfer, dz_sp_resume has nothing to resume
+        ph = ctypes.c_int32()
+        assert L.dz_sp_pending(ctx, ctypes.byref(ph), None, 0) == 0 and ph.value == -1
+        assert L.dz_sp_resume(ctx, None) == -4
+    finally:
+        L.dz_destroy(ctx)
+
+
+def test_external_exchange_allows_sp_without_nccl():
+    L = dz.lib()
+    c = _cfg(world_size=2, rank=1)
+    c.flags |= dz.FLAG_EXTERNAL_EXCHANGE
+    c.cache_storage = 0x100000
+    c.cache_bytes = L.dz_cache_bytes(ctypes.byref(c))
+    ctx = ctypes.c_void_p()
+    assert L.dz_create(ctypes.byref(c), ctypes.byref(ctx)) == 0
+    assert L.dz_sp_plan(ctx, 0, 128, None, 0) == 3 * 2
+    L.dz_destroy(ctx)

@@ -325,3 +325,131 @@ def test_sp_unpack_kernel(N, B, nl, Hl, D):
     torch.cuda.synchronize()
     want = recv.permute(1, 2, 0, 3, 4).reshape(B, nl, N * Hl, D)
     assert torch.equal(out, want)
+
+
+# ------------------------------------------------------------- boundary hardening --
+def _raw_create(gq, gk, max_abs_gain, flags=0):
+    import ctypes
+    import paper_2602_15922_b200 as dz
+    L = dz.lib()
+    c = dz.DzConfig()
+    c.batch, c.heads, c.head_dim = 1, gq.shape[0], gq.shape[1]
+    for i, d in enumerate((44, 42, 42)):
+        c.rope_dims[i] = d
+    c.cache_capacity_tokens, c.max_chunk_tokens = 256, 256
+    c.q_gain, c.k_gain = gq.data_ptr(), gk.data_ptr()
+    c.max_abs_gain = max_abs_gain
+    c.world_size, c.rank, c.flags = 1, 0, flags
+    nbytes = L.dz_cache_bytes(ctypes.byref(c))
+    store = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    c.cache_storage, c.cache_bytes = store.data_ptr(), nbytes
+    ctx = ctypes.c_void_p()
+    s = L.dz_create(ctypes.byref(c), ctypes.byref(ctx))
+    if s == 0:
+        L.dz_destroy(ctx)
+    return s
+
+
+def test_create_reads_gains_and_rejects_underreported_bound():
+    # dz_create takes max|g| from the device gains (the fixed softmax base depends on it);
+    # a caller bound below it, or a non-finite gain, is rejected with DZ_ERANGE
+    gq = (torch.rand(4, 128) + 0.5).cuda()
+    gk = (torch.rand(4, 128) + 0.5).cuda()
+    true_max = float(max(gq.abs().max(), gk.abs().max()))
+    assert _raw_create(gq, gk, 0.0) == 0
+    assert _raw_create(gq, gk, true_max) == 0
+    assert _raw_create(gq, gk, 0.5 * true_max) == -7
+    bad = gk.clone()
+    bad[2, 5] = float("nan")
+    assert _raw_create(gq, bad, 0.0) == -7
+    big = gk.clone()
+    big[0, 0] = 1e4            # sqrt(128) * 1e4 overflows fp16 Q'/K'
+    assert _raw_create(gq, big, 0.0) == -7
+
+
+def test_lse_against_oracle():
+    # DZ_FLAG_WRITE_LSE: the per-row natural-log LSE of the last attend vs the oracle's.  |dLSE| <=
+    # max_j |ds_j| (dLSE = sum_j p_j ds_j); the fp16 rounding of Q' and K' bounds |ds| by
+    # 2^-10 * ||q'|| ||k'|| * scale <= 2^-10 * D * max|g_q| max|g_k| * scale (+ fp32 sums, exp2 error)
+    import paper_2602_15922_b200 as dz
+    w = synth.scaled(synth.workload("C1"), heads=4, cached_chunks=2)
+    run = GpuRun(w, flags=dz.FLAG_WRITE_LSE)
+    run.fill()
+    run.attend()
+    got = run.cache.lse(w.chunk_tokens)[0].cpu().double().numpy()      # [H][n]
+    s = run.streams[0]
+    _, want = oracle.attend_chunk(run.gq, run.gk, s.cache_k, s.cache_v, s.cache_pos, s.cur_q[0], s.cur_k[0],
+                                  s.cur_v[0], s.cur_pos, w.rope_dims, with_lse=True)   # [n][H]
+    bound = 2.0 ** -10 * w.head_dim * float(run.gq.abs().max() * run.gk.abs().max()) * w.head_dim ** -0.5 + 1e-4
+    err = np.abs(got.T - want)
+    assert np.all(np.isfinite(got)) and err.max() <= bound, (err.max(), bound)
+    assert err.mean() < 0.1 * bound
+
+
+def test_lse_online_path_against_oracle():
+    import paper_2602_15922_b200 as dz
+    w = synth.scaled(synth.workload("C1"), heads=2, cached_chunks=1)
+    run = GpuRun(w, flags=dz.FLAG_WRITE_LSE | dz.FLAG_ONLINE_SOFTMAX)
+    run.fill()
+    run.attend()
+    got = run.cache.lse(w.chunk_tokens)[0].cpu().double().numpy()
+    s = run.streams[0]
+    _, want = oracle.attend_chunk(run.gq, run.gk, s.cache_k, s.cache_v, s.cache_pos, s.cur_q[0], s.cur_k[0],
+                                  s.cur_v[0], s.cur_pos, w.rope_dims, with_lse=True)
+    bound = 2.0 ** -10 * w.head_dim * float(run.gq.abs().max() * run.gk.abs().max()) * w.head_dim ** -0.5 + 1e-4
+    assert np.abs(got.T - want).max() <= bound
+
+
+def test_compaction_without_slack_equals_fresh_cache():
+    # slack 0: the append after an eviction runs past the slot range, so the committed window is
+    # compacted to slot 0 (device copies in pieces); the next attention equals a fresh cache's
+    w = _small(heads=4, cached_chunks=2)
+    n = w.chunk_tokens
+    run = GpuRun(w, capacity=2 * n, slack=0)
+    run.fill()
+    C = w.cached_chunks
+    q, k, v = synth.draw_qkv(w, 0, C)
+    pos = synth.chunk_positions(w, C).to(run.dev)
+    run.cache.attend(q[None].to(run.dev), k[None].to(run.dev), v[None].to(run.dev), pos, C)
+    run.cache.evict_front(1)
+    run.cache.append(k[None].to(run.dev), v[None].to(run.dev), pos, C)       # -> compaction
+    q2, k2, v2 = synth.draw_qkv(w, 0, C + 1)
+    pos2 = synth.chunk_positions(w, C + 1).to(run.dev)
+    got = run.cache.attend(q2[None].to(run.dev), k2[None].to(run.dev), v2[None].to(run.dev), pos2, C + 1)
+    fresh = GpuRun(w, capacity=2 * n)
+    s0 = fresh.streams[0]
+    fresh.cache.append(s0.cache_k[1][None].to(fresh.dev), s0.cache_v[1][None].to(fresh.dev),
+                       s0.cache_pos[1].to(fresh.dev), 1)
+    fresh.cache.append(k[None].to(fresh.dev), v[None].to(fresh.dev), pos, C)
+    want = fresh.cache.attend(q2[None].to(fresh.dev), k2[None].to(fresh.dev), v2[None].to(fresh.dev), pos2, C + 1)
+    torch.cuda.synchronize()
+    kc, vc = run.cache.cache_view(0)
+    kf, vf = fresh.cache.cache_view(0)
+    assert torch.equal(kc, kf) and torch.equal(vc, vf), "compacted cache differs"
+    assert torch.equal(got, want)
+
+
+def test_append_reads_inputs_after_their_producer():
+    # the append kernel may be scheduled while the previous kernel drains (PDL), but must read its
+    # inputs only after that kernel completes.  Here the producer of the appended k is the
+    # attention kernel itself (it triggers its dependents at its start and writes `out`):
+    # append(out) right behind attend(...) -> out must commit exactly what a synchronised append
+    # of the finished `out` commits.
+    w = _small(heads=4, cached_chunks=2)
+    n, C = w.chunk_tokens, w.cached_chunks
+    run = GpuRun(w, capacity=3 * n)
+    run.fill()
+    s0 = run.streams[0]
+    pos = s0.cur_pos.to(run.dev)
+    v = run.stack("cur_v", 0)
+    out = run.attend()
+    run.cache.append(out, v, pos, C)
+    torch.cuda.synchronize()
+    ref = GpuRun(w, capacity=3 * n)
+    ref.fill()
+    torch.cuda.synchronize()
+    ref.cache.append(out.clone(), v, pos, C)
+    torch.cuda.synchronize()
+    kc, vc = run.cache.cache_view(0)
+    kr, vr = ref.cache.cache_view(0)
+    assert torch.equal(kc, kr) and torch.equal(vc, vr)

@@ -39,6 +39,7 @@ def _ctx(world, rank, B, H, D, n, capacity, rope):
     c.q_gain = c.k_gain = FAKE_STORAGE
     c.max_abs_gain = 1.0
     c.world_size, c.rank, c.nccl_comm = world, rank, FAKE_COMM
+    c.flags = dz.FLAG_HOST_ONLY   # planning context: placeholder pointers, nothing dereferenced
     nbytes = L.dz_cache_bytes(ctypes.byref(c))
     assert nbytes > 0
     c.cache_storage, c.cache_bytes = FAKE_STORAGE, nbytes
