@@ -18,14 +18,19 @@ Useful FLOP counts only the attention.  Inputs are resident in HBM before
 the timed region; the L2 is flushed (a 512 MB write) before every timed step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dz|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...    (Ulysses SP, C4)
+    torchrun --nproc-per-node N bench.py --gpus N ...
+        C4 (default under torchrun): Ulysses SP, 40/N heads per rank, NCCL all-to-all;
+        --workload C3 at N=2: the CFG split (one batch element per GPU, no collective).
 
 Prints one JSON line (rank 0).  ``--impl reference`` times the fp64 CPU
 oracle (the tier's reference arm) on a bounded sample of the same workload.
+At N=1 the line also carries secondary workloads (C2, C4 on one GPU, C3 as
+4 graph-replayed denoising steps, Fig. 10(a) teacher forcing), each timed here.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -42,9 +47,10 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 
 METRIC = "block-causal chunk-attn TFLOP/s and % bf16 TC peak at 1/2/4/8 B200"
+TOL_MAX_ABS, TOL_REL_FRO = 2e-2, 5e-3     # BASELINE.json north_star
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -54,6 +60,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the secondary workloads (N=1)")
+    ap.add_argument("--secondary-steps", type=int, default=20)
     ap.add_argument("--no-flush", action="store_true", help="warm L2 (secondary measurement)")
     ap.add_argument("--tf-chunks", type=int, default=4, help="tf mode: M clean + M noisy chunks")
     ap.add_argument("--mode", choices=["chunk", "denoise", "tf"], default="chunk",
@@ -67,7 +75,7 @@ def parse():
     ap.add_argument("--online", action="store_true", help="force the online-softmax (running max) kernel")
     ap.add_argument("--flush-read", action="store_true",
                     help="after the 512 MB flush write, read 256 MB of it so no dirty flush lines stay in L2")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def visible_pairs(spans) -> int:
@@ -84,6 +92,15 @@ def visible_pairs(spans) -> int:
     return total
 
 
+def pct(xs, q):
+    """q-th percentile (0..100) of a list, linear interpolation."""
+    return float(np.percentile(np.asarray(xs, dtype=np.float64), q))
+
+
+def spread(xs):
+    return {"median": pct(xs, 50), "p10": pct(xs, 10), "p90": pct(xs, 90), "mean": float(np.mean(xs)), "n": len(xs)}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -92,15 +109,37 @@ def peaks():
     return 1590.0, 1400.0, 6650.0, "fallback"   # B200_PROFILING.md fallback figures
 
 
+def lib_sha():
+    import paper_2602_15922_b200 as dz
+    h = hashlib.sha256()
+    with open(dz.LIB_PATH, "rb") as f:
+        h.update(f.read())
+    return h.hexdigest()[:16]
+
+
+def stamped_traffic(workload: str):
+    """DRAM bytes per K2 launch from the committed ncu capture, only if it was taken on this very
+    library build (sha of libdz.so stamped into the file) and workload; else None."""
+    tp = os.path.join(ROOT, "profiles", "ncu_attention_traffic.json")
+    if not os.path.exists(tp):
+        return None, "no capture"
+    d = json.load(open(tp))
+    if d.get("workload") != workload:
+        return None, f"capture is of {d.get('workload')}"
+    if d.get("lib_sha16") != lib_sha():
+        return None, f"capture of another build ({d.get('lib_sha16')})"
+    return d.get("dram_bytes_per_launch"), d.get("source")
+
+
 class ClockSampler:
-    """NVML SM clock + clock-event reasons sampled during the timed region."""
+    """NVML SM clock + clock-event reasons sampled during the timed region (every 1 ms)."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
     def __init__(self, index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.power, self.reasons, self.max_mhz = [], [], set(), None
         self._stop = threading.Event()
         try:
             import pynvml
@@ -111,20 +150,25 @@ class ClockSampler:
         except Exception as e:  # pragma: no cover
             self.nv, self.err = None, str(e)
 
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.005)
+            self._sample()
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.nv:
+            self._sample()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
@@ -133,11 +177,14 @@ class ClockSampler:
         self._stop.set()
         if self.nv:
             self.t.join()
+            self._sample()
 
     def summary(self):
         if not self.nv:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "sm_mhz_min": min(self.samples) if self.samples else None,
+                "power_w_max": max(self.power) if self.power else None,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
@@ -145,12 +192,14 @@ class ClockSampler:
 _STREAMS = {}
 
 
-def oracle_sample(w: synth.Workload, heads=(0, 1), q_rows=None):
-    """Run the fp64 oracle (as it stands) on heads [h0, h1) and optional query rows; return (FLOP, seconds)."""
+def oracle_sample(w: synth.Workload, heads=(0, 1), q_rows=None, b=0):
+    """Run the fp64 oracle (as it stands) on heads [h0, h1) and optional query rows of batch
+    element b; return (FLOP, seconds, output [nq, h1-h0, D])."""
     import oracle
-    if w.name not in _STREAMS:          # draw once; samples slice heads out of the full draw
-        _STREAMS[w.name] = synth.draw_stream(w, 0, steps=1)
-    full = _STREAMS[w.name]
+    key = (w.name, b)
+    if key not in _STREAMS:          # draw once; samples slice heads out of the full draw
+        _STREAMS[key] = synth.draw_stream(w, b, steps=1)
+    full = _STREAMS[key]
     h0, h1 = heads
     hs = lambda x: x[:, h0:h1].contiguous()
     s = synth.ChunkStream([hs(k) for k in full.cache_k], [hs(v) for v in full.cache_v], full.cache_pos,
@@ -172,24 +221,42 @@ def oracle_sample(w: synth.Workload, heads=(0, 1), q_rows=None):
     kt = oracle.chunk_tags(list(range(C)) + [C], [oracle.CLEAN] * C + [oracle.NOISY],
                            [k.shape[0] for k in ks])
     qt = (np.full(nq, C, np.int32), np.full(nq, oracle.NOISY, np.int32), np.full(nq, C, np.int32))
-    oracle.attention(qn, np.concatenate(ks), np.concatenate(vs), qt, kt)
+    out = oracle.attention(qn, np.concatenate(ks), np.concatenate(vs), qt, kt)
     dt = time.perf_counter() - t0
     flop = 4.0 * w.head_dim * (h1 - h0) * nq * w.kv_tokens
-    return flop, dt
+    return flop, dt, out
 
 
-def cpu_baseline(w: synth.Workload, budget_s: float):
+def cpu_baseline(w: synth.Workload, budget_s: float, gpu_first=None):
+    """The oracle timed on the host cores on single-head passes of the workload.  Its first two
+    passes (heads 0 and H-1) are also the bench's parity check: the GPU output of the same
+    attention (gpu_first, [n, H, D] of batch element 0, computed before the timed region)
+    against the oracle within BASELINE.json's tolerance."""
     import oracle
     flop = secs = 0.0
     reps = 0
-    h = 0
-    while secs < budget_s or reps == 0:
-        f, d = oracle_sample(w, heads=(h % w.heads, h % w.heads + 1))
-        flop, secs, reps, h = flop + f, secs + d, reps + 1, h + 1
-    return {"value": flop / secs / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{w.name}: {reps} single-head passes (head i mod {w.heads}, all {w.chunk_tokens} queries x "
-                      f"{w.kv_tokens} keys incl. the cache prologue), fp64, {secs:.1f} s",
-            "cpu_model": _cpu_model()}
+    heads = [0, w.heads - 1] + [h for h in range(1, w.heads - 1)]
+    parity = []
+    while secs < budget_s or reps < 2:
+        h = heads[reps % len(heads)]
+        f, d, out = oracle_sample(w, heads=(h, h + 1))
+        if gpu_first is not None and reps < 2:
+            got = gpu_first[:, h:h + 1].astype(np.float64)
+            err = float(np.abs(got - out).max())
+            rel = float(np.linalg.norm(got - out) / np.linalg.norm(out))
+            parity.append({"head": h, "max_abs_err": err, "rel_fro_err": rel})
+        flop, secs, reps = flop + f, secs + d, reps + 1
+    res = {"value": flop / secs / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"{w.name}: {reps} single-head passes (heads 0, {w.heads - 1}, then 1.., all "
+                     f"{w.chunk_tokens} queries x {w.kv_tokens} keys incl. the cache prologue), fp64, {secs:.1f} s",
+           "cpu_model": _cpu_model()}
+    if parity:
+        res["parity"] = {"checks": parity, "tolerance": {"max_abs": TOL_MAX_ABS, "rel_fro": TOL_REL_FRO},
+                         "pass": all(p["max_abs_err"] <= TOL_MAX_ABS and p["rel_fro_err"] <= TOL_REL_FRO
+                                     for p in parity),
+                         "what": "GPU attend of the bench's config (batch element 0, before the timed region) "
+                                 "vs the fp64 oracle on the same seeded inputs"}
+    return res
 
 
 def _cpu_model():
@@ -211,7 +278,7 @@ def run_reference(args, w: synth.Workload, rank: int):
         oracle_sample(w, heads=(0, 1), q_rows=q_rows)
     flop = secs = 0.0
     for i in range(args.steps):
-        f, d = oracle_sample(w, heads=(i % w.heads, i % w.heads + 1), q_rows=q_rows)
+        f, d, _ = oracle_sample(w, heads=(i % w.heads, i % w.heads + 1), q_rows=q_rows)
         flop, secs = flop + f, secs + d
     value = flop / secs / 1e12
     sample = (f"{w.name}: per step one head x first {q_rows} queries x {w.kv_tokens} keys "
@@ -227,7 +294,184 @@ def run_reference(args, w: synth.Workload, rank: int):
     print(json.dumps(line), flush=True)
 
 
-# --------------------------------------------------------------------------- GPU arm
+# --------------------------------------------------------------------------- GPU timing
+class Timer:
+    """Times K steps with CUDA events at step boundaries only (an event between two kernels
+    would end their programmatic overlap), the L2 flushed before every step; the library's
+    per-kernel events are measured in a profiled step run after each timed one (same load and
+    clocks, not part of the sum)."""
+
+    def __init__(self, dev, flush=True, flush_read=False):
+        self.flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if flush else None
+        self.flush_read = flush_read
+
+    def flush(self):
+        if self.flush_buf is not None:
+            self.flush_buf.zero_()
+            if self.flush_read:
+                self.flush_buf[: self.flush_buf.numel() // 2].sum()
+
+    def run(self, step, steps, cache=None, profiled=True, clock_dev=None):
+        import paper_2602_15922_b200 as dz
+        if profiled:
+            cache.profile_enable(False)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        prof = {"prologue": [], "attention": [], "append": []}
+        launches = 0
+        torch.cuda.synchronize()
+        sampler = ClockSampler(clock_dev) if clock_dev is not None else None
+        if sampler:
+            sampler.__enter__()
+        for i in range(steps):
+            self.flush()
+            ev[i][0].record()
+            n0 = dz.kernel_launches()
+            step()
+            launches += dz.kernel_launches() - n0
+            ev[i][1].record()
+            if profiled:
+                cache.profile_enable(True)
+                self.flush()
+                step()
+                p = cache.profile_last()         # host-syncs on the library's events (last call)
+                for k in prof:
+                    prof[k].append(p[k])
+                cache.profile_enable(False)
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.__exit__()
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        return step_ms, prof, launches, (sampler.summary() if sampler else None)
+
+
+def make_cache(dz, w, dev, gq, gk, batch=None, world=1, rank=0, comm=0, flags=0, slack=None, max_chunk=None):
+    n = w.chunk_tokens
+    return dz.ChunkKVCache(w.batch if batch is None else batch, w.heads, w.head_dim, w.cache_tokens,
+                           n if max_chunk is None else max_chunk, w.rope_dims, gq.to(dev), gk.to(dev),
+                           rope_theta=w.rope_theta, rms_eps=w.rms_eps,
+                           window_slack=16 * n if slack is None else slack, world_size=world, rank=rank,
+                           nccl_comm=comm, flags=flags, device=dev)
+
+
+def device_inputs(w, dev, batch, seed, n_local=None):
+    """Timing-only inputs drawn on the device (same shapes and distributions as synth: N(0,1) bf16,
+    C2's 1% +-8 raw-K outliers)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    n = w.chunk_tokens if n_local is None else n_local
+    shp = (batch, n, w.heads, w.head_dim)
+    q, k, v = (torch.randn(shp, generator=g, device=dev).to(torch.bfloat16) for _ in range(3))
+    if w.outliers:
+        u1 = torch.rand(shp, generator=g, device=dev)
+        u2 = torch.rand(shp, generator=g, device=dev)
+        k = torch.where(u1 < 0.01, 8.0 * torch.sign(u2 - 0.5), k.float()).to(torch.bfloat16)
+    return q, k, v
+
+
+def secondary(dz, dev, steps, timer: Timer):
+    """Secondary workloads at one GPU, each timed like the primary (events at step boundaries,
+    kernels in profiled steps): K2 TFLOP/s and fraction of the measured peak.  Timing only:
+    inputs drawn on the device; parity of these configs is in tests/ (pytest -m gpu)."""
+    peak, _, hbm, _ = peaks()
+    out = {}
+
+    def chunk_line(w, name):
+        gq, gk = synth.draw_gains(w)
+        cache = make_cache(dz, w, dev, gq, gk, flags=dz.FLAG_PROFILE)
+        C = w.cached_chunks
+        for c in range(C):
+            _, k, v = device_inputs(w, dev, w.batch, 10_000 + c)
+            cache.append(k, v, synth.chunk_positions(w, c).to(dev), c)
+        q, k, v = device_inputs(w, dev, w.batch, 20_000)
+        _, kc, vc = device_inputs(w, dev, w.batch, 30_000)
+        pos = synth.chunk_positions(w, C).to(dev)
+        o = torch.empty_like(q)
+        cid = [C]
+
+        def step():
+            cache.attend(q, k, v, pos, cid[0], out=o)
+            cache.evict_front(1)
+            cache.append(kc, vc, pos, cid[0])
+            cid[0] += 1
+        for _ in range(3):
+            step()
+        sm, prof, launches, clk = timer.run(step, steps, cache, clock_dev=dev.index)
+        flop = w.useful_flop()
+        k2 = statistics.median(prof["attention"])
+        app_bytes = 2 * 2 * w.batch * w.chunk_tokens * w.heads * w.head_dim * 2
+        out[name] = {"workload": w.name, "mode": "chunk (attend + evict + append)",
+                     "step_tflops": flop / (statistics.median(sm) * 1e-3) / 1e12,
+                     "step_ms": spread(sm), "k2_ms": spread(prof["attention"]),
+                     "k2_tflops": flop / (k2 * 1e-3) / 1e12, "k2_frac": flop / (k2 * 1e-3) / 1e12 / peak,
+                     "append_gbs": app_bytes / (statistics.median(prof["append"]) * 1e-3) / 1e9,
+                     "append_frac_hbm": app_bytes / (statistics.median(prof["append"]) * 1e-3) / 1e9 / hbm,
+                     "gpu_launches_per_step": launches / steps, "clocks": clk}
+        cache.close()
+
+    chunk_line(synth.workload("C2"), "C2")
+    chunk_line(synth.workload("C4"), "C4@1")
+
+    # C3: 4 denoising steps x CFG batch 2 over one cache of 8 chunks, one CUDA graph replay
+    w = synth.workload("C3")
+    gq, gk = synth.draw_gains(w)
+    cache = make_cache(dz, w, dev, gq, gk, slack=0)
+    for c in range(w.cached_chunks):
+        _, k, v = device_inputs(w, dev, w.batch, 40_000 + c)
+        cache.append(k, v, synth.chunk_positions(w, c).to(dev), c)
+    S = w.steps
+    ins = [device_inputs(w, dev, w.batch, 50_000 + s) for s in range(S)]
+    outs = [torch.empty_like(ins[0][0]) for _ in range(S)]
+    pos = synth.chunk_positions(w, w.cached_chunks).to(dev)
+
+    def denoise():
+        for s in range(S):
+            cache.attend(*ins[s], pos, w.cached_chunks, out=outs[s])
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        denoise()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        denoise()
+    for _ in range(3):
+        graph.replay()
+    sm, _, launches, clk = timer.run(graph.replay, steps, profiled=False, clock_dev=dev.index)
+    flop = w.useful_flop() * S
+    out["C3_denoise_graph"] = {"workload": "C3", "mode": f"{S} denoising steps x batch 2 (K1 + K2 each), one CUDA "
+                               "graph replay per step", "step_ms": spread(sm),
+                               "step_tflops": flop / (statistics.median(sm) * 1e-3) / 1e12,
+                               "step_frac": flop / (statistics.median(sm) * 1e-3) / 1e12 / peak,
+                               "gpu_launches_per_step": 2 * S, "clocks": clk}
+    cache.close()
+
+    # Fig. 10(a) teacher forcing [C0..C3; Z1..Z4] x 1344 tokens, one attend_spans (SKIP tiles never loaded)
+    w = synth.workload("C1")
+    gq, gk = synth.draw_gains(w)
+    spans = synth.teacher_forcing_spans(4, w.chunk_tokens)
+    n_tf = sum(s.n_tokens for s in spans)
+    cache = dz.ChunkKVCache(1, w.heads, w.head_dim, 0, n_tf, w.rope_dims, gq.to(dev), gk.to(dev),
+                            flags=dz.FLAG_PROFILE, device=dev)
+    q, k, v = device_inputs(w, dev, 1, 60_000, n_local=n_tf)
+    pos = torch.cat([synth.chunk_positions(w, s.chunk) for s in spans]).to(dev)
+    o = torch.empty_like(q)
+    sl = [(s.chunk, s.kind, s.n_tokens) for s in spans]
+    step = lambda: cache.attend_spans(q, k, v, pos, sl, out=o)
+    for _ in range(3):
+        step()
+    sm, prof, launches, clk = timer.run(step, steps, cache, clock_dev=dev.index)
+    flop = 4.0 * w.head_dim * w.heads * visible_pairs(spans)
+    k2 = statistics.median(prof["attention"])
+    out["tf_fig10a"] = {"workload": "C1 shape, [C0..C3; Z1..Z4] x 1344", "mode": "teacher forcing (attend_spans)",
+                        "visible_fraction": visible_pairs(spans) / n_tf ** 2, "step_ms": spread(sm),
+                        "step_tflops": flop / (statistics.median(sm) * 1e-3) / 1e12,
+                        "k2_ms": spread(prof["attention"]), "k2_tflops": flop / (k2 * 1e-3) / 1e12,
+                        "k2_frac": flop / (k2 * 1e-3) / 1e12 / peak, "clocks": clk}
+    cache.close()
+    return out
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -249,35 +493,38 @@ def main():
     dev = torch.device("cuda", local)
     pg = None
     comm = 0
+    cfg_split = world > 1 and w.name == "C3"      # CFG parallelism: one batch element per GPU
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            uid = torch.frombuffer(bytearray(dz.nccl_unique_id()), dtype=torch.uint8)
-        uid = uid.to(dev)
-        dist.broadcast(uid, 0)
-        comm = dz.nccl_comm_init(world, bytes(uid.cpu().numpy().tobytes()), rank)
+        if not cfg_split:
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                uid = torch.frombuffer(bytearray(dz.nccl_unique_id()), dtype=torch.uint8)
+            uid = uid.to(dev)
+            dist.broadcast(uid, 0)
+            comm = dz.nccl_comm_init(world, bytes(uid.cpu().numpy().tobytes()), rank)
+    if cfg_split and world != w.batch:
+        print(json.dumps({"error": f"CFG split of {w.name} needs {w.batch} GPUs"}))
+        sys.exit(2)
 
-    N = world
+    N = 1 if cfg_split else world                 # Ulysses ranks
     n, H, D = w.chunk_tokens, w.heads, w.head_dim
     n_loc = n // N
+    B = 1 if cfg_split else w.batch               # batch elements held by this rank
+    b_elems = [rank] if cfg_split else list(range(w.batch))
     gq, gk = synth.draw_gains(w)
     C = w.cached_chunks
-    slack = 16 * n
-    cache = dz.ChunkKVCache(w.batch, H, D, w.cache_tokens, n, w.rope_dims, gq.to(dev), gk.to(dev),
-                            rope_theta=w.rope_theta, rms_eps=w.rms_eps, window_slack=slack, world_size=N,
-                            rank=rank, nccl_comm=comm,
-                            flags=(0 if args.no_profile else dz.FLAG_PROFILE) | (dz.FLAG_ONLINE_SOFTMAX if args.online else 0),
-                            device=dev)
-    sl = slice(rank * n_loc, (rank + 1) * n_loc)
+    flags = (0 if args.no_profile else dz.FLAG_PROFILE) | (dz.FLAG_ONLINE_SOFTMAX if args.online else 0)
+    cache = make_cache(dz, w, dev, gq, gk, batch=B, world=N, rank=0 if cfg_split else rank, comm=comm, flags=flags)
+    sl = slice(rank * n_loc, (rank + 1) * n_loc) if N > 1 else slice(0, n)
 
     def dev_chunk(x):   # [B][n][H][D] bf16 -> this rank's tokens on the device
         return x[:, sl].contiguous().to(dev)
 
     S = (args.denoise_steps or w.steps) if args.mode == "denoise" else 1
-    streams = [synth.draw_stream(w, b, steps=max(2, S)) for b in range(w.batch)]
+    streams = [synth.draw_stream(w, b, steps=max(2, S)) for b in b_elems]
     stack = lambda key, c: torch.stack([getattr(s, key)[c] for s in streams])
     for c in range(C):
         cache.append(dev_chunk(stack("cache_k", c)), dev_chunk(stack("cache_v", c)),
@@ -286,7 +533,10 @@ def main():
     kc, vc = dev_chunk(stack("cur_k", 1)), dev_chunk(stack("cur_v", 1))   # the ground-truth clean chunk
     pos = streams[0].cur_pos[sl].contiguous().to(dev)
     out = torch.empty_like(q)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # parity sample (outside the timed region): the first attention of this config, batch element 0
+    first = None
+    if world == 1 and args.mode == "chunk":
+        first = cache.attend(q, k, v, pos, C, out=torch.empty_like(q))[0].float().cpu().numpy()
     chunk_id = [C]
 
     def step(qq=q, kk=k, vv=v, kkc=kc, vvc=vc, pp=pos, oo=out):
@@ -297,7 +547,7 @@ def main():
         chunk_id[0] += 1
 
     graph = None
-    flop_one = w.useful_flop()
+    flop_one = w.useful_flop()                     # whole job: all batch elements, all ranks
     if args.mode == "tf":
         # Fig. 10(a) teacher forcing at the Wan shape: M clean chunks then M noisy chunks, one call
         tf_spans = synth.teacher_forcing_spans(args.tf_chunks, n)
@@ -341,42 +591,13 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    # ---------------- timed region: per-step CUDA events, L2 flushed between steps.  The library's
-    # per-kernel events are off in the timed steps: an event between two kernels ends their
-    # programmatic overlap (PDL), so the kernels are timed in a profiled step after each timed one.
-    flop_step = flop_one * S                         # global useful FLOP of one step
+    # ---------------- timed region
+    flop_step = flop_one * S                         # global useful FLOP of one step (all ranks)
     profiled = graph is None and not args.no_profile
-    if profiled:
-        cache.profile_enable(False)
-
-    def flush_l2():
-        if not args.no_flush:
-            flush.zero_()
-            if args.flush_read:
-                flush_sum = flush[: flush.numel() // 2].sum()  # noqa: F841
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    attn_ms, pro_ms, app_ms = [], [], []
+    timer = Timer(dev, flush=not args.no_flush, flush_read=args.flush_read)
     if pg:
         pg.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush_l2()
-            ev[i][0].record()
-            step()
-            ev[i][1].record()
-            if profiled:  # a profiled step between two timed ones (same load and clocks), not in the sum
-                cache.profile_enable(True)
-                flush_l2()
-                step()
-                prof = cache.profile_last()         # host-syncs on the library's events (last call)
-                attn_ms.append(prof["attention"])
-                pro_ms.append(prof["prologue"])
-                app_ms.append(prof["append"])
-                cache.profile_enable(False)
-    torch.cuda.synchronize()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    step_ms, prof, launches, clocks = timer.run(step, args.steps, cache, profiled=profiled, clock_dev=local)
     total_ms = sum(step_ms)
     if pg:
         t = torch.tensor([total_ms], device=dev)
@@ -388,10 +609,9 @@ def main():
     # ---------------- end to end through the public API with host buffers
     e2e = None
     if args.e2e_steps > 0 and args.mode == "chunk":  # (other modes: device-resident only)
-        # End to end through the public API with host buffers: every step copies its inputs from
-        # pinned host memory (H2D) and reads its output back (D2H), double-buffered so that the
-        # copies of step i+1 and the read-back of step i-1 overlap the kernels of step i (a
-        # user's pipelined denoising loop).  PCIe, not the kernels, bounds this number.
+        # Every step copies its inputs from pinned host memory (H2D) and reads its output back
+        # (D2H), double-buffered so that the copies of step i+1 and the read-back of step i-1
+        # overlap the kernels of step i (a user's pipelined denoising loop).  PCIe bounds it.
         pin = lambda x: x.cpu().pin_memory()
         hin = [pin(x) for x in (q, k, v, kc, vc, pos)]
         houts = [torch.empty(out.shape, dtype=out.dtype).pin_memory() for _ in range(2)]
@@ -400,45 +620,45 @@ def main():
         dins = [[torch.empty_like(x, device=dev) for x in (q, k, v, kc, vc, pos)] for _ in range(2)]
         douts = [torch.empty_like(out) for _ in range(2)]
         s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
-        main = torch.cuda.current_stream()
+        main_s = torch.cuda.current_stream()
         copied = [torch.cuda.Event() for _ in range(2)]
         computed = [torch.cuda.Event() for _ in range(2)]
         drained = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
 
         def h2d_copy(i):
-            sl = i % 2
+            s_ = i % 2
             with torch.cuda.stream(s_h2d):
                 if i >= 2:
-                    s_h2d.wait_event(consumed[sl])          # the step that read this buffer is done
-                for d_, h_ in zip(dins[sl], hin):
+                    s_h2d.wait_event(consumed[s_])          # the step that read this buffer is done
+                for d_, h_ in zip(dins[s_], hin):
                     d_.copy_(h_, non_blocking=True)
-                copied[sl].record(s_h2d)
+                copied[s_].record(s_h2d)
 
         if pg:
             pg.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        s_h2d.wait_stream(main)
-        s_d2h.wait_stream(main)
+        s_h2d.wait_stream(main_s)
+        s_d2h.wait_stream(main_s)
         h2d_copy(0)
         for i in range(args.e2e_steps):
-            sl = i % 2
+            s_ = i % 2
             if i + 1 < args.e2e_steps:
                 h2d_copy(i + 1)
-            main.wait_event(copied[sl])
+            main_s.wait_event(copied[s_])
             if i >= 2:
-                main.wait_event(drained[sl])                 # douts[sl] has been read back
-            dq, dk, dv, dkc, dvc, dpos = dins[sl]
-            step(dq, dk, dv, dkc, dvc, dpos, douts[sl])
-            consumed[sl].record(main)
-            computed[sl].record(main)
+                main_s.wait_event(drained[s_])                 # douts[s_] has been read back
+            dq, dk, dv, dkc, dvc, dpos = dins[s_]
+            step(dq, dk, dv, dkc, dvc, dpos, douts[s_])
+            consumed[s_].record(main_s)
+            computed[s_].record(main_s)
             with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(computed[sl])
-                houts[sl].copy_(douts[sl], non_blocking=True)
-                drained[sl].record(s_d2h)
-        main.wait_stream(s_d2h)
+                s_d2h.wait_event(computed[s_])
+                houts[s_].copy_(douts[s_], non_blocking=True)
+                drained[s_].record(s_d2h)
+        main_s.wait_stream(s_d2h)
         e1.record()
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
@@ -452,31 +672,29 @@ def main():
                        "neighbouring steps overlapped on two copy streams"}
 
     peak, peak_sus, hbm, src = peaks()
-    if not profiled:   # no per-kernel events: K1 + K2 of every step together
-        attn_ms = [m / S for m in step_ms]
-        pro_ms, app_ms = [float("nan")], [float("nan")]
-    attn_mean = statistics.mean(attn_ms)
-    flop_launch = flop_step / N / S
-    achieved = flop_launch / (attn_mean * 1e-3) / 1e12
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_attention_traffic.json")
-    if os.path.exists(tp):
-        d = json.load(open(tp))
-        if d.get("workload") == w.name:
-            traffic = d.get("dram_bytes_per_launch")
+    attn_ms = prof["attention"] if profiled else [m / S for m in step_ms]
+    attn_med = statistics.median(attn_ms)
+    ranks_work = 1 if cfg_split else N
+    flop_launch = flop_step / S / (w.batch if cfg_split else ranks_work)   # one rank's K2 launch
+    achieved = flop_launch / (attn_med * 1e-3) / 1e12
+    traffic, traffic_src = stamped_traffic(w.name) if (N == 1 and not cfg_split and args.mode == "chunk") else (None, "n/a")
     n_new = n_tf if args.mode == "tf" else n_loc
     # attend prologue: read q, k (+ v) and write q', k' (+ the V staging copy); with one GPU and the
     # new keys starting at a 128-key step the attention reads V in place (dz.h), no V copy
     v_in_place = N == 1 and (0 if args.mode == "tf" else w.cache_tokens) % 128 == 0
-    pro_bytes = 2 * (2 if v_in_place else 3) * w.batch * n_new * H * D * 2
-    app_bytes = 2 * 2 * w.batch * n_loc * H * D * 2     # read k,v + write k',v
+    pro_bytes = 2 * (2 if v_in_place else 3) * B * n_new * H * D * 2
+    app_bytes = 2 * 2 * B * n_loc * H * D * 2     # read k,v + write k',v
+    pro_med = statistics.median(prof["prologue"]) if profiled else float("nan")
+    app_med = statistics.median(prof["append"]) if profiled else float("nan")
     line = {
-        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": N, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak" if N == 1 else "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": w.name, "batch": w.batch, "heads": H, "head_dim": D, "chunk_tokens": n,
                    "cache_tokens": w.cache_tokens, "kv_tokens": w.kv_tokens, "useful_flop_per_step": flop_step,
-                   "parallelism": "single GPU" if N == 1 else f"ulysses sp{N}",
+                   "parallelism": ("single GPU" if world == 1 else
+                                   f"cfg split ({world} GPUs, one batch element each, no collective)" if cfg_split
+                                   else f"ulysses sp{N}"),
                    "step": ("attend (K1+K2) + append (K4) + evict, sliding window" if args.mode == "chunk" else
                             f"teacher forcing [C0..C{args.tf_chunks - 1}; Z1..Z{args.tf_chunks}] x {n} tokens, "
                             "one attend_spans (K1+K2, SKIP tiles never loaded)" if args.mode == "tf" else
@@ -484,29 +702,35 @@ def main():
                             + (", one CUDA graph replay" if graph is not None else ", eager")),
                    "l2": "flushed before every timed step (512 MB write)" if not args.no_flush else "warm",
                    "qk_storage": "fp16 (post-RMSNorm)", "pv": "bf16", "accumulate": "fp32"},
-        "pct_peak": value / (N * peak), "pct_peak_sustained": value / (N * peak_sus),
+        "pct_peak": value / (world * peak), "pct_peak_sustained": value / (world * peak_sus),
+        "step_ms": spread(step_ms),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "attn_fwd_kernel (K2)" if graph is None else "K1 + K2 per denoise step (graph replay)",
-                     "timing": ("CUDA events around K2 on the library stream, in a profiled step after each "
-                                "timed step (events between kernels end their PDL overlap)" if profiled else
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "kernel": "attn_fwd_kernel (K2)" if profiled else "K1 + K2 per denoise step (no per-kernel events)",
+                     "timing": ("median of CUDA events around K2 on the library stream, in a profiled step after "
+                                "each timed step (events between kernels end their PDL overlap)" if profiled else
                                 "step events / steps (no per-kernel events)"),
+                     "k2_ms": spread(attn_ms),
                      "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({src}, burst)",
-                     "frac_vs_sustained": achieved / peak_sus, "attn_ms_mean": attn_mean,
-                     "flop_per_launch": flop_launch},
-        "kernels": {"prologue_ms": statistics.mean(pro_ms),  # (denoise mode: the last step's; graph: n/a)
-                    "prologue_gbs": pro_bytes / (statistics.mean(pro_ms) * 1e-3) / 1e9,
-                    "append_ms": statistics.mean(app_ms),
-                    "append_gbs": (app_bytes / (statistics.mean(app_ms) * 1e-3) / 1e9
-                                   if N == 1 and args.mode == "chunk" and statistics.mean(app_ms) > 0 else None),
+                     "frac_vs_sustained": achieved / peak_sus, "flop_per_launch": flop_launch},
+        "kernels": {"prologue_ms": spread(prof["prologue"]) if profiled else None,
+                    "prologue_gbs": pro_bytes / (pro_med * 1e-3) / 1e9 if profiled else None,
+                    "append_ms": spread(prof["append"]) if profiled else None,
+                    "append_gbs": (app_bytes / (app_med * 1e-3) / 1e9
+                                   if N == 1 and args.mode == "chunk" and profiled and app_med > 0 else None),
                     "hbm_peak_gbs": hbm},
-        "gpu_launches": args.steps * ((3 if N == 1 else 4) if args.mode == "chunk" else 2 * S),  # K1, K2 (K4)
-        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "gpu_launches_how": "dz_kernel_launches() difference over the timed steps (host count at launch)",
+        "clocks": clocks,
         "e2e": e2e,
-        "parity": "tests/test_gpu_parity.py (pytest -m gpu); bench.py runs no oracle on the GPU arm",
     }
-    if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+    if rank == 0 and N == 1 and not cfg_split and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds, first)
+        if "parity" in line["cpu_baseline"]:
+            line["parity"] = line["cpu_baseline"]["parity"]
+    if rank == 0 and world == 1 and args.mode == "chunk" and not args.no_secondary and w.name == "C1":
+        cache.close()
+        line["secondary"] = secondary(dz, dev, args.secondary_steps, timer)
     if rank == 0:
         print(json.dumps(line), flush=True)
     cache.close()

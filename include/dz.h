@@ -320,6 +320,11 @@ DZ_API dz_status dz_sp_resume(dz_ctx* ctx, void* stream);
 DZ_API dz_status dz_debug_sp_unpack(const void* recv, void* out, int32_t world_size, int32_t batch, int32_t n_local,
                                     int32_t heads_local, int32_t head_dim, void* stream);
 
+/* Kernels this library has enqueued in this process so far (prologue, RoPE table,
+ * attention, unpack), counted on the host at launch: the difference over a region
+ * is the number of the library's kernels in it (benchmark evidence). */
+DZ_API int64_t dz_kernel_launches(void);
+
 /* Number of attention work units (batch x heads/world_size x query-tile pairs)
  * for an n-token chunk; the persistent grid is min(units, SM count). */
 DZ_API int32_t dz_attention_units(const dz_ctx* ctx, int32_t n_tokens);

@@ -102,6 +102,7 @@ SIGNATURES = [
     ("dz_profile_last", I32, [P, P]),
     ("dz_profile_enable", I32, [P, I32]),
     ("dz_debug_trace", I32, [I32, P, SZ]),
+    ("dz_kernel_launches", I64, []),
 ]
 
 _lib = None
@@ -145,6 +146,11 @@ def _need(t: torch.Tensor, name: str, dtype: torch.dtype, shape: Sequence[int], 
         raise ValueError(f"{name}: on {t.device}, expected {device}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+
+
+def kernel_launches() -> int:
+    """Kernels the library has enqueued in this process (host-side count at launch)."""
+    return int(lib().dz_kernel_launches())
 
 
 def watchdog(reset: bool = True):

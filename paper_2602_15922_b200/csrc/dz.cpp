@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <cstdlib>
 #include <deque>
 #include <mutex>
@@ -27,6 +28,7 @@
 namespace {
 
 constexpr size_t kAlign = 256;
+std::atomic<int64_t> g_launches{0};  // kernels this library enqueued (dz_kernel_launches)
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {  // byte offsets inside the caller's storage
@@ -352,11 +354,14 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
     dz_status r = cuda_check(c, dz::launch_rope_table(reinterpret_cast<float2*>(c->base + c->L.rope_off),
                                                       dz::kRopeLen, a, st), "rope table launch");
     if (r) return r;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     // a fill recorded into a graph being captured has not run yet: fill again on the next eager call
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) c->rope_ready = true;
   }
-  return cuda_check(c, dz::launch_prologue(a, st), "prologue launch");
+  dz_status r = cuda_check(c, dz::launch_prologue(a, st), "prologue launch");
+  if (!r) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return r;
 }
 
 // one grouped NCCL send/recv per plan entry (all peers, all tensors) on the caller's stream
@@ -447,7 +452,9 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
     c->have_map = true;
   }
   c->last_nq = (int32_t)n;
-  return cuda_check(c, dz::launch_attention(a, st), "attention launch");
+  dz_status r = cuda_check(c, dz::launch_attention(a, st), "attention launch");
+  if (!r) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return r;
 }
 
 }  // namespace
@@ -629,6 +636,7 @@ dz_status attend_unpack(dz_ctx* c, int64_t n, void* out, bool prof, cudaStream_t
                                                    c->D, st),
                            "unpack launch");
   if (r) return r;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   attend_mark(c, prof, 4, st);
   return DZ_OK;
 }
@@ -972,6 +980,8 @@ dz_status dz_debug_sp_unpack(const void* recv, void* out, int32_t world_size, in
              ? DZ_OK
              : DZ_ECUDA;
 }
+
+int64_t dz_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int32_t dz_attention_units(const dz_ctx* c, int32_t n) {
   if (!c || n <= 0) return 0;
