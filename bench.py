@@ -679,10 +679,11 @@ def main():
     achieved = flop_launch / (attn_med * 1e-3) / 1e12
     traffic, traffic_src = stamped_traffic(w.name) if (N == 1 and not cfg_split and args.mode == "chunk") else (None, "n/a")
     n_new = n_tf if args.mode == "tf" else n_loc
-    # attend prologue: read q, k (+ v) and write q', k' (+ the V staging copy); with one GPU and the
-    # new keys starting at a 128-key step the attention reads V in place (dz.h), no V copy
+    # attend prologue (K1): reads q, k (+ v) and writes q', k' (+ the V staging copy); with one GPU and
+    # the new keys starting at a 128-key step the attention reads V in place (dz.h), no V copy
     v_in_place = N == 1 and (0 if args.mode == "tf" else w.cache_tokens) % 128 == 0
-    pro_bytes = 2 * (2 if v_in_place else 3) * B * n_new * H * D * 2
+    pro_tensors = 2 if v_in_place else 3
+    pro_bytes = 2 * pro_tensors * B * n_new * H * D * 2
     app_bytes = 2 * 2 * B * n_loc * H * D * 2     # read k,v + write k',v
     pro_med = statistics.median(prof["prologue"]) if profiled else float("nan")
     app_med = statistics.median(prof["append"]) if profiled else float("nan")

@@ -28,6 +28,7 @@
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "rmsrope.cuh"
 
 namespace dz {
 namespace {
@@ -48,26 +49,8 @@ constexpr int kThreads = 256;
 constexpr int kCtasPerSm = DZ_PRO_CTAS;
 constexpr int kMaxStageBytes = DZ_PRO_RING_KB * 1024;  // ring size cap per CTA
 
-__device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    f[2 * i] = __uint_as_float(w[i] << 16);
-    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-  }
-}
-
-__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
-  __half2 h = __floats2half2_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-
-// (cos, sin) of the angle p * omega in fp64, rounded to fp32 (table fill, untabulated positions)
-__device__ __noinline__ float2 rope_cs(int p, double omega) {
-  double sn, cn;
-  sincos((double)p * omega, &sn, &cn);
-  return make_float2((float)cn, (float)sn);
-}
+using rr::bf16x8_to_f32;
+using rr::rope_cs;
 
 // shared-memory carve-up for H heads, nt tensors present, S stages
 struct ProSmem {
@@ -207,20 +190,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
           bf16x8_to_f32(v[i], f[i]);
-          ss[i] = 0.f;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) ss[i] = fmaf(f[i][e], f[i][e], ss[i]);
+          ss[i] = rr::chunk_ss(f[i]);
         }
+        // butterfly within each half-row, then across the halves (rmsrope.cuh)
 #pragma unroll
-        for (int m = G / 2; m >= 1; m >>= 1)
+        for (int m = G / 4; m >= 1; m >>= 1)
 #pragma unroll
-          for (int i = 0; i < kPer; ++i) ss[i] += __shfl_xor_sync(0xffffffffu, ss[i], m);
+          for (int i = 0; i < kPer; ++i) ss[i] = __fadd_rn(ss[i], __shfl_xor_sync(0xffffffffu, ss[i], m));
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) ss[i] = __fadd_rn(ss[i], __shfl_xor_sync(0xffffffffu, ss[i], G / 2));
         const float sc = w == 0 ? a.q_scale : 1.f;  // Q' leaves pre-scaled by softmax_scale*log2(e)
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
           const int h = h0 + g + kGroups * i;
           if (h >= H) continue;
-          const float inv = rsqrtf(ss[i] * (1.0f / D) + a.eps);
+          const float inv = rr::inv_rms(ss[i], D, a.eps);
           float gg[8];
           if (gains_in_regs) {
 #pragma unroll
@@ -233,12 +217,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
           }
           uint32_t pk[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float u = f[i][2 * e] * inv * gg[2 * e];
-            const float x = f[i][2 * e + 1] * inv * gg[2 * e + 1];
-            const float2 c = csr[e];
-            pk[e] = pack_half2((u * c.x - x * c.y) * sc, (u * c.y + x * c.x) * sc);
-          }
+          for (int e = 0; e < 4; ++e) pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
           reinterpret_cast<uint4*>(o.base)[(base + rowoff[h]) / 8 + li] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
       }
@@ -345,30 +324,27 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         bf16x8_to_f32(v[w][i], f[i]);
-        ss[i] = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) ss[i] = fmaf(f[i][e], f[i][e], ss[i]);
+        ss[i] = rr::chunk_ss(f[i]);
       }
+      // butterfly within each half-row, then across the halves (rmsrope.cuh)
 #pragma unroll
-      for (int m = G / 2; m >= 1; m >>= 1)
+      for (int m = G / 4; m >= 1; m >>= 1)
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) ss[i] += __shfl_xor_sync(0xffffffffu, ss[i], m);
+        for (int i = 0; i < kPer; ++i) ss[i] = __fadd_rn(ss[i], __shfl_xor_sync(0xffffffffu, ss[i], m));
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) ss[i] = __fadd_rn(ss[i], __shfl_xor_sync(0xffffffffu, ss[i], G / 2));
       const float sc = w == 0 ? a.q_scale : 1.f;
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         if (!hv[i]) continue;
         const int h = g + kRows * i;
-        const float inv = rsqrtf(ss[i] * (1.0f / D) + a.eps);
+        const float inv = rr::inv_rms(ss[i], D, a.eps);
         const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
         const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
         const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
         uint32_t pk[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float u = f[i][2 * e] * inv * gg[2 * e];
-          const float x = f[i][2 * e + 1] * inv * gg[2 * e + 1];
-          pk[e] = pack_half2((u * csr[e].x - x * csr[e].y) * sc, (u * csr[e].y + x * csr[e].x) * sc);
-        }
+        for (int e = 0; e < 4; ++e) pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
         reinterpret_cast<uint4*>(static_cast<__half*>(o.base) + base + ooff[w][i])[0] =
             make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }

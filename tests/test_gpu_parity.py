@@ -84,7 +84,7 @@ def test_attend_parity_c1_all_heads():
 
 
 @pytest.mark.parametrize("D,rd", [(128, (44, 42, 42)), (64, (16, 24, 24))])
-@pytest.mark.parametrize("n,cached", [(1, 0), (64, 0), (130, 1), (200, 2), (256, 3), (383, 2), (1344, 1)])
+@pytest.mark.parametrize("n,cached", [(1, 0), (64, 0), (130, 1), (200, 2), (256, 3), (300, 2), (320, 1), (383, 2), (1344, 1)])
 def test_attend_parity_ragged(D, rd, n, cached):
     # chunk sizes spanning several tiles with ragged tails; cache of `cached` chunks
     w = synth.Workload(f"R{n}", 7, batch=1, heads=3, head_dim=D, rope_dims=rd, frames=1, grid_h=1, grid_w=n,
