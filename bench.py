@@ -7,13 +7,15 @@ fraction of the measured bf16 tensor-core peak (MEASURED_PEAKS.json).
 
 One step = one pass of the whole hot path for one chunk, as
 Alg. 2 runs it in the DreamZero-Flash 1-step regime:
-  attend  -- K1 RMSNorm+3D-RoPE prologue of the noisy chunk's Q/K/V (+ Ulysses
+  append  -- the ground-truth clean chunk c-1 enters the cache: K'/V written
+             (update=True, l.601-602; its observation precedes chunk c's denoising);
+  attend  -- the RMSNorm+3D-RoPE prologue of the noisy chunk c's Q/K (+ Ulysses
              all-to-all under SP) and K2 tcgen05 attention over the KV cache plus
-             the chunk itself (update=False);
+             the chunk itself (update=False, l.584-585);
   evict   -- the oldest chunk leaves the window, keeping the context length
-             fixed (l.510 sliding context), so every step sees the same shapes;
-  append  -- K4: the ground-truth clean chunk's K'/V written into the cache
-             (update=True, l.601-602).
+             fixed (l.510 sliding context), so every step sees the same shapes.
+On one GPU append + attend are one dz_append_attend call: both prologues (the
+K4 append and the K1 attend prologue) in one kernel launch, then K2.
 Useful FLOP counts only the attention.  Inputs are resident in HBM before
 the timed region; the L2 is flushed (a 512 MB write) before every timed step.
 
@@ -379,32 +381,33 @@ def secondary(dz, dev, steps, timer: Timer):
         gq, gk = synth.draw_gains(w)
         cache = make_cache(dz, w, dev, gq, gk, flags=dz.FLAG_PROFILE)
         C = w.cached_chunks
-        for c in range(C):
+        for c in range(C - 1):
             _, k, v = device_inputs(w, dev, w.batch, 10_000 + c)
             cache.append(k, v, synth.chunk_positions(w, c).to(dev), c)
         q, k, v = device_inputs(w, dev, w.batch, 20_000)
         _, kc, vc = device_inputs(w, dev, w.batch, 30_000)
         pos = synth.chunk_positions(w, C).to(dev)
         o = torch.empty_like(q)
-        cid = [C]
+        cid = [C - 1]
 
-        def step():
-            cache.attend(q, k, v, pos, cid[0], out=o)
+        def step():   # inject chunk cid, denoise chunk cid + 1 over C cached chunks, evict the oldest
+            cache.append_attend(kc, vc, pos, cid[0], q, k, v, pos, cid[0] + 1, out=o)
             cache.evict_front(1)
-            cache.append(kc, vc, pos, cid[0])
             cid[0] += 1
         for _ in range(3):
             step()
         sm, prof, launches, clk = timer.run(step, steps, cache, clock_dev=dev.index)
         flop = w.useful_flop()
         k2 = statistics.median(prof["attention"])
-        app_bytes = 2 * 2 * w.batch * w.chunk_tokens * w.heads * w.head_dim * 2
-        out[name] = {"workload": w.name, "mode": "chunk (attend + evict + append)",
+        # the fused prologue reads k_gt, v_gt, q, k and writes K', V (cache) and Q', K' (noisy chunk)
+        pro_bytes = 2 * 4 * w.batch * w.chunk_tokens * w.heads * w.head_dim * 2
+        pro = statistics.median(prof["prologue"])
+        out[name] = {"workload": w.name, "mode": "chunk (append_attend + evict)",
                      "step_tflops": flop / (statistics.median(sm) * 1e-3) / 1e12,
                      "step_ms": spread(sm), "k2_ms": spread(prof["attention"]),
                      "k2_tflops": flop / (k2 * 1e-3) / 1e12, "k2_frac": flop / (k2 * 1e-3) / 1e12 / peak,
-                     "append_gbs": app_bytes / (statistics.median(prof["append"]) * 1e-3) / 1e9,
-                     "append_frac_hbm": app_bytes / (statistics.median(prof["append"]) * 1e-3) / 1e9 / hbm,
+                     "prologue_ms": spread(prof["prologue"]), "prologue_gbs": pro_bytes / (pro * 1e-3) / 1e9,
+                     "prologue_frac_hbm": pro_bytes / (pro * 1e-3) / 1e9 / hbm,
                      "gpu_launches_per_step": launches / steps, "clocks": clk}
         cache.close()
 
@@ -537,13 +540,15 @@ def main():
     first = None
     if world == 1 and args.mode == "chunk":
         first = cache.attend(q, k, v, pos, C, out=torch.empty_like(q))[0].float().cpu().numpy()
+    if args.mode == "chunk":
+        cache.evict_front(1)               # C-1 chunks: each step injects one, attends with C, evicts one
     chunk_id = [C]
 
     def step(qq=q, kk=k, vv=v, kkc=kc, vvc=vc, pp=pos, oo=out):
         cid = chunk_id[0]
-        cache.attend(qq, kk, vv, pp, cid, out=oo)
-        cache.evict_front(1)               # window full: the oldest chunk leaves ...
-        cache.append(kkc, vvc, pp, cid)    # ... and the ground-truth chunk enters
+        # the ground-truth chunk cid enters, chunk cid + 1 is denoised ...
+        cache.append_attend(kkc, vvc, pp, cid, qq, kk, vv, pp, cid + 1, out=oo)
+        cache.evict_front(1)               # ... and the oldest chunk leaves the window
         chunk_id[0] += 1
 
     graph = None
@@ -683,6 +688,8 @@ def main():
     # the new keys starting at a 128-key step the attention reads V in place (dz.h), no V copy
     v_in_place = N == 1 and (0 if args.mode == "tf" else w.cache_tokens) % 128 == 0
     pro_tensors = 2 if v_in_place else 3
+    if N == 1 and args.mode == "chunk":
+        pro_tensors += 2      # dz_append_attend: the ground-truth chunk's k, v (K4) in the same launch
     pro_bytes = 2 * pro_tensors * B * n_new * H * D * 2
     app_bytes = 2 * 2 * B * n_loc * H * D * 2     # read k,v + write k',v
     pro_med = statistics.median(prof["prologue"]) if profiled else float("nan")
@@ -696,7 +703,10 @@ def main():
                    "parallelism": ("single GPU" if world == 1 else
                                    f"cfg split ({world} GPUs, one batch element each, no collective)" if cfg_split
                                    else f"ulysses sp{N}"),
-                   "step": ("attend (K1+K2) + append (K4) + evict, sliding window" if args.mode == "chunk" else
+                   "step": (("append_attend (one prologue launch for the K4 append and the K1 attend "
+                             "prologue, then K2) + evict, sliding window" if N == 1 else
+                             "append (K4 + exchange) + attend (K1 + exchange + K2 + exchange + K5) + evict")
+                            if args.mode == "chunk" else
                             f"teacher forcing [C0..C{args.tf_chunks - 1}; Z1..Z{args.tf_chunks}] x {n} tokens, "
                             "one attend_spans (K1+K2, SKIP tiles never loaded)" if args.mode == "tf" else
                             f"{S} denoising steps of one chunk (K1+K2 each) over a fixed cache"

@@ -197,6 +197,17 @@ DZ_API dz_status dz_attend_spans(dz_ctx* ctx, const void* q_raw, const void* k_r
                                  const int32_t* pos_thw, const dz_span* spans, int32_t n_spans, void* out,
                                  void* stream);
 
+/* Ground-truth injection of one chunk followed by the denoising step of the next (Alg. 2: the
+ * update=True pass of chunk c-1, l.601-602, then u_theta(x_t; KV, ..., update=False) of chunk c,
+ * l.584-585): exactly dz_append_kv(k_gt, v_gt, gt) then dz_attend_chunk(q_raw, k_raw, v_raw, chunk,
+ * out) -- same results, same cache state -- but on one GPU both prologues (the appended chunk's K'/V
+ * and the attended chunk's Q'/K') run in one kernel launch.  Validation as for the two calls, plus
+ * chunk->chunk_id > gt->chunk_id (else DZ_ESTATE); nothing is enqueued if either fails.  Under SP
+ * (or with more heads than one prologue pass holds) it performs the two calls; not available with
+ * DZ_FLAG_EXTERNAL_EXCHANGE (DZ_EINVAL). */
+DZ_API dz_status dz_append_attend(dz_ctx* ctx, const void* k_gt, const void* v_gt, const dz_span* gt, const void* q_raw,
+                                  const void* k_raw, const void* v_raw, const dz_span* chunk, void* out, void* stream);
+
 /* Commit the chunk staged by the last dz_attend_chunk (which must have had
  * kind DZ_CLEAN and this chunk_id): the model-side "attend the clean chunk,
  * then update the cache" form of Alg. 2 l.601-602.  Moves no data.  DZ_ESTATE

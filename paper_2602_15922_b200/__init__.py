@@ -80,6 +80,7 @@ SIGNATURES = [
     ("dz_append_kv", I32, [P, P, P, ctypes.POINTER(DzSpan), P]),
     ("dz_attend_chunk", I32, [P, P, P, P, ctypes.POINTER(DzSpan), P, P]),
     ("dz_attend_spans", I32, [P, P, P, P, P, ctypes.POINTER(DzSpan), I32, P, P]),
+    ("dz_append_attend", I32, [P, P, P, ctypes.POINTER(DzSpan), P, P, P, ctypes.POINTER(DzSpan), P, P]),
     ("dz_commit_staged", I32, [P, I32, P]),
     ("dz_evict_front", I32, [P, I32, P]),
     ("dz_cache_state", I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32)]),
@@ -279,6 +280,30 @@ class ChunkKVCache:
         span = self._span(chunk_id, kind, n_local, pos)
         self._check(lib().dz_attend_chunk(self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), ctypes.byref(span),
                                           out.data_ptr(), _stream_ptr(stream)), "dz_attend_chunk")
+        return out
+
+    def append_attend(self, k_gt: torch.Tensor, v_gt: torch.Tensor, pos_gt: torch.Tensor, gt_chunk_id: int,
+                      q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor, chunk_id: int,
+                      kind: int = NOISY, out: Optional[torch.Tensor] = None,
+                      stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Append the ground-truth chunk ``gt_chunk_id`` then attend chunk ``chunk_id`` (Alg. 2's cache update
+        followed by the next chunk's denoising step) -- the same as ``append`` then ``attend``, with both
+        prologues in one kernel launch on one GPU."""
+        n_gt = k_gt.shape[1]
+        self._act(k_gt, "k_gt", n_gt)
+        self._act(v_gt, "v_gt", n_gt)
+        n_local = q.shape[1]
+        for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+            self._act(t, nm, n_local)
+        if out is None:
+            out = torch.empty_like(q)
+        else:
+            self._act(out, "out", n_local)
+        gspan = self._span(gt_chunk_id, CLEAN, n_gt, pos_gt)
+        span = self._span(chunk_id, kind, n_local, pos)
+        self._check(lib().dz_append_attend(self._ctx, k_gt.data_ptr(), v_gt.data_ptr(), ctypes.byref(gspan),
+                                           q.data_ptr(), k.data_ptr(), v.data_ptr(), ctypes.byref(span),
+                                           out.data_ptr(), _stream_ptr(stream)), "dz_append_attend")
         return out
 
     def attend_spans(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pos: torch.Tensor,

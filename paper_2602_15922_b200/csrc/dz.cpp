@@ -287,8 +287,8 @@ dz_status check_span(dz_ctx* c, const dz_span* s) {
 
 // Keep [start, start + valid + max_chunk) inside the slot range: compact the
 // committed window down to slot 0 when it would run past the end.
-dz_status ensure_staging_room(dz_ctx* c, cudaStream_t st) {
-  if (c->start + c->valid + c->cfg.max_chunk_tokens <= c->L.slots) return DZ_OK;
+dz_status ensure_staging_room(dz_ctx* c, cudaStream_t st, int64_t extra = 0) {
+  if (c->start + c->valid + extra + c->cfg.max_chunk_tokens <= c->L.slots) return DZ_OK;
   if (c->host_only) {  // a planning context holds no data: bookkeeping only
     c->start = 0;
     return DZ_OK;
@@ -323,8 +323,17 @@ void fill_prologue_common(dz_ctx* c, dz::PrologueArgs& a, const int32_t* pos, in
 
 // K1 prologue for the current chunk: Q' and the chunk's K'/V, written either
 // straight into the staging slot (N == 1) or into the all-to-all send layout.
+// A ground-truth chunk appended in the same prologue launch as an attend (dz_append_attend, one GPU):
+// its K'/V go to slots [valid, valid + n) and the attended chunk's staging slots follow them.
+struct AppendJob {
+  const void* k = nullptr;
+  const void* v = nullptr;
+  const int32_t* pos = nullptr;
+  int64_t n = 0;
+};
+
 dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, const int32_t* pos, int64_t n,
-                       cudaStream_t st, bool cur_separate = false) {
+                       cudaStream_t st, bool cur_separate = false, const AppendJob* aj = nullptr) {
   const int64_t n_loc = n / c->N;
   dz::PrologueArgs a;
   fill_prologue_common(c, a, pos, n_loc);
@@ -335,7 +344,16 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
   if (c->N == 1) {
     a.heads_per_dest = c->H;
     a.y[0] = {c->base + c->L.q_off, n * c->H * c->D, (int64_t)c->H * c->D, 0};
-    const int64_t slot = c->start + c->valid;
+    const int64_t slot = c->start + c->valid + (aj ? aj->n : 0);
+    if (aj) {  // the ground-truth chunk: K' and V into the slots right after the committed ones
+      a.j1.x[1] = aj->k;
+      a.j1.x[2] = aj->v;
+      a.j1.x_bstride = aj->n * c->H * c->D;
+      a.j1.pos = aj->pos;
+      a.j1.n = (int32_t)aj->n;
+      a.j1.y[1] = {c->kslot(0, c->start + c->valid), c->L.slots * c->H * c->D, (int64_t)c->H * c->D, 0};
+      a.j1.y[2] = {c->vslot(0, c->start + c->valid), c->L.slots * c->H * c->D, (int64_t)c->H * c->D, 0};
+    }
     if (cur_separate)  // a noisy chunk's K' goes to its own buffer; the committed cache is only read
       a.y[1] = {c->base + c->L.kc_off, n * c->H * c->D, (int64_t)c->H * c->D, 0};
     else
@@ -662,19 +680,29 @@ dz_status attend_sp_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, 
 // n new tokens described by `spans`; keys = committed chunks + the new tokens.
 dz_status attend_impl(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw, const int32_t* pos,
                       int64_t n, const dz::SpanTable& spans, void* out, bool may_commit, int32_t chunk_id,
-                      int32_t kind, cudaStream_t st) {
+                      int32_t kind, cudaStream_t st, const AppendJob* aj = nullptr, int32_t aj_id = 0) {
   dz_status r;
   c->staged = false;
+  if (aj) {  // room for the appended chunk and the staging slots after it (compaction if needed)
+    if ((r = ensure_staging_room(c, st, aj->n))) return r;
+  }
+  const int64_t valid_new = c->valid + (aj ? aj->n : 0);
   // The new tokens' K'/V are only staged after the committed slots when the chunk may be committed
   // (attend_chunk of a CLEAN chunk), the exchange needs them (SP) or the new keys do not start at a
   // key step; otherwise K' goes to the current-chunk buffer, V is read in place from the caller's
   // input, and the attention only reads the committed cache.
-  const bool cur_sep = c->N == 1 && !may_commit && c->valid % dz::attention_step_keys(c->m_static) == 0;
+  const bool cur_sep = c->N == 1 && !may_commit && valid_new % dz::attention_step_keys(c->m_static) == 0;
   c->staging_read = !cur_sep;
   const bool prof = c->ev[0] != nullptr && c->prof_on;
   const bool stage_chunk = chunk_id >= 0;
   attend_mark(c, prof, 0, st);
-  if ((r = run_prologue(c, q_raw, k_raw, cur_sep ? nullptr : v_raw, pos, n, st, cur_sep))) return r;
+  if ((r = run_prologue(c, q_raw, k_raw, cur_sep ? nullptr : v_raw, pos, n, st, cur_sep, aj))) return r;
+  if (aj) {  // the ground-truth chunk is committed: the attention's keys include it
+    c->valid += aj->n;
+    c->chunks.emplace_back(aj_id, aj->n);
+    c->last_id = aj_id;
+    c->have_append_ev = false;
+  }
   attend_mark(c, prof, 1, st);
   if (c->N == 1) {
     attend_mark(c, prof, 2, st);
@@ -768,6 +796,42 @@ dz_status dz_attend_spans(dz_ctx* c, const void* q_raw, const void* k_raw, const
   }
   if ((r = check_device(c))) return r;
   return attend_impl(c, q_raw, k_raw, v_raw, pos_thw, n, t, out, false, -1, 0, static_cast<cudaStream_t>(stream));
+}
+
+dz_status dz_append_attend(dz_ctx* c, const void* k_gt, const void* v_gt, const dz_span* gt, const void* q_raw,
+                           const void* k_raw, const void* v_raw, const dz_span* s, void* out, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if (!k_gt || !v_gt || !aligned16(k_gt) || !aligned16(v_gt)) return fail(c, DZ_EINVAL, "null/misaligned k_gt or v_gt");
+  if ((r = check_attend_ptrs(c, q_raw, k_raw, v_raw, out))) return r;
+  if ((r = check_span(c, gt))) return r;
+  if (gt->kind != DZ_CLEAN) return fail(c, DZ_ESTATE, "only clean chunks enter the cache (Alg. 2 l.603)");
+  if (c->valid + gt->n_tokens > c->cfg.cache_capacity_tokens)
+    return fail(c, DZ_ECAPACITY, "cache full: %lld + %d > %lld", (long long)c->valid, gt->n_tokens,
+                (long long)c->cfg.cache_capacity_tokens);
+  if ((r = check_span(c, s))) return r;
+  if (s->chunk_id <= gt->chunk_id)
+    return fail(c, DZ_ESTATE, "chunk id %d must exceed the appended chunk's id %d", s->chunk_id, gt->chunk_id);
+  if (c->external_x)
+    return fail(c, DZ_EINVAL, "with DZ_FLAG_EXTERNAL_EXCHANGE call dz_append_kv and dz_attend_chunk");
+  if ((r = check_device(c))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // one launch for both prologues needs the token-loop prologue (one GPU, H within one pass of it)
+  const bool fused = c->N == 1 && c->H <= 3 * (256 / (c->D / 8));
+  if (!fused) {
+    if ((r = dz_append_kv(c, k_gt, v_gt, gt, stream))) return r;
+    return dz_attend_chunk(c, q_raw, k_raw, v_raw, s, out, stream);
+  }
+  dz::SpanTable t;
+  t.n = 1;
+  set_span(t, 0, s->chunk_id, s->kind, 0, s->n_tokens);
+  AppendJob aj;
+  aj.k = k_gt;
+  aj.v = v_gt;
+  aj.pos = gt->pos_thw;
+  aj.n = gt->n_tokens;
+  return attend_impl(c, q_raw, k_raw, v_raw, s->pos_thw, s->n_tokens, t, out, s->kind == DZ_CLEAN, s->chunk_id,
+                     s->kind, st, &aj, gt->chunk_id);
 }
 
 int32_t dz_sp_pending(const dz_ctx* c, int32_t* phase, dz_xfer* out, int32_t cap) {

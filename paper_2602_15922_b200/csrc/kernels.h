@@ -36,7 +36,18 @@ struct OutSlot {
   int64_t bstride = 0, tstride = 0, dstride = 0;
 };
 
+// A second token set processed in the same launch (dz_append_attend: the ground-truth chunk's
+// append next to the noisy chunk's prologue; one GPU).  Tensors with x[w] == nullptr are absent.
+struct PrologueJob {
+  const void* x[3] = {nullptr, nullptr, nullptr};
+  int64_t x_bstride = 0;
+  const int32_t* pos = nullptr;
+  OutSlot y[3];
+  int32_t n = 0;
+};
+
 struct PrologueArgs {
+  PrologueJob j1;                                  // optional second token set (j1.n > 0)
   const void* x[3] = {nullptr, nullptr, nullptr};  // raw bf16 q, k, v: [B][n][H][D]
   int64_t x_bstride = 0;                           // elements between batch elements
   const int32_t* pos = nullptr;                    // [n][3] (t, h, w)

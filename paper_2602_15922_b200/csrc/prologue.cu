@@ -240,12 +240,22 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
 // (It replaced a one-token-per-CTA kernel that ncu showed instruction-bound -- 7060 warp
 // instructions per token, mostly per-token address and division arithmetic: attend prologue
 // 24.2 -> 22.4 us, append 19.7 -> 17.1 us at C1.)
-template <int D, int MASK>
+// DUAL: a second token set (a.j1, one GPU) follows the first in the item sequence; MASK is then the
+// union of both sets' tensors and a tensor absent from an item's set (x[w] == nullptr) is skipped.
+template <int D, int MASK, bool DUAL>
 __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(const PrologueArgs a) {
   constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
   ptx::pdl_launch_dependents();
   const int tid = threadIdx.x, g = tid / G, li = tid % G;
-  const int H = a.H, items = a.B * a.n;
+  const int H = a.H, items0 = a.B * a.n, items = items0 + (DUAL ? a.B * a.j1.n : 0);
+  // item -> (set, batch element, token)
+  auto locate = [&](int item, int& b, int& t) -> bool {
+    const bool s1 = DUAL && item >= items0;
+    const int it = s1 ? item - items0 : item, nn = s1 ? a.j1.n : a.n;
+    b = it / nn;
+    t = it - b * nn;
+    return s1;
+  };
   const int64_t tokD = (int64_t)H * D;
   // per (tensor, head slot): output offset inside the token's block, in elements
   int64_t ooff[3][kPer];
@@ -260,16 +270,19 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
       if (MASK >> w & 1) ooff[w][i] = (int64_t)dest * a.y[w].dstride + (int64_t)(h - dest * a.heads_per_dest) * D + li * 8;
   }
   auto load = [&](int item, uint4 (&v)[3][kPer]) {
-    const int b = item / a.n, t = item - b * a.n;
-    const int64_t src = (int64_t)b * a.x_bstride + (int64_t)t * tokD + g * D + li * 8;
+    int b, t;
+    const bool s1 = locate(item, b, t);
+    const int64_t src = (int64_t)b * (s1 ? a.j1.x_bstride : a.x_bstride) + (int64_t)t * tokD + g * D + li * 8;
 #pragma unroll
-    for (int w = 0; w < 3; ++w)
-      if (MASK >> w & 1)
+    for (int w = 0; w < 3; ++w) {
+      const void* xw = s1 ? a.j1.x[w] : a.x[w];
+      if ((MASK >> w & 1) && (!DUAL || xw != nullptr))
 #pragma unroll
         for (int i = 0; i < kPer; ++i)
           if (hv[i])
-            v[w][i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.x[w]) + src +
+            v[w][i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(xw) + src +
                                                           (int64_t)kRows * i * D));
+    }
   };
   // this thread's 4 rotation pairs j = 4 li + e: their axis is fixed, their angle depends on the
   // token's position on that axis; (cos, sin) come from the table (positions two tokens ahead,
@@ -279,9 +292,10 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
   for (int e = 0; e < 4; ++e) ax[e] = a.axis[li * 4 + e];
   auto positions = [&](int item, int (&p)[4]) {
     if (item >= items) return;
-    const int t = item % a.n;
+    int b, t;
+    const int32_t* pos = locate(item, b, t) ? a.j1.pos : a.pos;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) p[e] = __ldg(a.pos + 3 * t + ax[e]);
+    for (int e = 0; e < 4; ++e) p[e] = __ldg(pos + 3 * t + ax[e]);
   };
   auto angles = [&](const int (&p)[4], float2 (&c)[4]) {
 #pragma unroll
@@ -307,11 +321,13 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
       angles(pn, csn);
       positions(nxt + gridDim.x, pn);
     }
-    const int b = item / a.n, t = item - b * a.n;
+    int b, t;
+    const bool s1 = locate(item, b, t);
 #pragma unroll
     for (int w = 0; w < 3; ++w) {
       if (!(MASK >> w & 1)) continue;
-      const OutSlot& o = a.y[w];
+      if (DUAL && (s1 ? a.j1.x[w] : a.x[w]) == nullptr) continue;  // (uniform per item)
+      const OutSlot& o = s1 ? a.j1.y[w] : a.y[w];
       const int64_t base = (int64_t)b * o.bstride + (int64_t)t * o.tstride;
       if (w == 2) {
 #pragma unroll
@@ -368,22 +384,27 @@ __global__ void rope_table_kernel(float2* __restrict__ tab, int32_t len, const P
 
 }  // namespace
 
-template <int D, int MASK>
+template <int D, int MASK, bool DUAL = false>
 cudaError_t launch_loop(const PrologueArgs& a, cudaStream_t s) {
   static int grid_cap = 0;
   if (grid_cap == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_loop_kernel<D, MASK>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_loop_kernel<D, MASK, DUAL>, 256, 0);
     grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
   }
-  const int items = a.B * a.n;
-  return launch_pdl(prologue_loop_kernel<D, MASK>, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s, a);
+  const int items = a.B * (a.n + (DUAL ? a.j1.n : 0));
+  return launch_pdl(prologue_loop_kernel<D, MASK, DUAL>, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s,
+                    a);
 }
 
 template <int D>
 cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
+  if (a.j1.n > 0) {  // two token sets in one launch (one GPU, H within one pass of the token loop)
+    if (a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
+    return launch_loop<D, 7, true>(a, s);
+  }
   if (a.H <= 3 * (256 / (D / 8))) {
     const int mask = (a.x[0] ? 1 : 0) | (a.x[1] ? 2 : 0) | (a.x[2] ? 4 : 0);
     switch (mask) {

@@ -453,3 +453,97 @@ def test_append_reads_inputs_after_their_producer():
     kc, vc = run.cache.cache_view(0)
     kr, vr = ref.cache.cache_view(0)
     assert torch.equal(kc, kr) and torch.equal(vc, vr)
+
+
+# ------------------------------------------------------- fused append + attend --
+@pytest.mark.parametrize("wname,heads,cached,kind", [("C1", 40, 3, 1), ("C1", 4, 2, 0), ("C0", 2, 1, 1)])
+def test_append_attend_equals_append_then_attend(wname, heads, cached, kind):
+    # dz_append_attend(gt, chunk) == dz_append_kv(gt); dz_attend_chunk(chunk): output, cache contents and
+    # state bitwise (one prologue launch instead of two); kind 0 (CLEAN) also stages for a commit
+    import paper_2602_15922_b200 as dz
+    w = synth.scaled(synth.workload(wname), heads=heads, cached_chunks=cached)
+    n, C = w.chunk_tokens, w.cached_chunks
+    runs = [GpuRun(w, capacity=(C + 2) * n, steps=2) for _ in range(2)]
+    for r in runs:
+        r.fill()
+    s0 = runs[0].streams[0]
+    kg, vg = (runs[0].stack(x, 1) for x in ("cur_k", "cur_v"))           # the ground-truth chunk C
+    pg = synth.chunk_positions(w, C).to(runs[0].dev)
+    q, k, v = synth.draw_qkv(w, 0, C + 1)
+    q, k, v = (x[None].to(runs[0].dev) for x in (q, k, v))
+    pq = synth.chunk_positions(w, C + 1).to(runs[0].dev)
+    runs[0].cache.append(kg, vg, pg, C)
+    a = runs[0].cache.attend(q, k, v, pq, C + 1, kind=kind)
+    b = runs[1].cache.append_attend(kg, vg, pg, C, q, k, v, pq, C + 1, kind=kind)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert runs[0].cache.state() == runs[1].cache.state() == ((C + 1) * n, C + 1, C)
+    for x, y in zip(runs[0].cache.cache_view(0), runs[1].cache.cache_view(0)):
+        assert torch.equal(x, y)
+    if kind == dz.CLEAN:   # the attended clean chunk was staged after the appended one: commit both ways
+        for r in runs:
+            r.cache.commit_staged(C + 1)
+        torch.cuda.synchronize()
+        for x, y in zip(runs[0].cache.cache_view(0), runs[1].cache.cache_view(0)):
+            assert torch.equal(x, y)
+    got = b[0].cpu().double().numpy()
+    gq, gk = runs[0].gq, runs[0].gk
+    want = oracle.attend_chunk(gq, gk, list(s0.cache_k) + [s0.cur_k[1]], list(s0.cache_v) + [s0.cur_v[1]],
+                               list(s0.cache_pos) + [pg.cpu()], q[0].cpu(), k[0].cpu(), v[0].cpu(), pq.cpu(),
+                               w.rope_dims)
+    assert_parity(got, want, "append_attend")
+
+
+def test_append_attend_sliding_window_with_compaction():
+    # the bench's step (append_attend + evict) with no slack: compactions happen inside the fused call;
+    # every attention equals the same attention on a cache built from scratch
+    w = _small(heads=4, cached_chunks=3)
+    n, C = w.chunk_tokens, w.cached_chunks
+    run = GpuRun(w, capacity=C * n, slack=0)
+    run.fill()
+    s0 = run.streams[0]
+    run.cache.evict_front(1)                         # cache: chunks 1 .. C-1
+    extra = [synth.draw_qkv(w, 0, C + i) for i in range(5)]
+    chunks = {c: (s0.cache_k[c], s0.cache_v[c]) for c in range(C)}
+    for i in range(5):
+        chunks[C + i] = tuple(extra[i][1:])
+    outs = []
+    for i in range(4):
+        gt_id, cid = C + i, C + i + 1                # inject chunk C+i, denoise chunk C+i+1
+        kg, vg = chunks[gt_id]
+        q, k, v = extra[i + 1]
+        outs.append(run.cache.append_attend(kg[None].to(run.dev), vg[None].to(run.dev),
+                                            synth.chunk_positions(w, gt_id).to(run.dev), gt_id,
+                                            q[None].to(run.dev), k[None].to(run.dev), v[None].to(run.dev),
+                                            synth.chunk_positions(w, cid).to(run.dev), cid))
+        run.cache.evict_front(1)
+    torch.cuda.synchronize()
+    for i in range(4):
+        cid = C + i + 1
+        fresh = GpuRun(w, capacity=C * n)
+        for j in range(cid - C, cid):                # the window of C chunks the i-th attention saw
+            kk, vv = chunks[j]
+            fresh.cache.append(kk[None].to(fresh.dev), vv[None].to(fresh.dev),
+                               synth.chunk_positions(w, j).to(fresh.dev), j)
+        q, k, v = extra[i + 1]
+        want = fresh.cache.attend(q[None].to(fresh.dev), k[None].to(fresh.dev), v[None].to(fresh.dev),
+                                  synth.chunk_positions(w, cid).to(fresh.dev), cid)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[i], want), f"step {i}"
+
+
+def test_append_attend_validation():
+    import paper_2602_15922_b200 as dz
+    w = _small(heads=4, cached_chunks=1)
+    run = GpuRun(w, capacity=2 * w.chunk_tokens)
+    run.fill()
+    q, k, v = (run.stack(x, 0) for x in ("cur_q", "cur_k", "cur_v"))
+    pos = run.streams[0].cur_pos.to(run.dev)
+    with pytest.raises(dz.DzError) as e:        # the attended chunk must come after the appended one
+        run.cache.append_attend(k, v, pos, 2, q, k, v, pos, 2)
+    assert e.value.status == -4
+    with pytest.raises(dz.DzError) as e:        # capacity: 1 committed + 2 more would exceed 2 chunks
+        run.cache.append(k, v, pos, 1)
+        run.cache.append_attend(k, v, pos, 2, q, k, v, pos, 3)
+    assert e.value.status == -3
+    assert run.cache.state()[1] == 2            # the failed call changed nothing
