@@ -817,7 +817,8 @@ dz_status dz_append_attend(dz_ctx* c, const void* k_gt, const void* v_gt, const 
   if ((r = check_device(c))) return r;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // one launch for both prologues needs the token-loop prologue (one GPU, H within one pass of it)
-  const bool fused = c->N == 1 && c->H <= 3 * (256 / (c->D / 8));
+  static const bool no_fuse = getenv("DZ_NO_FUSED_APPEND") != nullptr;  // diagnostics: the two calls
+  const bool fused = c->N == 1 && c->H <= 3 * (256 / (c->D / 8)) && !no_fuse;
   if (!fused) {
     if ((r = dz_append_kv(c, k_gt, v_gt, gt, stream))) return r;
     return dz_attend_chunk(c, q_raw, k_raw, v_raw, s, out, stream);

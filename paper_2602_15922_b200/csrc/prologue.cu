@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -405,7 +406,8 @@ cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
     if (a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
     return launch_loop<D, 7, true>(a, s);
   }
-  if (a.H <= 3 * (256 / (D / 8))) {
+  static const bool force_ring = getenv("DZ_PRO_RING") != nullptr;  // diagnostics: the TMA-ring kernel
+  if (a.H <= 3 * (256 / (D / 8)) && !force_ring) {
     const int mask = (a.x[0] ? 1 : 0) | (a.x[1] ? 2 : 0) | (a.x[2] ? 4 : 0);
     switch (mask) {
       case 1: return launch_loop<D, 1>(a, s);
