@@ -83,9 +83,18 @@ enum {
   DZ_FLAG_WHOLE_UNITS = 32,   /* no stream-K split: each (batch, head, 256-row query group) is computed
                                  whole by one CTA pair, so its bits do not depend on the unit count
                                  (identical results at every world size, reading A21) */
-  DZ_FLAG_HOST_ONLY = 64      /* planning context: never touches the device (gains unread, the caller's
+  DZ_FLAG_HOST_ONLY = 64,     /* planning context: never touches the device (gains unread, the caller's
                                  max_abs_gain is taken as given); compute calls validate, then
                                  return DZ_ESTATE without enqueuing; dz_sp_plan works (host tests) */
+  DZ_FLAG_PEER_STORE = 128    /* Ulysses without exchange copies: the prologue
+                                 stores each destination rank's Q'/K'/V rows straight into that
+                                 rank's storage and the attention's epilogue stores O rows straight
+                                 into their owner's receive buffer, through the peer storage
+                                 pointers of dz_sp_set_peers (CUDA IPC / NVLink-mapped on a node);
+                                 the exchanges become barriers (a 4-byte NCCL all-reduce, or an
+                                 empty dz_sp_pending list with DZ_FLAG_EXTERNAL_EXCHANGE).
+                                 2 <= world_size <= 8 and at most 48 heads at head_dim 128
+                                 (96 at 64), else DZ_ESHAPE */
 };
 
 typedef struct {
@@ -323,6 +332,12 @@ DZ_API int32_t dz_sp_plan(const dz_ctx* ctx, int32_t phase, int32_t n_tokens, dz
  * the unpack; append: the commit).  Lets a caller use its own transport (and the
  * tests run N ranks on one GPU with one device copy per transfer). */
 DZ_API int32_t dz_sp_pending(const dz_ctx* ctx, int32_t* phase, dz_xfer* out, int32_t cap);
+
+/* DZ_FLAG_PEER_STORE: storages[p] = rank p's cache_storage as addressable from this process (the
+ * peer-mapped pointer on a node; storages[rank] must be this context's own).  Every rank's context
+ * must have the same configuration and see the same sequence of calls.  Required before the first
+ * compute call (else DZ_ESTATE).  Host only. */
+DZ_API dz_status dz_sp_set_peers(dz_ctx* ctx, void* const* storages, int32_t n);
 DZ_API dz_status dz_sp_resume(dz_ctx* ctx, void* stream);
 
 /* K5 (the post-exchange unpack) on its own, for tests: recv bf16

@@ -37,6 +37,7 @@ FLAG_TILE_MAP = 8
 FLAG_EXTERNAL_EXCHANGE = 16
 FLAG_WHOLE_UNITS = 32
 FLAG_HOST_ONLY = 64
+FLAG_PEER_STORE = 128
 
 STATUS = {0: "DZ_OK", -1: "DZ_EINVAL", -2: "DZ_ESHAPE", -3: "DZ_ECAPACITY", -4: "DZ_ESTATE",
           -5: "DZ_ECUDA", -6: "DZ_ENCCL", -7: "DZ_ERANGE"}
@@ -98,6 +99,7 @@ SIGNATURES = [
     ("dz_sp_plan", I32, [P, I32, I32, ctypes.POINTER(DzXfer), I32]),
     ("dz_sp_pending", I32, [P, ctypes.POINTER(I32), ctypes.POINTER(DzXfer), I32]),
     ("dz_sp_resume", I32, [P, P]),
+    ("dz_sp_set_peers", I32, [P, P, I32]),
     ("dz_debug_sp_unpack", I32, [P, P, I32, I32, I32, I32, I32, P]),
     ("dz_debug_watchdog", I32, [P, I32]),
     ("dz_profile_last", I32, [P, P]),
@@ -335,6 +337,11 @@ class ChunkKVCache:
         arr = (DzXfer * max(cnt, 1))()
         lib().dz_sp_pending(self._ctx, ctypes.byref(ph), arr, cnt)
         return ph.value, [(x.peer, x.tensor, x.send_off, x.recv_off, x.bytes) for x in arr[:cnt]]
+
+    def set_peers(self, storages: Sequence[int]):
+        """FLAG_PEER_STORE: every rank's storage base address (as mapped in this process), by rank."""
+        arr = (P * len(storages))(*[int(x) for x in storages])
+        self._check(lib().dz_sp_set_peers(self._ctx, arr, len(storages)), "dz_sp_set_peers")
 
     def sp_resume(self, stream: Optional[torch.cuda.Stream] = None):
         """Continue the suspended call after its pending transfers have been delivered."""

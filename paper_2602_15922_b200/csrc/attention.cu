@@ -340,7 +340,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     __nv_bfloat16* __restrict__ out, int64_t o_bstride,
                     int64_t o_tstride, float* __restrict__ lse, uint8_t* __restrict__ tile_map, int B, int H,
                     int nq, int kv_len, float m_static, int dbg, float* __restrict__ ws, int* __restrict__ ws_cnt,
-                    const __grid_constant__ SpanTable st) {
+                    const __grid_constant__ SpanTable st, const __grid_constant__ PeerMaps pm) {
   using C = Cfg<D, PP>;
   constexpr int BN = C::kBN;  // keys per step (shadows the file-level 256)
   ptx::pdl_launch_dependents();  // the next kernel may take SMs as our CTAs finish (it waits for us)
@@ -680,7 +680,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        ptx::tma_store_4d(&tm_o, sOw, hc * (D / 2), h_, qt_ * BM + quad * 32, b_);
+        const int r0 = qt_ * BM + quad * 32;
+        if (pm.n == 0) {
+          ptx::tma_store_4d(&tm_o, sOw, hc * (D / 2), h_, r0, b_);
+        } else {
+          // peer stores: the 32 rows go to their owners' receive buffers as 4 boxes of 8 rows (owner
+          // boundaries n_loc are multiples of 8, so a box never straddles two owners; an 8-row slice
+          // of the SW128 staging tile is one 1024-byte swizzle atom)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = r0 + 8 * i;
+            if (rr < nq) {
+              const int p = rr / pm.n_loc;
+              ptx::tma_store_4d(&pm.m[p], sOw + i * 8 * D, hc * (D / 2), h_, rr - p * pm.n_loc, b_);
+            }
+          }
+        }
         ptx::bulk_commit_group();
       }
     };
@@ -1021,7 +1036,7 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
   return launch_pdl(k, dim3(a.grid), dim3(kThreads), C::kSmem, s, a.tm_q, a.tm_k, a.tm_v, a.tm_k2, a.tm_v2, a.tm_o,
                     a.cur_step,
                     static_cast<__nv_bfloat16*>(a.out), a.o_bstride, a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq,
-                    a.kv_len, a.m_static, a.debug_flags, a.ws, a.ws_cnt, a.spans);
+                    a.kv_len, a.m_static, a.debug_flags, a.ws, a.ws_cnt, a.spans, a.pm);
 }
 
 }  // namespace

@@ -34,7 +34,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct Layout {  // byte offsets inside the caller's storage
   int64_t slots = 0;
   size_t k_off = 0, v_off = 0, q_off = 0, kc_off = 0, lse_off = 0, sq_off = 0, sk_off = 0, sv_off = 0, ol_off = 0,
-         or_off = 0, map_off = 0, ws_off = 0, cnt_off = 0, cnt_bytes = 0, rope_off = 0, total = 0;
+         or_off = 0, map_off = 0, ws_off = 0, cnt_off = 0, cnt_bytes = 0, rope_off = 0, bar_off = 0, total = 0;
 };
 
 bool basic_cfg_ok(const dz_config* c) {
@@ -89,6 +89,7 @@ Layout make_layout(const dz_config* c) {
     L.sv_off = take(sb);
     L.ol_off = take((size_t)B * mc * Hl * D * 2);                    // O local [B][n][Hl][D]
     L.or_off = take(sb);                                              // O recv [N][B][n_loc][Hl][D]
+    L.bar_off = take(256);                                            // barrier scratch (peer stores)
   }
   L.total = off;
   return L;
@@ -160,6 +161,9 @@ struct dz_ctx {
   bool prof_on = true;  // dz_profile_enable: events are recorded only while on
   bool external_x = false;  // DZ_FLAG_EXTERNAL_EXCHANGE: the caller runs the all-to-all transfers
   bool host_only = false;   // DZ_FLAG_HOST_ONLY: planning context, never touches the device
+  bool peer_mode = false;   // DZ_FLAG_PEER_STORE: stores into the peers' storages instead of exchanges
+  bool peers_set = false;
+  char* peers[dz::kMaxPeers] = {};  // every rank's cache_storage base (dz_sp_set_peers)
   float max_gain = 0.f;     // max |g| over q_gain and k_gain (read from the device at create)
   // An operation suspended at an exchange point (DZ_FLAG_EXTERNAL_EXCHANGE): the caller runs
   // `plan` (dz_sp_pending), then dz_sp_resume enqueues the rest.
@@ -271,6 +275,7 @@ dz_status check_ready(dz_ctx* c) {
 // a planning context (DZ_FLAG_HOST_ONLY) validates a compute call, then refuses to enqueue it
 dz_status check_device(dz_ctx* c) {
   if (c->host_only) return fail(c, DZ_ESTATE, "host-only (planning) context: nothing is enqueued");
+  if (c->peer_mode && !c->peers_set) return fail(c, DZ_ESTATE, "DZ_FLAG_PEER_STORE: dz_sp_set_peers first");
   return DZ_OK;
 }
 
@@ -278,6 +283,8 @@ dz_status check_span(dz_ctx* c, const dz_span* s) {
   if (!s || !s->pos_thw) return fail(c, DZ_EINVAL, "null span or positions");
   if (s->kind != DZ_CLEAN && s->kind != DZ_NOISY) return fail(c, DZ_EINVAL, "bad span kind %d", s->kind);
   if (s->n_tokens <= 0 || s->n_tokens % c->N) return fail(c, DZ_ESHAPE, "n_tokens %d not a positive multiple of world_size %d", s->n_tokens, c->N);
+  if (c->peer_mode && (s->n_tokens / c->N) % 8)
+    return fail(c, DZ_ESHAPE, "DZ_FLAG_PEER_STORE: n_tokens / world_size = %d is not a multiple of 8", s->n_tokens / c->N);
   if (s->n_tokens > c->cfg.max_chunk_tokens)
     return fail(c, DZ_ECAPACITY, "chunk of %d tokens exceeds max_chunk_tokens %d", s->n_tokens, c->cfg.max_chunk_tokens);
   if (s->chunk_id <= c->last_id)
@@ -365,6 +372,20 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
     a.y[0] = {c->base + c->L.sq_off, bst, tst, dst};
     a.y[1] = {c->base + c->L.sk_off, bst, tst, dst};
     a.y[2] = {c->base + c->L.sv_off, bst, tst, dst};
+    if (c->peer_mode) {
+      // straight into rank p's receive locations (the recv_off of dz_sp_plan): Q' scratch rows
+      // [rank * n_loc, ...) of [B][n][Hl][D], K'/V staging slots start + valid + rank * n_loc + t
+      a.peer = 1;
+      const int64_t row = (int64_t)c->Hl * c->D * 2, slot = c->start + c->valid + (int64_t)c->rank * n_loc;
+      a.y[0] = {nullptr, n * tst, tst, 0};
+      a.y[1] = {nullptr, c->L.slots * tst, tst, 0};
+      a.y[2] = {nullptr, c->L.slots * tst, tst, 0};
+      for (int p = 0; p < c->N; ++p) {
+        a.peer_y[0][p] = c->peers[p] + c->L.q_off + (int64_t)c->rank * n_loc * row;
+        a.peer_y[1][p] = c->peers[p] + c->L.k_off + slot * row;
+        a.peer_y[2][p] = c->peers[p] + c->L.v_off + slot * row;
+      }
+    }
   }
   a.rope_tab = reinterpret_cast<const float2*>(c->base + c->L.rope_off);
   a.rope_len = dz::kRopeLen;
@@ -384,6 +405,10 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
 
 // one grouped NCCL send/recv per plan entry (all peers, all tensors) on the caller's stream
 dz_status run_exchange(dz_ctx* c, int phase, int64_t n, cudaStream_t st) {
+  if (c->peer_mode) {  // peer stores put the data in place: only order the ranks (a 4-byte all-reduce)
+    void* flag = c->base + c->L.bar_off;
+    return nccl_check(c, ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, c->comm, st), "ncclAllReduce (barrier)");
+  }
   const std::vector<dz_xfer> plan = make_plan(c, phase, n);
   dz_status r = nccl_check(c, ncclGroupStart(), "ncclGroupStart");
   if (r) return r;
@@ -426,6 +451,15 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
                    (uint32_t)step_keys))
       return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (new tokens) failed");
     a.cur_step = (int32_t)(c->valid / step_keys);
+  }
+  if (c->peer_mode && c->N > 1) {  // O rows to their owners' receive buffers ([N][B][n_loc][Hl][D], block `rank`)
+    const int64_t n_loc = n / c->N, blk = (int64_t)c->B * n_loc * c->Hl * c->D * 2;
+    a.pm.n = c->N;
+    a.pm.n_loc = (int32_t)n_loc;
+    for (int p = 0; p < c->N; ++p)
+      if (!make_tmap(&a.pm.m[p], c->peers[p] + c->L.or_off + (int64_t)c->rank * blk, true, c->D, c->Hl, n_loc, c->B,
+                     n_loc * c->Hl * c->D, (uint32_t)c->D / 2, 8))
+        return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (peer O) failed");
   }
   a.out = out_local;
   a.o_bstride = o_bstride;
@@ -522,6 +556,12 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   Layout L = make_layout(cfg);
   if (cfg->cache_bytes < L.total) return DZ_ECAPACITY;
 
+  if (cfg->flags & DZ_FLAG_PEER_STORE) {  // one node, the token-loop prologue (H within one pass of it);
+    // the epilogue's 8-row O boxes need owner boundaries (n / world_size) on multiples of 8
+    if (cfg->world_size < 2 || cfg->world_size > dz::kMaxPeers || cfg->heads > 3 * (256 / (cfg->head_dim / 8)) ||
+        (cfg->max_chunk_tokens / cfg->world_size) % 8)
+      return DZ_ESHAPE;
+  }
   dz_ctx* c = new (std::nothrow) dz_ctx();
   if (!c) return DZ_ECUDA;
   c->cfg = *cfg;
@@ -538,6 +578,7 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   c->base = static_cast<char*>(cfg->cache_storage);
   c->comm = static_cast<ncclComm_t>(cfg->nccl_comm);
   c->external_x = external_x;
+  c->peer_mode = (cfg->flags & DZ_FLAG_PEER_STORE) != 0;
   c->host_only = host_only;
   c->max_gain = (float)gmax;
   int dev = 0;
@@ -592,7 +633,8 @@ void suspend(dz_ctx* c, int op, int phase, int64_t n) {
   c->pend.op = op;
   c->pend.phase = phase;
   c->pend.n = n;
-  c->pend.plan = make_plan(c, phase, n);
+  // peer stores: the data is already in place; the caller only orders the ranks (a barrier)
+  if (c->peer_mode) c->pend.plan.clear(); else c->pend.plan = make_plan(c, phase, n);
 }
 
 }  // namespace
@@ -785,6 +827,8 @@ dz_status dz_attend_spans(dz_ctx* c, const void* q_raw, const void* k_raw, const
     n += s.n_tokens;
   }
   if (n % c->N) return fail(c, DZ_ESHAPE, "%lld tokens not a multiple of world_size %d", (long long)n, c->N);
+  if (c->peer_mode && (n / c->N) % 8)
+    return fail(c, DZ_ESHAPE, "DZ_FLAG_PEER_STORE: %lld tokens per rank is not a multiple of 8", (long long)(n / c->N));
   if (n > c->cfg.max_chunk_tokens)
     return fail(c, DZ_ECAPACITY, "%lld span tokens exceed max_chunk_tokens %d", (long long)n, c->cfg.max_chunk_tokens);
   if (n_spans > 1) {  // K2 keeps the (query group, key step) classes of a span layout in a 65536-tile table
@@ -833,6 +877,20 @@ dz_status dz_append_attend(dz_ctx* c, const void* k_gt, const void* v_gt, const 
   aj.n = gt->n_tokens;
   return attend_impl(c, q_raw, k_raw, v_raw, s->pos_thw, s->n_tokens, t, out, s->kind == DZ_CLEAN, s->chunk_id,
                      s->kind, st, &aj, gt->chunk_id);
+}
+
+dz_status dz_sp_set_peers(dz_ctx* c, void* const* storages, int32_t n) {
+  if (!c || !storages) return DZ_EINVAL;
+  if (!c->peer_mode) return fail(c, DZ_ESTATE, "created without DZ_FLAG_PEER_STORE");
+  if (n != c->N) return fail(c, DZ_EINVAL, "%d peer storages for world_size %d", n, c->N);
+  for (int p = 0; p < n; ++p) {
+    if (!storages[p] || (reinterpret_cast<uintptr_t>(storages[p]) & (kAlign - 1)))
+      return fail(c, DZ_EINVAL, "peer %d storage null or not 256-byte aligned", p);
+    c->peers[p] = static_cast<char*>(storages[p]);
+  }
+  if (c->peers[c->rank] != c->base) return fail(c, DZ_EINVAL, "entry %d must be this rank's cache_storage", c->rank);
+  c->peers_set = true;
+  return DZ_OK;
 }
 
 int32_t dz_sp_pending(const dz_ctx* c, int32_t* phase, dz_xfer* out, int32_t cap) {

@@ -46,8 +46,14 @@ struct PrologueJob {
   int32_t n = 0;
 };
 
+constexpr int kMaxPeers = 8;  // Ulysses ranks of one node
+
 struct PrologueArgs {
   PrologueJob j1;                                  // optional second token set (j1.n > 0)
+  // peer stores (DZ_FLAG_PEER_STORE): output rows of destination rank p go to peer_y[w][p] +
+  // b*bstride + t*tstride + (h % heads_per_dest)*D (y[w].dstride unused); null: y[w].base as usual
+  void* peer_y[3][kMaxPeers] = {};
+  int32_t peer = 0;
   const void* x[3] = {nullptr, nullptr, nullptr};  // raw bf16 q, k, v: [B][n][H][D]
   int64_t x_bstride = 0;                           // elements between batch elements
   const int32_t* pos = nullptr;                    // [n][3] (t, h, w)
@@ -84,8 +90,17 @@ struct SpanTable {
   int32_t qth[kMaxSpans] = {};
 };
 
+// K2 epilogue stores to the owners of the query rows (DZ_FLAG_PEER_STORE): rows [p*n_loc, (p+1)*n_loc)
+// of this rank's head shard go to rank p's receive buffer through m[p], dims (D, H/N, n_loc, B).
+struct PeerMaps {
+  CUtensorMap m[kMaxPeers];
+  int32_t n = 0;       // 0: O goes to tm_o
+  int32_t n_loc = 0;
+};
+
 struct AttnArgs {
   SpanTable spans;
+  PeerMaps pm;
   CUtensorMap tm_q;   // Q' fp16, dims (D, H, nq, B), box (64, 1, 128, 1), SW128
   CUtensorMap tm_k;   // K' fp16 cache, dims (D, H, kv_len, B)
   CUtensorMap tm_v;   // V  bf16 cache, dims (D, H, kv_len, B)

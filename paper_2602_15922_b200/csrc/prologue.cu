@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
 // 24.2 -> 22.4 us, append 19.7 -> 17.1 us at C1.)
 // DUAL: a second token set (a.j1, one GPU) follows the first in the item sequence; MASK is then the
 // union of both sets' tensors and a tensor absent from an item's set (x[w] == nullptr) is skipped.
-template <int D, int MASK, bool DUAL>
+// PEER: rows go straight to the destination ranks' buffers (a.peer_y, DZ_FLAG_PEER_STORE).
+template <int D, int MASK, bool DUAL, bool PEER = false>
 __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(const PrologueArgs a) {
   constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
   ptx::pdl_launch_dependents();
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
   const int64_t tokD = (int64_t)H * D;
   // per (tensor, head slot): output offset inside the token's block, in elements
   int64_t ooff[3][kPer];
+  void* pbase[3][kPer];  // PEER: the destination rank's buffer of (tensor, head slot)
   bool hv[kPer];
 #pragma unroll
   for (int i = 0; i < kPer; ++i) {
@@ -268,7 +270,10 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
     const int dest = h / a.heads_per_dest;
 #pragma unroll
     for (int w = 0; w < 3; ++w)
-      if (MASK >> w & 1) ooff[w][i] = (int64_t)dest * a.y[w].dstride + (int64_t)(h - dest * a.heads_per_dest) * D + li * 8;
+      if (MASK >> w & 1) {
+        ooff[w][i] = (PEER ? 0 : (int64_t)dest * a.y[w].dstride) + (int64_t)(h - dest * a.heads_per_dest) * D + li * 8;
+        pbase[w][i] = PEER && hv[i] ? a.peer_y[w][dest] : nullptr;
+      }
   }
   auto load = [&](int item, uint4 (&v)[3][kPer]) {
     int b, t;
@@ -333,7 +338,9 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
       if (w == 2) {
 #pragma unroll
         for (int i = 0; i < kPer; ++i)
-          if (hv[i]) reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(o.base) + base + ooff[w][i])[0] = v[w][i];
+          if (hv[i])
+            reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(PEER ? pbase[w][i] : o.base) + base + ooff[w][i])[0] =
+                v[w][i];
         continue;
       }
       float ss[kPer];
@@ -362,7 +369,7 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
-        reinterpret_cast<uint4*>(static_cast<__half*>(o.base) + base + ooff[w][i])[0] =
+        reinterpret_cast<uint4*>(static_cast<__half*>(PEER ? pbase[w][i] : o.base) + base + ooff[w][i])[0] =
             make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
     }
@@ -385,23 +392,28 @@ __global__ void rope_table_kernel(float2* __restrict__ tab, int32_t len, const P
 
 }  // namespace
 
-template <int D, int MASK, bool DUAL = false>
+template <int D, int MASK, bool DUAL = false, bool PEER = false>
 cudaError_t launch_loop(const PrologueArgs& a, cudaStream_t s) {
   static int grid_cap = 0;
   if (grid_cap == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_loop_kernel<D, MASK, DUAL>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_loop_kernel<D, MASK, DUAL, PEER>, 256, 0);
     grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
   }
   const int items = a.B * (a.n + (DUAL ? a.j1.n : 0));
-  return launch_pdl(prologue_loop_kernel<D, MASK, DUAL>, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s,
-                    a);
+  return launch_pdl(prologue_loop_kernel<D, MASK, DUAL, PEER>, dim3((unsigned)std::min(items, grid_cap)), dim3(256),
+                    0, s, a);
 }
 
 template <int D>
 cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
+  if (a.peer) {  // peer stores (Ulysses, one node): q, k, v (attend) or k, v (append); token loop only
+    if (a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
+    if (a.x[0]) return launch_loop<D, 7, false, true>(a, s);
+    return launch_loop<D, 6, false, true>(a, s);
+  }
   if (a.j1.n > 0) {  // two token sets in one launch (one GPU, H within one pass of the token loop)
     if (a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
     return launch_loop<D, 7, true>(a, s);

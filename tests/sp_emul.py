@@ -7,7 +7,8 @@ per transfer between the ranks' storages, then resumes every rank.  Everything
 the N-GPU path runs -- K1 writing the [N][B][n/N][H/N][D] send layout, the
 exchange plan, K2 on a head shard over the head-sharded cache, the O exchange
 and the K5 unpack -- runs here; only the transport (NCCL send/recv over
-NVLink) is replaced by cudaMemcpyAsync.  No kernel waits on another rank's
+NVLink) is replaced by cudaMemcpyAsync.  With peer=True (DZ_FLAG_PEER_STORE, NEXT-3) there is no
+transfer at all: the kernels store into the other ranks' storages and the exchanges are barriers.  No kernel waits on another rank's
 kernel: the ranks' stages are enqueued one after the other on one stream.
 """
 from __future__ import annotations
@@ -21,7 +22,7 @@ import synth
 
 class SpRanks:
     def __init__(self, w: synth.Workload, N: int, gq: torch.Tensor, gk: torch.Tensor, dev, capacity=None,
-                 slack=0, flags=0, batch=None, max_chunk=None):
+                 slack=0, flags=0, batch=None, max_chunk=None, peer=False):
         import paper_2602_15922_b200 as dz
         self.dz, self.w, self.N, self.dev = dz, w, N, torch.device(dev)
         self.batch = w.batch if batch is None else batch
@@ -30,8 +31,13 @@ class SpRanks:
         self.caches = [dz.ChunkKVCache(self.batch, w.heads, w.head_dim, cap, mc, w.rope_dims, gq.to(self.dev),
                                        gk.to(self.dev), rope_theta=w.rope_theta, rms_eps=w.rms_eps,
                                        window_slack=slack, world_size=N, rank=r,
-                                       flags=flags | dz.FLAG_EXTERNAL_EXCHANGE, device=self.dev)
+                                       flags=flags | dz.FLAG_EXTERNAL_EXCHANGE | (dz.FLAG_PEER_STORE if peer else 0),
+                                       device=self.dev)
                        for r in range(N)]
+        if peer:   # NEXT-3: every rank stores into the others' storages (here: the same GPU's memory)
+            bases = [c.storage.data_ptr() for c in self.caches]
+            for c in self.caches:
+                c.set_peers(bases)
         self.transfers = 0
         self.phases = []
 

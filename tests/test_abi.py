@@ -163,3 +163,31 @@ def test_external_exchange_allows_sp_without_nccl():
     assert L.dz_create(ctypes.byref(c), ctypes.byref(ctx)) == 0
     assert L.dz_sp_plan(ctx, 0, 128, None, 0) == 3 * 2
     L.dz_destroy(ctx)
+
+
+def test_peer_store_validation():
+    # DZ_FLAG_PEER_STORE (NEXT-3): 2..8 ranks, token-loop prologue heads, n / world_size a multiple of 8;
+    # compute calls need dz_sp_set_peers first, whose entry `rank` must be the context's own storage
+    L = dz.lib()
+    bad = _cfg(world_size=1)
+    bad.flags |= dz.FLAG_PEER_STORE
+    bad.cache_storage, bad.cache_bytes = 0x100000, 1 << 40
+    ctx = ctypes.c_void_p()
+    assert L.dz_create(ctypes.byref(bad), ctypes.byref(ctx)) == -2
+    c = _cfg(world_size=2, rank=1, nccl_comm=1)
+    c.flags |= dz.FLAG_PEER_STORE
+    c.cache_storage = 0x100000
+    c.cache_bytes = L.dz_cache_bytes(ctypes.byref(c))
+    assert L.dz_create(ctypes.byref(c), ctypes.byref(ctx)) == 0
+    try:
+        span = dz.DzSpan(0, dz.NOISY, 128, 0x200000)
+        assert L.dz_attend_chunk(ctx, 0x300000, 0x300000, 0x300000, ctypes.byref(span), 0x300000, None) == -4
+        peers = (ctypes.c_void_p * 2)(0x200000, 0x100000)
+        assert L.dz_sp_set_peers(ctx, peers, 1) == -1              # one entry per rank
+        wrong = (ctypes.c_void_p * 2)(0x100000, 0x200000)
+        assert L.dz_sp_set_peers(ctx, wrong, 2) == -1              # entry 1 must be this rank's storage
+        assert L.dz_sp_set_peers(ctx, peers, 2) == 0
+        odd = dz.DzSpan(0, dz.NOISY, 2 * 60, 0x200000)             # 60 tokens per rank: not a multiple of 8
+        assert L.dz_attend_chunk(ctx, 0x300000, 0x300000, 0x300000, ctypes.byref(odd), 0x300000, None) == -2
+    finally:
+        L.dz_destroy(ctx)

@@ -52,17 +52,20 @@ def _check_caches(w, single: GpuRun, sp: SpRanks):
             assert torch.equal(vr, v1[:, r * Hl:(r + 1) * Hl]), f"rank {r} b {b}: V differs from the 1-GPU cache"
 
 
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("N", [2, 4, 8])
-def test_sp_bitwise_equals_single_gpu_c1(N):
+def test_sp_bitwise_equals_single_gpu_c1(N, peer):
     import paper_2602_15922_b200 as dz
     w = synth.workload("C1")
     single = GpuRun(w, flags=dz.FLAG_WHOLE_UNITS)
-    sp = SpRanks(w, N, single.gq, single.gk, DEV, flags=dz.FLAG_WHOLE_UNITS)
+    sp = SpRanks(w, N, single.gq, single.gk, DEV, flags=dz.FLAG_WHOLE_UNITS, peer=peer)
     _fill_both(w, single, sp)
     _check_caches(w, single, sp)
     a, b = _attend_both(w, single, sp)
     assert sp.phases[-2:] == [0, 2], sp.phases   # attend: pre-exchange then post-exchange
     assert torch.equal(a, b), f"N={N}: SP output differs from the 1-GPU output"
+    if peer:
+        assert sp.transfers == 0, "peer stores: the exchanges must move no bytes"
     got = b[0].cpu().double().numpy()
     for h in (0, w.heads - 1):
         assert_parity(got[:, h:h + 1], single.oracle_out(heads=(h, h + 1)), f"SP N={N} head {h}")
@@ -85,12 +88,13 @@ def test_sp_default_schedule_c1(N):
     sp.close()
 
 
-def test_sp_append_against_oracle():
+@pytest.mark.parametrize("peer", [False, True])
+def test_sp_append_against_oracle(peer):
     # phase-1 exchange: rank r's cache holds K' / V of heads [r*Hl, (r+1)*Hl) of every token
     w = synth.scaled(synth.workload("C1"), cached_chunks=2)
     N = 4
     gq, gk = synth.draw_gains(w)
-    sp = SpRanks(w, N, gq, gk, DEV)
+    sp = SpRanks(w, N, gq, gk, DEV, peer=peer)
     s = synth.draw_stream(w, 0)
     for c in range(w.cached_chunks):
         sp.append(s.cache_k[c][None], s.cache_v[c][None], s.cache_pos[c], c)
@@ -109,14 +113,14 @@ def test_sp_append_against_oracle():
     sp.close()
 
 
-@pytest.mark.parametrize("N", [2, 4, 8])
-def test_sp_c4_against_oracle_and_single_gpu(N):
+@pytest.mark.parametrize("N,peer", [(2, False), (4, False), (8, False), (8, True)])
+def test_sp_c4_against_oracle_and_single_gpu(N, peer):
     # BASELINE C4: 32 cached chunks of 2688 tokens, 40/N heads per rank; oracle on heads 0 and 39
     # (ranks 0 and N-1) at sampled query rows; the N-rank output against the 1-GPU run
     import paper_2602_15922_b200 as dz
     w = synth.workload("C4")
     single = GpuRun(w, flags=dz.FLAG_WHOLE_UNITS)
-    sp = SpRanks(w, N, single.gq, single.gk, DEV, flags=dz.FLAG_WHOLE_UNITS)
+    sp = SpRanks(w, N, single.gq, single.gk, DEV, flags=dz.FLAG_WHOLE_UNITS, peer=peer)
     _fill_both(w, single, sp)
     a, b = _attend_both(w, single, sp)
     assert torch.equal(a, b), f"C4 N={N}: SP output differs from the 1-GPU output"
@@ -129,14 +133,15 @@ def test_sp_c4_against_oracle_and_single_gpu(N):
     sp.close()
 
 
-def test_sp_gt_injection_and_window():
+@pytest.mark.parametrize("peer", [False, True])
+def test_sp_gt_injection_and_window(peer):
     # under SP: attend a clean chunk then commit its staged (exchanged) K'/V; evict the oldest
     # chunk (compaction with no slack); the next attention equals the 1-GPU one bitwise
     import paper_2602_15922_b200 as dz
     w = synth.scaled(synth.workload("C1"), heads=8, cached_chunks=2)
     N, C, n = 4, 2, w.chunk_tokens
     single = GpuRun(w, capacity=3 * n, flags=dz.FLAG_WHOLE_UNITS, steps=2)
-    sp = SpRanks(w, N, single.gq, single.gk, DEV, capacity=3 * n, flags=dz.FLAG_WHOLE_UNITS)
+    sp = SpRanks(w, N, single.gq, single.gk, DEV, capacity=3 * n, flags=dz.FLAG_WHOLE_UNITS, peer=peer)
     _fill_both(w, single, sp)
     s0 = single.streams[0]
     q, k, v = (_stack(single, x, 0) for x in ("cur_q", "cur_k", "cur_v"))
@@ -158,7 +163,8 @@ def test_sp_gt_injection_and_window():
     sp.close()
 
 
-def test_sp_teacher_forcing_spans():
+@pytest.mark.parametrize("peer", [False, True])
+def test_sp_teacher_forcing_spans(peer):
     # Fig. 10(a) layout under SP: [C0 C1; Z1 Z2], sequence-sharded; equals the 1-GPU call bitwise
     import paper_2602_15922_b200 as dz
     w = synth.scaled(synth.workload("C1"), heads=8, cached_chunks=0)
@@ -171,7 +177,7 @@ def test_sp_teacher_forcing_spans():
     one = dz.ChunkKVCache(1, w.heads, w.head_dim, 0, 4 * n, w.rope_dims, gq.to(DEV), gk.to(DEV),
                           flags=dz.FLAG_WHOLE_UNITS, device=DEV)
     a = one.attend_spans(q.to(DEV), k.to(DEV), v.to(DEV), pos.to(DEV), sl)
-    sp = SpRanks(w, N, gq, gk, DEV, capacity=0, max_chunk=4 * n, flags=dz.FLAG_WHOLE_UNITS)
+    sp = SpRanks(w, N, gq, gk, DEV, capacity=0, max_chunk=4 * n, flags=dz.FLAG_WHOLE_UNITS, peer=peer)
     b = sp.attend_spans(q, k, v, pos, sl)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
