@@ -377,9 +377,9 @@ def secondary(dz, dev, steps, timer: Timer):
     peak, _, hbm, _ = peaks()
     out = {}
 
-    def chunk_line(w, name):
+    def chunk_line(w, name, extra_flags=0):
         gq, gk = synth.draw_gains(w)
-        cache = make_cache(dz, w, dev, gq, gk, flags=dz.FLAG_PROFILE)
+        cache = make_cache(dz, w, dev, gq, gk, flags=dz.FLAG_PROFILE | extra_flags)
         C = w.cached_chunks
         for c in range(C - 1):
             _, k, v = device_inputs(w, dev, w.batch, 10_000 + c)
@@ -402,10 +402,17 @@ def secondary(dz, dev, steps, timer: Timer):
         # the fused prologue reads k_gt, v_gt, q, k and writes K', V (cache) and Q', K' (noisy chunk)
         pro_bytes = 2 * 4 * w.batch * w.chunk_tokens * w.heads * w.head_dim * 2
         pro = statistics.median(prof["prologue"])
+        pk = peak
+        if extra_flags & dz.FLAG_FP8_QK:
+            # half the useful FLOP (QK^T) at the FP8 rate, half (PV) at bf16: the mix's peak is
+            # 2 / (1/P8 + 1/P16) with P8 = 2 x the measured bf16 peak (the nominal dense FP8:BF16
+            # ratio, 4.5 : 2.25 PFLOP/s; no FP8 GEMM was measured) = 4/3 x 1630.3
+            pk = peak * 4.0 / 3.0
         out[name] = {"workload": w.name, "mode": "chunk (append_attend + evict)",
                      "step_tflops": flop / (statistics.median(sm) * 1e-3) / 1e12,
                      "step_ms": spread(sm), "k2_ms": spread(prof["attention"]),
-                     "k2_tflops": flop / (k2 * 1e-3) / 1e12, "k2_frac": flop / (k2 * 1e-3) / 1e12 / peak,
+                     "k2_tflops": flop / (k2 * 1e-3) / 1e12, "k2_frac": flop / (k2 * 1e-3) / 1e12 / pk,
+                     "k2_peak": pk,
                      "prologue_ms": spread(prof["prologue"]), "prologue_gbs": pro_bytes / (pro * 1e-3) / 1e9,
                      "prologue_frac_hbm": pro_bytes / (pro * 1e-3) / 1e9 / hbm,
                      "gpu_launches_per_step": launches / steps, "clocks": clk}
@@ -413,6 +420,7 @@ def secondary(dz, dev, steps, timer: Timer):
 
     chunk_line(synth.workload("C2"), "C2")
     chunk_line(synth.workload("C4"), "C4@1")
+    chunk_line(synth.workload("C1"), "C1_fp8_qk", dz.FLAG_FP8_QK)   # NEXT-2: E4M3 QK^T, bf16 PV
 
     # C3: 4 denoising steps x CFG batch 2 over one cache of 8 chunks, one CUDA graph replay
     w = synth.workload("C3")

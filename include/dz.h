@@ -86,6 +86,12 @@ enum {
   DZ_FLAG_HOST_ONLY = 64,     /* planning context: never touches the device (gains unread, the caller's
                                  max_abs_gain is taken as given); compute calls validate, then
                                  return DZ_ESTATE without enqueuing; dz_sp_plan works (host tests) */
+  DZ_FLAG_FP8_QK = 256,       /* Q' and K' (cache and current chunk) stored as
+                                 FP8 E4M3 (times 2^a and 2^-a, a chosen at create from the gains so
+                                 scores need no descale) and QK^T on tcgen05 kind::f8f6f4; PV stays
+                                 bf16.  Its own error budget, not BJ:5.  One GPU,
+                                 head_dim 128, <= 48 heads (else DZ_ESHAPE) and the fixed softmax
+                                 base (else DZ_ERANGE).  dz_cache_view's K' is then E4M3 bytes */
   DZ_FLAG_PEER_STORE = 128    /* Ulysses without exchange copies: the prologue
                                  stores each destination rank's Q'/K'/V rows straight into that
                                  rank's storage and the attention's epilogue stores O rows straight

@@ -38,6 +38,7 @@ FLAG_EXTERNAL_EXCHANGE = 16
 FLAG_WHOLE_UNITS = 32
 FLAG_HOST_ONLY = 64
 FLAG_PEER_STORE = 128
+FLAG_FP8_QK = 256
 
 STATUS = {0: "DZ_OK", -1: "DZ_EINVAL", -2: "DZ_ESHAPE", -3: "DZ_ECAPACITY", -4: "DZ_ESTATE",
           -5: "DZ_ECUDA", -6: "DZ_ENCCL", -7: "DZ_ERANGE"}
@@ -368,12 +369,14 @@ class ChunkKVCache:
         if tokens is None:
             tokens = self.state()[0]
         base = self.storage.data_ptr()
-        nb = tokens * stride.value * 2
 
-        def view(ptr, dt):
+        def view(ptr, dt, es):
             off = ptr - base
-            return self.storage[off:off + nb].view(dt).view(tokens, self.heads_local, self.head_dim)
-        return view(k0.value, torch.float16), view(v0.value, torch.bfloat16)
+            return self.storage[off:off + tokens * stride.value * es].view(dt).view(tokens, self.heads_local,
+                                                                                self.head_dim)
+        fp8 = bool(self._cfg.flags & FLAG_FP8_QK)
+        return (view(k0.value, torch.float8_e4m3fn if fp8 else torch.float16, 1 if fp8 else 2),
+                view(v0.value, torch.bfloat16, 2))
 
     def tile_map(self, with_tiles: bool = False):
         """The kernel's tile decisions of the last attend for (b, h) = (0, 0) (needs FLAG_TILE_MAP):

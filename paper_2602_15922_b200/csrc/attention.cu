@@ -102,12 +102,18 @@ __device__ __forceinline__ uint32_t gtime() {
 // split in two key halves between the two warp groups.
 constexpr int kClsWords = kMaxStepTiles / 16;  // step-class table (several spans): 16 KB static shared memory
 
-template <int D, bool PP>
+// F8 (DZ_FLAG_FP8_QK): Q' and K' are E4M3, one byte per element; QK^T by tcgen05.mma kind::f8f6f4
+// (K = 32 per instruction), PV unchanged (bf16).
+template <int D, bool PP, bool F8 = false>
 struct Cfg {
   static constexpr int kBN = PP ? 128 : 256;               // keys per step
-  static constexpr int kQBoxes = D / 64;                  // 64-column SW128 boxes per Q / K row
-  static constexpr int kQTileBytes = BM * D * 2;          // one CTA's query tile (fp16)
+  static constexpr int kQKBytes = F8 ? 1 : 2;             // bytes per Q' / K' element
+  static constexpr int kQBoxes = D * kQKBytes / 128;      // 128-byte SW128 boxes per Q / K row
+  static constexpr int kBoxElems = 128 / kQKBytes;        // elements of a row per box
+  static constexpr int kQTileBytes = BM * D * kQKBytes;   // one CTA's query tile
   static constexpr int kStageBytes = kBN * D;             // K (kBN/2 keys x D) or V (kBN keys x D/2) per CTA
+  static constexpr int kKBytes = kBN / 2 * D * kQKBytes;  // bytes of a K stage one CTA loads
+  static constexpr int kQKSteps = D * kQKBytes / 32;      // MMAs per QK (32 bytes of K per instruction)
 #ifndef DZ_KST
 #define DZ_KST 4   // measured on C1 (K/V stages), first kernel: 7/5 192.7 us, 6/4 190.3, 5/4 191.0, 5/3 190.0;
 #endif               // current kernel: 6/3 176.5, 5/4 177.5, 5/3 175.4, 4/3 174.2, 4/2 176.8, 3/3 174.8, 3/2 176.9
@@ -127,6 +133,7 @@ struct Cfg {
   static constexpr int kBarOff = kOOff + 8 * 32 * D;
   static constexpr int kSmem = kBarOff + 1024 + 1024;             // + barriers/schedule + alignment slack
   static_assert(kSmem + (kTab ? kClsWords * 4 : 0) <= 232448, "shared memory per CTA");
+  static_assert(8 * 32 * D <= 32768 || !F8, "O staging");
   static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, 2 * BM, BN / 2);  // f16 x f16, K-major, per half
   static constexpr uint32_t kIdescPV = ptx::idesc_f16(1, 1, 0, 1, 2 * BM, D);   // P (TMEM) x V (MN-major)
   static constexpr int kVRowBytes = D;                      // V half row: D/2 bf16
@@ -332,7 +339,7 @@ __device__ __forceinline__ int step_of(const SpanTable& st, int g, int k, int nq
 }
 
 
-template <int D, bool PP>
+template <int D, bool PP, bool F8>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_k2,
@@ -341,7 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     int64_t o_tstride, float* __restrict__ lse, uint8_t* __restrict__ tile_map, int B, int H,
                     int nq, int kv_len, float m_static, int dbg, float* __restrict__ ws, int* __restrict__ ws_cnt,
                     const __grid_constant__ SpanTable st, const __grid_constant__ PeerMaps pm) {
-  using C = Cfg<D, PP>;
+  using C = Cfg<D, PP, F8>;
   constexpr int BN = C::kBN;  // keys per step (shadows the file-level 256)
   ptx::pdl_launch_dependents();  // the next kernel may take SMs as our CTAs finish (it waits for us)
   extern __shared__ uint8_t smem_raw[];
@@ -506,7 +513,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (leader) ptx::mbar_arrive_expect_tx(bar(bars->q_full), min(2, n_qtiles - 2 * g) * C::kQTileBytes);
           if (qt < n_qtiles)  // a tile wholly past nq is not loaded (its rows are never stored)
             for (int x = 0; x < C::kQBoxes; ++x)
-              ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * 64, h, qt * BM, b, pol_q);
+              ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * C::kBoxElems, h, qt * BM, b,
+                                    pol_q);
         }
       }
       int j = step_of<BN, kTab>(st, g, sg.k0, nq, kv_len, nkv);
@@ -523,7 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0 && (dbg & 1)) {  // diagnostics: no K/V traffic, MMAs read stale smem
           if (leader) ptx::mbar_arrive(bar(bars->kv_full[sl]));
         } else if (lane == 0) {
-          if (leader) ptx::mbar_arrive_expect_tx(bar(bars->kv_full[sl]), 2 * C::kStageBytes);
+          if (leader) ptx::mbar_arrive_expect_tx(bar(bars->kv_full[sl]), do_k ? 2 * C::kKBytes : 2 * C::kStageBytes);
           const uint32_t dst = sKV + sl * C::kStageBytes;
           if (do_k) {
             // S half hh (keys 128hh..128hh+127 of the step) takes 64 keys from each CTA:
@@ -535,7 +543,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int hh = 0; hh < BN / 128; ++hh)
               for (int x = 0; x < C::kQBoxes; ++x)
                 ptx::tma_load_4d_2cta(dst + (hh * C::kQBoxes + x) * 64 * 128, tk, lbar(bars->kv_full[sl]),
-                                      x * 64, h, row0 + 128 * hh, b, pol_kv);
+                                      x * C::kBoxElems, h, row0 + 128 * hh, b, pol_kv);
           } else {
             if (j >= cur_step)  // the new tokens' V, read in place from the caller's input (no staging copy)
               ptx::tma_load_4d_2cta(dst, &tm_v2, lbar(bars->kv_full[sl]), (int)rank * (D / 2), h, (j - cur_step) * BN,
@@ -599,11 +607,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint32_t ka = sKV + k_st * C::kStageBytes + hh * C::kQBoxes * 64 * 128;
               const uint64_t dq0 = ptx::sdesc_sw128(sQ, 16, 1024), dk0 = ptx::sdesc_sw128(ka, 16, 1024);
 #pragma unroll
-              for (int kk = 0; kk < D / 16; ++kk) {
+              for (int kk = 0; kk < C::kQKSteps; ++kk) {
                 const uint32_t qoff = (kk / 4) * (128 * 128) + (kk % 4) * 32;  // Q: 128 rows per box
                 const uint32_t koff = (kk / 4) * (64 * 128) + (kk % 4) * 32;   // K half: 64 rows per box
                 // descriptors: the start address field is addr >> 4 in the low bits, offsets add
-                ptx::mma_ss_2cta(tmem + kColS + sb * 128, dq0 + (qoff >> 4), dk0 + (koff >> 4), C::kIdescQK, kk > 0);
+                if constexpr (F8)  // (the idesc's E4M3 format codes are the f16 kind's F16 codes: 0)
+                  ptx::mma_ss_2cta_f8(tmem + kColS + sb * 128, dq0 + (qoff >> 4), dk0 + (koff >> 4), C::kIdescQK,
+                                      kk > 0);
+                else
+                  ptx::mma_ss_2cta(tmem + kColS + sb * 128, dq0 + (qoff >> 4), dk0 + (koff >> 4), C::kIdescQK, kk > 0);
                 if (tr && j == 9) trace[kTraceSteps * 8 + hh * 8 + kk] = (uint32_t)clock();
               }
               ptx::tc_commit_2cta(bar(bars->s_full[sb]), kBoth);
@@ -1027,10 +1039,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == kWarpTmem) ptx::tmem_dealloc_2cta<512>(tmem);
 }
 
-template <int D, bool PP>
+template <int D, bool PP, bool F8 = false>
 cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
-  using C = Cfg<D, PP>;
-  auto k = attn_fwd_kernel<D, PP>;
+  using C = Cfg<D, PP, F8>;
+  auto k = attn_fwd_kernel<D, PP, F8>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
   if (e != cudaSuccess) return e;
   return launch_pdl(k, dim3(a.grid), dim3(kThreads), C::kSmem, s, a.tm_q, a.tm_k, a.tm_v, a.tm_k2, a.tm_v2, a.tm_o,
@@ -1066,6 +1078,7 @@ int attention_units(int32_t B, int32_t H, int32_t nq) {
 
 cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s) {
   const bool pp = attention_step_keys(a.m_static) == 128;
+  if (a.fp8) return (a.D == 128 && pp) ? launch_t<128, true, true>(a, s) : cudaErrorInvalidValue;
   if (a.D == 128) return pp ? launch_t<128, true>(a, s) : launch_t<128, false>(a, s);
   if (a.D == 64) return pp ? launch_t<64, true>(a, s) : launch_t<64, false>(a, s);
   return cudaErrorInvalidValue;

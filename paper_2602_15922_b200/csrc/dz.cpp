@@ -110,16 +110,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 4D token-major tensor [B][tokens][H][D] (16-bit elements) as TMA dims (D, H, tokens, B),
 // box (box_d, 1, box_t, 1); swizzle = box_d * 2 bytes (128 or 64); out-of-bounds elements read as zero.
-bool make_tmap(CUtensorMap* m, const void* base, bool bf16, int64_t D, int64_t H, int64_t tokens, int64_t B,
+// dt: 0 fp16, 1 bf16 (2-byte elements), 2 E4M3 as uint8 (1-byte elements)
+bool make_tmap(CUtensorMap* m, const void* base, int dt, int64_t D, int64_t H, int64_t tokens, int64_t B,
                int64_t batch_stride_elems, uint32_t box_d, uint32_t box_t) {
   auto fn = encode_fn();
   if (!fn) return false;
+  const int64_t es = dt == 2 ? 1 : 2;
   cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)tokens, (cuuint64_t)B};
-  cuuint64_t strides[3] = {(cuuint64_t)(D * 2), (cuuint64_t)(H * D * 2), (cuuint64_t)(batch_stride_elems * 2)};
+  cuuint64_t strides[3] = {(cuuint64_t)(D * es), (cuuint64_t)(H * D * es), (cuuint64_t)(batch_stride_elems * es)};
   cuuint32_t box[4] = {box_d, 1, box_t, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUtensorMapSwizzle sw = box_d * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+  const CUtensorMapSwizzle sw = box_d * es == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const CUtensorMapDataType ty = dt == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : dt == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUresult r = fn(m, ty, 4,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -180,8 +184,11 @@ struct dz_ctx {
   } pend;
   std::string err;
 
+  bool f8 = false;          // DZ_FLAG_FP8_QK: Q' and K' (cache and current chunk) are E4M3
+  float f8_mul[2] = {1.f, 1.f};  // power-of-two factors on Q' and K' (product 1)
+  int64_t krow() const { return (int64_t)Hl * D * (f8 ? 1 : 2); }  // bytes of one slot of K'
   void* kslot(int b, int64_t slot) const {
-    return base + L.k_off + ((size_t)b * L.slots + slot) * Hl * D * 2;
+    return base + L.k_off + ((size_t)b * L.slots + slot) * krow();
   }
   void* vslot(int b, int64_t slot) const {
     return base + L.v_off + ((size_t)b * L.slots + slot) * Hl * D * 2;
@@ -300,7 +307,6 @@ dz_status ensure_staging_room(dz_ctx* c, cudaStream_t st, int64_t extra = 0) {
     c->start = 0;
     return DZ_OK;
   }
-  const size_t row = (size_t)c->Hl * c->D * 2;
   const int64_t s0 = c->start;
   for (int b = 0; b < c->B; ++b) {
     for (int kv = 0; kv < 2; ++kv) {
@@ -309,6 +315,7 @@ dz_status ensure_staging_room(dz_ctx* c, cudaStream_t st, int64_t extra = 0) {
         const int64_t len = std::min<int64_t>(s0, c->valid - done);
         void* dst = kv == 0 ? c->kslot(b, done) : c->vslot(b, done);
         const void* src = kv == 0 ? c->kslot(b, s0 + done) : c->vslot(b, s0 + done);
+        const size_t row = kv == 0 ? (size_t)c->krow() : (size_t)c->Hl * c->D * 2;
         dz_status r = cuda_check(c, cudaMemcpyAsync(dst, src, len * row, cudaMemcpyDeviceToDevice, st), "compact");
         if (r) return r;
       }
@@ -389,6 +396,9 @@ dz_status run_prologue(dz_ctx* c, const void* q, const void* k, const void* v, c
   }
   a.rope_tab = reinterpret_cast<const float2*>(c->base + c->L.rope_off);
   a.rope_len = dz::kRopeLen;
+  a.fp8 = c->f8 ? 1 : 0;
+  a.f8_mul[0] = c->f8_mul[0];
+  a.f8_mul[1] = c->f8_mul[1];
   if (!c->rope_ready) {  // first prologue: fill the table; this prologue waits for it before reading
     dz_status r = cuda_check(c, dz::launch_rope_table(reinterpret_cast<float2*>(c->base + c->L.rope_off),
                                                       dz::kRopeLen, a, st), "rope table launch");
@@ -435,19 +445,23 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   const int64_t bs = c->L.slots * c->Hl * c->D;
   // Q: 128-row tiles per CTA; K: each CTA of a pair loads 2 x 64 of a step's 256 keys;
   // V: each CTA loads D/2 of the columns of all 256 keys (see attention.cu).
-  if (!make_tmap(&a.tm_q, c->base + c->L.q_off, false, c->D, c->Hl, n, c->B, n * c->Hl * c->D, 64, 128) ||
-      !make_tmap(&a.tm_k, c->kslot(0, c->start), false, c->D, c->Hl, kv_len, c->B, bs, 64, 64) ||
-      !make_tmap(&a.tm_v, c->vslot(0, c->start), true, c->D, c->Hl, kv_len, c->B, bs, (uint32_t)c->D / 2,
+  // FP8 QK: Q' / K' are E4M3 rows of D bytes: one 128-byte SW128 box per row
+  const int qk_dt = c->f8 ? 2 : 0;
+  const uint32_t qk_box = c->f8 ? (uint32_t)c->D : 64u;
+  a.fp8 = c->f8 ? 1 : 0;
+  if (!make_tmap(&a.tm_q, c->base + c->L.q_off, qk_dt, c->D, c->Hl, n, c->B, n * c->Hl * c->D, qk_box, 128) ||
+      !make_tmap(&a.tm_k, c->kslot(0, c->start), qk_dt, c->D, c->Hl, kv_len, c->B, bs, qk_box, 64) ||
+      !make_tmap(&a.tm_v, c->vslot(0, c->start), 1, c->D, c->Hl, kv_len, c->B, bs, (uint32_t)c->D / 2,
                  (uint32_t)dz::attention_step_keys(c->m_static)))
     return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled failed");
   // O rows are token-major with o_tstride == Hl * D (the caller's [B][n][H][D] or the SP local buffer)
   if (o_tstride != (int64_t)c->Hl * c->D ||
-      !make_tmap(&a.tm_o, out_local, true, c->D, c->Hl, n, c->B, o_bstride, (uint32_t)c->D / 2, 32))
+      !make_tmap(&a.tm_o, out_local, 1, c->D, c->Hl, n, c->B, o_bstride, (uint32_t)c->D / 2, 32))
     return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (O) failed");
   if (v_new != nullptr) {  // the new tokens: K' from the current-chunk buffer, V from the caller's input
     const int step_keys = dz::attention_step_keys(c->m_static);
-    if (!make_tmap(&a.tm_k2, k_new, false, c->D, c->Hl, n, c->B, n * c->Hl * c->D, 64, 64) ||
-        !make_tmap(&a.tm_v2, v_new, true, c->D, c->Hl, n, c->B, n * c->Hl * c->D, (uint32_t)c->D / 2,
+    if (!make_tmap(&a.tm_k2, k_new, qk_dt, c->D, c->Hl, n, c->B, n * c->Hl * c->D, qk_box, 64) ||
+        !make_tmap(&a.tm_v2, v_new, 1, c->D, c->Hl, n, c->B, n * c->Hl * c->D, (uint32_t)c->D / 2,
                    (uint32_t)step_keys))
       return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (new tokens) failed");
     a.cur_step = (int32_t)(c->valid / step_keys);
@@ -457,7 +471,7 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
     a.pm.n = c->N;
     a.pm.n_loc = (int32_t)n_loc;
     for (int p = 0; p < c->N; ++p)
-      if (!make_tmap(&a.pm.m[p], c->peers[p] + c->L.or_off + (int64_t)c->rank * blk, true, c->D, c->Hl, n_loc, c->B,
+      if (!make_tmap(&a.pm.m[p], c->peers[p] + c->L.or_off + (int64_t)c->rank * blk, 1, c->D, c->Hl, n_loc, c->B,
                      n_loc * c->Hl * c->D, (uint32_t)c->D / 2, 8))
         return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (peer O) failed");
   }
@@ -556,6 +570,9 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   Layout L = make_layout(cfg);
   if (cfg->cache_bytes < L.total) return DZ_ECAPACITY;
 
+  if (cfg->flags & DZ_FLAG_FP8_QK) {  // E4M3 QK: one GPU, D = 128, the token-loop prologue
+    if (cfg->head_dim != 128 || cfg->world_size != 1 || cfg->heads > 48) return DZ_ESHAPE;
+  }
   if (cfg->flags & DZ_FLAG_PEER_STORE) {  // one node, the token-loop prologue (H within one pass of it);
     // the epilogue's 8-row O boxes need owner boundaries (n / world_size) on multiples of 8
     if (cfg->world_size < 2 || cfg->world_size > dz::kMaxPeers || cfg->heads > 3 * (256 / (cfg->head_dim / 8)) ||
@@ -601,6 +618,25 @@ dz_status dz_create(const dz_config* cfg, dz_ctx** out) {
   {
     const double bound = (double)cfg->head_dim * gmax * gmax * c->scale * 1.4426950408889634 * 1.005;
     c->m_static = (!(cfg->flags & DZ_FLAG_ONLINE_SOFTMAX) && bound <= 60.0) ? (float)std::max(bound, 1.0) : 0.f;  // > 0 selects the fixed base
+  }
+  if (cfg->flags & DZ_FLAG_FP8_QK) {
+    // the fixed softmax base is required (scores stay in [-60, 60] log2 units); Q' * 2^a and
+    // K' * 2^-a as E4M3 with a balancing their bounds (|q'| <= sqrt(D) G scale log2e, |k'| <= sqrt(D) G),
+    // both far inside E4M3's +-448, so the MMA's scores need no descale
+    if (c->m_static <= 0.f) {
+      delete c;
+      return DZ_ERANGE;
+    }
+    const double bq = std::sqrt((double)cfg->head_dim) * gmax * c->scale * 1.4426950408889634;
+    const double bk = std::sqrt((double)cfg->head_dim) * gmax;
+    const int e = (int)std::lround(0.5 * std::log2(bk / bq));
+    c->f8 = true;
+    c->f8_mul[0] = std::ldexp(1.f, e);
+    c->f8_mul[1] = std::ldexp(1.f, -e);
+    if (bq * c->f8_mul[0] > 448.0 || bk * c->f8_mul[1] > 448.0) {
+      delete c;
+      return DZ_ERANGE;
+    }
   }
   if ((cfg->flags & DZ_FLAG_PROFILE) && !host_only) {
     for (auto& e : c->ev)

@@ -62,6 +62,10 @@ struct PrologueArgs {
   int32_t B = 0, n = 0, H = 0, D = 0, heads_per_dest = 0;
   float eps = 1e-6f;
   float q_scale = 1.f;                             // extra factor on Q' (softmax_scale * log2e)
+  // FP8 QK (DZ_FLAG_FP8_QK): Q' and K' are stored as E4M3 (1 byte) after multiplying by the
+  // power-of-two factors f8_mul[0] (Q') and f8_mul[1] (K'), whose product is 1 (scores unchanged)
+  int32_t fp8 = 0;
+  float f8_mul[2] = {1.f, 1.f};
   const float2* rope_tab = nullptr;                // [rope_len][D/2] (cos, sin) of p * omega_j, or null
   int32_t rope_len = 0;                            // positions 0 .. rope_len-1 tabulated (others computed)
   double omega[kMaxHeadDim / 2];                   // per pair j: theta^(-2i/d_a), fp64 (host)
@@ -101,6 +105,7 @@ struct PeerMaps {
 struct AttnArgs {
   SpanTable spans;
   PeerMaps pm;
+  int32_t fp8 = 0;  // 1: Q' and K' are E4M3 (QK^T by tcgen05.mma kind::f8f6f4)
   CUtensorMap tm_q;   // Q' fp16, dims (D, H, nq, B), box (64, 1, 128, 1), SW128
   CUtensorMap tm_k;   // K' fp16 cache, dims (D, H, kv_len, B)
   CUtensorMap tm_v;   // V  bf16 cache, dims (D, H, kv_len, B)

@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
 // DUAL: a second token set (a.j1, one GPU) follows the first in the item sequence; MASK is then the
 // union of both sets' tensors and a tensor absent from an item's set (x[w] == nullptr) is skipped.
 // PEER: rows go straight to the destination ranks' buffers (a.peer_y, DZ_FLAG_PEER_STORE).
-template <int D, int MASK, bool DUAL, bool PEER = false>
+// F8: Q' and K' are stored as E4M3 (DZ_FLAG_FP8_QK; one byte per element, rows of D bytes).
+template <int D, int MASK, bool DUAL, bool PEER = false, bool F8 = false>
 __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(const PrologueArgs a) {
   constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
   ptx::pdl_launch_dependents();
@@ -366,6 +367,17 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
         const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
         const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
         const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        if constexpr (F8) {  // E4M3 rows of D bytes: this thread's 8 elements are 8 bytes
+          uint16_t q8[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            q8[e] = rr::rot_pair_e4m3(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc,
+                                      a.f8_mul[w]);
+          uint8_t* dst = static_cast<uint8_t*>(PEER ? pbase[w][i] : o.base) + base + ooff[w][i];
+          *reinterpret_cast<uint2*>(dst) = make_uint2((uint32_t)q8[0] | ((uint32_t)q8[1] << 16),
+                                                      (uint32_t)q8[2] | ((uint32_t)q8[3] << 16));
+          continue;
+        }
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
@@ -392,23 +404,34 @@ __global__ void rope_table_kernel(float2* __restrict__ tab, int32_t len, const P
 
 }  // namespace
 
-template <int D, int MASK, bool DUAL = false, bool PEER = false>
+template <int D, int MASK, bool DUAL = false, bool PEER = false, bool F8 = false>
 cudaError_t launch_loop(const PrologueArgs& a, cudaStream_t s) {
   static int grid_cap = 0;
   if (grid_cap == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_loop_kernel<D, MASK, DUAL, PEER>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_loop_kernel<D, MASK, DUAL, PEER, F8>, 256, 0);
     grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
   }
   const int items = a.B * (a.n + (DUAL ? a.j1.n : 0));
-  return launch_pdl(prologue_loop_kernel<D, MASK, DUAL, PEER>, dim3((unsigned)std::min(items, grid_cap)), dim3(256),
-                    0, s, a);
+  return launch_pdl(prologue_loop_kernel<D, MASK, DUAL, PEER, F8>, dim3((unsigned)std::min(items, grid_cap)),
+                    dim3(256), 0, s, a);
 }
 
 template <int D>
 cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
+  if (a.fp8) {  // E4M3 Q'/K' (one GPU, token loop): attend (q, k [, v]), append (k, v), both in one launch
+    if (a.peer || a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
+    if (a.j1.n > 0) return launch_loop<D, 7, true, false, true>(a, s);
+    const int mask = (a.x[0] ? 1 : 0) | (a.x[1] ? 2 : 0) | (a.x[2] ? 4 : 0);
+    switch (mask) {
+      case 3: return launch_loop<D, 3, false, false, true>(a, s);
+      case 6: return launch_loop<D, 6, false, false, true>(a, s);
+      case 7: return launch_loop<D, 7, false, false, true>(a, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (a.peer) {  // peer stores (Ulysses, one node): q, k, v (attend) or k, v (append); token loop only
     if (a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
     if (a.x[0]) return launch_loop<D, 7, false, true>(a, s);

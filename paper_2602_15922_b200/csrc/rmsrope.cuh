@@ -63,6 +63,19 @@ __device__ __forceinline__ uint32_t rot_pair(float f0, float f1, float inv, floa
   return pack_half2(a, b);
 }
 
+// FP8 (E4M3) form of rot_pair: the rotated pair times sc, then times f8 (a power of two), rounded to
+// nearest E4M3 with saturation; two bytes (lo = element 2i, hi = element 2i+1)
+__device__ __forceinline__ uint16_t rot_pair_e4m3(float f0, float f1, float inv, float g0, float g1, float2 cs,
+                                                  float sc, float f8) {
+  const float u = __fmul_rn(__fmul_rn(f0, inv), g0);
+  const float x = __fmul_rn(__fmul_rn(f1, inv), g1);
+  const float a = __fmul_rn(__fmul_rn(__fsub_rn(__fmul_rn(u, cs.x), __fmul_rn(x, cs.y)), sc), f8);
+  const float b = __fmul_rn(__fmul_rn(__fadd_rn(__fmul_rn(u, cs.y), __fmul_rn(x, cs.x)), sc), f8);
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(b), "f"(a));
+  return r;
+}
+
 // (cos, sin) of the angle p * omega in fp64, rounded to fp32 (the RoPE table's values; used in place
 // for positions beyond the table)
 __device__ __noinline__ inline float2 rope_cs(int p, double omega) {
