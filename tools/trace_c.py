@@ -7,7 +7,7 @@ import numpy as np, torch, synth
 import paper_2602_15922_b200 as dz
 from helpers import GpuRun
 w = synth.workload(sys.argv[1] if len(sys.argv) > 1 else "C1")
-run = GpuRun(w); run.fill(); run.attend(); torch.cuda.synchronize()
+run = GpuRun(w, flags=int(os.environ.get("DZ_FLAGS", "0"))); run.fill(); run.attend(); torch.cuda.synchronize()
 dz.debug_trace(True); run.attend(); torch.cuda.synchronize()
 tr = dz.debug_trace(False, read=True).astype(np.int64)
 base = tr[0]
