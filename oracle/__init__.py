@@ -16,8 +16,10 @@ and composes its steps in the paper's order:
   Alg. 2 l.601-602) plus the current noisy chunk, which sees all of them and
   itself (Alg. 2 l.584-585, update=False).
 
-Every function is pinned by ``tests/test_oracle_pins.py``.  Parity pinned for
-all functions (no "parity unpinned" entries).
+Every function is pinned by ``tests/test_oracle_pins.py``; the backward
+(``oracle/backward.py``: gradients of the same path for teacher-forced training,
+NEXT-1) by ``tests/test_oracle_backward.py`` against central finite differences of
+this forward.  Parity pinned for all functions (no "parity unpinned" entries).
 """
 from __future__ import annotations
 
