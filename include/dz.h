@@ -92,6 +92,7 @@ enum {
                                  bf16.  Its own error budget, not BJ:5.  One GPU,
                                  head_dim 128, <= 48 heads (else DZ_ESHAPE) and the fixed softmax
                                  base (else DZ_ERANGE).  dz_cache_view's K' is then E4M3 bytes */
+  DZ_FLAG_BACKWARD = 512,     /* allocate the backward workspace (dz_attend_spans_backward) */
   DZ_FLAG_PEER_STORE = 128    /* Ulysses without exchange copies: the prologue
                                  stores each destination rank's Q'/K'/V rows straight into that
                                  rank's storage and the attention's epilogue stores O rows straight
@@ -222,6 +223,20 @@ DZ_API dz_status dz_attend_spans(dz_ctx* ctx, const void* q_raw, const void* k_r
  * DZ_FLAG_EXTERNAL_EXCHANGE (DZ_EINVAL). */
 DZ_API dz_status dz_append_attend(dz_ctx* ctx, const void* k_gt, const void* v_gt, const dz_span* gt, const void* q_raw,
                                   const void* k_raw, const void* v_raw, const dz_span* chunk, void* out, void* stream);
+
+/* Backward of dz_attend_spans for teacher-forced training (PAPER.md l.115-119
+ * "trajectory-level updates", Fig. 10(a) layout [C0 .. C_{M-1}; Z1 .. Z_M], Alg. 1 l.512-553):
+ * given the same q_raw, k_raw, v_raw, positions and spans as the forward, its output `out` and its
+ * natural-log LSE rows `lse` (fp32 [batch][heads][n], DZ_FLAG_WRITE_LSE + dz_copy_lse) and dout =
+ * dL/dout, writes dq_raw, dk_raw, dv_raw = dL/d{q,k,v}_raw (bf16 [batch][n][heads][head_dim]) and
+ * dq_gain, dk_gain = dL/dg (fp32 [heads*head_dim], overwritten), through the RMSNorm, the gains, the
+ * 3D RoPE and the Fig. 10-masked attention.  Key tiles no query sees are never loaded against those
+ * queries.  Needs DZ_FLAG_BACKWARD, one GPU, head_dim 128, the bf16 path (DZ_ESHAPE) and an empty
+ * cache (DZ_ESTATE).  Tolerance against the fp64 oracle: DESIGN.md §4. */
+DZ_API dz_status dz_attend_spans_backward(dz_ctx* ctx, const void* q_raw, const void* k_raw, const void* v_raw,
+                                          const int32_t* pos_thw, const dz_span* spans, int32_t n_spans,
+                                          const void* out, const float* lse, const void* dout, void* dq_raw,
+                                          void* dk_raw, void* dv_raw, float* dq_gain, float* dk_gain, void* stream);
 
 /* Commit the chunk staged by the last dz_attend_chunk (which must have had
  * kind DZ_CLEAN and this chunk_id): the model-side "attend the clean chunk,

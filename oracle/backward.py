@@ -68,12 +68,14 @@ def attention_backward(qn, kn, v, q_tags, k_tags, dout, scale=None):
     nk = kn.shape[0]
     if scale is None:
         scale = D ** -0.5
-    vis = np.zeros((nq, nk), dtype=bool)
-    qc, qk, qs = (oracle._i32(t) for t in q_tags)
-    kc, kk, ks = (oracle._i32(t) for t in k_tags)
-    for s in range(nq):                                            # the oracle's own visibility rule
-        for j in range(nk):
-            vis[s, j] = oracle.visible(int(qc[s]), int(qk[s]), int(qs[s]), int(kc[j]), int(kk[j]), int(ks[j]))
+    # the oracle's own visibility rule (oracle.visible), evaluated once per distinct pair of
+    # (chunk, kind, span) tags and broadcast to the tokens carrying them
+    qtag = np.stack([oracle._i32(t) for t in q_tags], axis=1)
+    ktag = np.stack([oracle._i32(t) for t in k_tags], axis=1)
+    uq, qi = np.unique(qtag, axis=0, return_inverse=True)
+    uk, ki = np.unique(ktag, axis=0, return_inverse=True)
+    table = np.array([[oracle.visible(*map(int, a), *map(int, b)) for b in uk] for a in uq], dtype=bool)
+    vis = table[qi.reshape(-1)][:, ki.reshape(-1)]
     dq, dk, dv = np.zeros_like(qn), np.zeros_like(kn), np.zeros_like(v)
     out = np.zeros_like(qn)
     lse = np.zeros((nq, H))

@@ -39,6 +39,7 @@ FLAG_WHOLE_UNITS = 32
 FLAG_HOST_ONLY = 64
 FLAG_PEER_STORE = 128
 FLAG_FP8_QK = 256
+FLAG_BACKWARD = 512
 
 STATUS = {0: "DZ_OK", -1: "DZ_EINVAL", -2: "DZ_ESHAPE", -3: "DZ_ECAPACITY", -4: "DZ_ESTATE",
           -5: "DZ_ECUDA", -6: "DZ_ENCCL", -7: "DZ_ERANGE"}
@@ -84,6 +85,7 @@ SIGNATURES = [
     ("dz_attend_spans", I32, [P, P, P, P, P, ctypes.POINTER(DzSpan), I32, P, P]),
     ("dz_append_attend", I32, [P, P, P, ctypes.POINTER(DzSpan), P, P, P, ctypes.POINTER(DzSpan), P, P]),
     ("dz_commit_staged", I32, [P, I32, P]),
+    ("dz_attend_spans_backward", I32, [P, P, P, P, P, ctypes.POINTER(DzSpan), I32, P, P, P, P, P, P, P, P, P]),
     ("dz_evict_front", I32, [P, I32, P]),
     ("dz_cache_state", I32, [P, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32)]),
     ("dz_cache_view", I32, [P, I32, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(I64)]),
@@ -347,6 +349,24 @@ class ChunkKVCache:
     def sp_resume(self, stream: Optional[torch.cuda.Stream] = None):
         """Continue the suspended call after its pending transfers have been delivered."""
         self._check(lib().dz_sp_resume(self._ctx, _stream_ptr(stream)), "dz_sp_resume")
+
+    def attend_spans_backward(self, q, k, v, pos, spans, out, lse, dout, stream=None):
+        """Gradients of sum(dout * out) for a teacher-forced span layout (FLAG_BACKWARD, empty cache):
+        returns (dq, dk, dv) bf16 like q and (dq_gain, dk_gain) fp32 [heads, head_dim]."""
+        n_local = q.shape[1]
+        for t, nm in ((q, "q"), (k, "k"), (v, "v"), (out, "out"), (dout, "dout")):
+            self._act(t, nm, n_local)
+        _need(pos, "pos", torch.int32, (n_local, 3), self.device)
+        _need(lse, "lse", torch.float32, (self.batch, self.heads_local, n_local), self.device)
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        dgq = torch.empty(self.heads, self.head_dim, dtype=torch.float32, device=self.device)
+        dgk = torch.empty_like(dgq)
+        arr = (DzSpan * len(spans))(*[DzSpan(int(c), int(kd), int(nn), None) for c, kd, nn in spans])
+        self._check(lib().dz_attend_spans_backward(self._ctx, q.data_ptr(), k.data_ptr(), v.data_ptr(), pos.data_ptr(),
+                                                   arr, len(spans), out.data_ptr(), lse.data_ptr(), dout.data_ptr(),
+                                                   dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), dgq.data_ptr(),
+                                                   dgk.data_ptr(), _stream_ptr(stream)), "dz_attend_spans_backward")
+        return dq, dk, dv, dgq, dgk
 
     def commit_staged(self, chunk_id: int, stream: Optional[torch.cuda.Stream] = None):
         self._check(lib().dz_commit_staged(self._ctx, chunk_id, _stream_ptr(stream)), "dz_commit_staged")

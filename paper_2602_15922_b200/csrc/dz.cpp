@@ -34,7 +34,8 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct Layout {  // byte offsets inside the caller's storage
   int64_t slots = 0;
   size_t k_off = 0, v_off = 0, q_off = 0, kc_off = 0, lse_off = 0, sq_off = 0, sk_off = 0, sv_off = 0, ol_off = 0,
-         or_off = 0, map_off = 0, ws_off = 0, cnt_off = 0, cnt_bytes = 0, rope_off = 0, bar_off = 0, total = 0;
+         or_off = 0, map_off = 0, ws_off = 0, cnt_off = 0, cnt_bytes = 0, rope_off = 0, bar_off = 0, bq_off = 0,
+         bk_off = 0, bd_off = 0, bl_off = 0, total = 0;
 };
 
 bool basic_cfg_ok(const dz_config* c) {
@@ -82,6 +83,12 @@ Layout make_layout(const dz_config* c) {
   L.cnt_bytes = (size_t)B * Hl * ((mc + dz::kTileQ - 1) / dz::kTileQ) * 2 * 4;
   L.cnt_off = take(L.cnt_bytes);
   L.rope_off = take((size_t)dz::kRopeLen * (D / 2) * 8);             // RoPE (cos, sin) table, fp32
+  if (c->flags & DZ_FLAG_BACKWARD) {                                  // NEXT-1 backward workspace
+    L.bq_off = take((size_t)B * mc * Hl * D * 4);                     // dL/dq' fp32 (atomic accumulation)
+    L.bk_off = take((size_t)B * mc * Hl * D * 4);                     // dL/dk' fp32
+    L.bd_off = take((size_t)B * Hl * mc * 4);                         // delta = <dO, O>
+    L.bl_off = take((size_t)B * Hl * mc * 4);                         // lse * log2(e)
+  }
   if (N > 1) {
     const size_t sb = (size_t)B * (mc / N) * c->heads * D * 2;       // [N][B][n_loc][Hl][D]
     L.sq_off = take(sb);
@@ -927,6 +934,96 @@ dz_status dz_sp_set_peers(dz_ctx* c, void* const* storages, int32_t n) {
   if (c->peers[c->rank] != c->base) return fail(c, DZ_EINVAL, "entry %d must be this rank's cache_storage", c->rank);
   c->peers_set = true;
   return DZ_OK;
+}
+
+dz_status dz_attend_spans_backward(dz_ctx* c, const void* q_raw, const void* k_raw, const void* v_raw,
+                                   const int32_t* pos_thw, const dz_span* spans, int32_t n_spans, const void* out,
+                                   const float* lse, const void* dout, void* dq_raw, void* dk_raw, void* dv_raw,
+                                   float* dq_gain, float* dk_gain, void* stream) {
+  dz_status r = check_ready(c);
+  if (r) return r;
+  if ((r = check_attend_ptrs(c, q_raw, k_raw, v_raw, out))) return r;
+  if (!pos_thw || !spans || !lse || !dout || !dq_raw || !dk_raw || !dv_raw || !dq_gain || !dk_gain ||
+      !aligned16(dout) || !aligned16(dq_raw) || !aligned16(dk_raw) || !aligned16(dv_raw) || !aligned16(lse))
+    return fail(c, DZ_EINVAL, "null or misaligned backward argument");
+  if (!(c->cfg.flags & DZ_FLAG_BACKWARD)) return fail(c, DZ_ESTATE, "created without DZ_FLAG_BACKWARD");
+  if (c->N != 1 || c->D != 128 || c->f8) return fail(c, DZ_ESHAPE, "backward: one GPU, head_dim 128, bf16 path");
+  if (c->valid != 0) return fail(c, DZ_ESTATE, "backward: the teacher-forced layout has no committed cache");
+  if (n_spans <= 0 || n_spans > dz::kMaxSpans)
+    return fail(c, DZ_EINVAL, "n_spans %d outside [1, %d]", n_spans, dz::kMaxSpans);
+  dz::SpanTable t;
+  t.n = n_spans;
+  int64_t n = 0;
+  for (int i = 0; i < n_spans; ++i) {
+    const dz_span& s = spans[i];
+    if (s.kind != DZ_CLEAN && s.kind != DZ_NOISY) return fail(c, DZ_EINVAL, "span %d: bad kind %d", i, s.kind);
+    if (s.n_tokens <= 0) return fail(c, DZ_ESHAPE, "span %d: n_tokens %d must be positive", i, s.n_tokens);
+    set_span(t, i, s.chunk_id, s.kind, (int32_t)n, s.n_tokens);
+    n += s.n_tokens;
+  }
+  if (n > c->cfg.max_chunk_tokens)
+    return fail(c, DZ_ECAPACITY, "%lld span tokens exceed max_chunk_tokens %d", (long long)n, c->cfg.max_chunk_tokens);
+  t.valid = 0;
+  if ((r = check_device(c))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // recompute Q' (pre-scaled, fp16) and K' (fp16, current-chunk buffer) with the forward's prologue
+  if ((r = run_prologue(c, q_raw, k_raw, nullptr, pos_thw, n, st, true))) return r;
+  dz::BwdArgs a;
+  a.dq_acc = reinterpret_cast<float*>(c->base + c->L.bq_off);
+  a.dk = reinterpret_cast<float*>(c->base + c->L.bk_off);
+  a.delta = reinterpret_cast<float*>(c->base + c->L.bd_off);
+  a.lse2 = reinterpret_cast<float*>(c->base + c->L.bl_off);
+  const size_t nel = (size_t)c->B * n * c->H * c->D;
+  if ((r = cuda_check(c, cudaMemsetAsync(a.dq_acc, 0, nel * 4, st), "dq clear"))) return r;
+  if ((r = cuda_check(c, cudaMemsetAsync(dq_gain, 0, (size_t)c->H * c->D * 4, st), "dgq clear"))) return r;
+  if ((r = cuda_check(c, cudaMemsetAsync(dk_gain, 0, (size_t)c->H * c->D * 4, st), "dgk clear"))) return r;
+  const int64_t bs = n * c->H * c->D;
+  if (!make_tmap(&a.tm_k, c->base + c->L.kc_off, 0, c->D, c->H, n, c->B, bs, 64, 128) ||
+      !make_tmap(&a.tm_v, v_raw, 1, c->D, c->H, n, c->B, bs, 64, 128) ||
+      !make_tmap(&a.tm_q, c->base + c->L.q_off, 0, c->D, c->H, n, c->B, bs, 64, 128) ||
+      !make_tmap(&a.tm_do, dout, 1, c->D, c->H, n, c->B, bs, 64, 128))
+    return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (backward) failed");
+  a.dout = dout;
+  a.out = out;
+  a.lse = lse;
+  a.dv = dv_raw;
+  a.q_raw = q_raw;
+  a.k_raw = k_raw;
+  a.dq = dq_raw;
+  a.dk_raw = dk_raw;
+  a.gain[0] = c->cfg.q_gain;
+  a.gain[1] = c->cfg.k_gain;
+  a.dgain[0] = dq_gain;
+  a.dgain[1] = dk_gain;
+  a.pos = pos_thw;
+  a.tab = reinterpret_cast<const float2*>(c->base + c->L.rope_off);
+  a.tab_len = dz::kRopeLen;
+  a.eps = c->eps;
+  a.B = c->B;
+  a.n = (int32_t)n;
+  a.H = c->H;
+  a.D = c->D;
+  a.scale_q = c->scale;
+  a.scale_k = 0.69314718055994530942f;  // Q' carries scale * log2(e): dk' = scale * dS^T q' = ln 2 * dS^T Q'
+  a.spans = t;
+  for (int j = 0; j < c->D / 2; ++j) {
+    a.omega[j] = c->pro.omega[j];
+    a.axis[j] = c->pro.axis[j];
+  }
+  r = cuda_check(c, dz::launch_attention_backward(a, st), "backward launch");
+    for (int sec = 0; sec < 3; ++sec) {
+      struct timespec ts = {1, 0};
+      nanosleep(&ts, nullptr);
+    }
+    const int ctas = c->B * c->H * (int)((n + 127) / 128);
+    for (int i = 0; i < ctas && i < 4096; ++i)
+      fprintf(stderr, "cta %d: w0 %d w1 %d w2 %d w3 %d issuer %d w5 %d\n", i, hp[i * 8], hp[i * 8 + 1], hp[i * 8 + 2],
+              hp[i * 8 + 3], hp[i * 8 + 4], hp[i * 8 + 5]);
+    return r;
+  }
+  r = cuda_check(c, dz::launch_attention_backward(a, st), "backward launch");
+  if (!r) g_launches.fetch_add(3, std::memory_order_relaxed);
+  return r;
 }
 
 int32_t dz_sp_pending(const dz_ctx* c, int32_t* phase, dz_xfer* out, int32_t cap) {

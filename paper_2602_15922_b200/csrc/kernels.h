@@ -139,6 +139,36 @@ cudaError_t read_watchdog(uint32_t* host8);   // {fired, block, warp, bar addr, 
 cudaError_t reset_watchdog();
 cudaError_t trace_control(int enable, uint32_t* host, size_t n);  // K2 cycle trace (CTA 0, first unit)  // work units (b, h, q-tile pair)
 
+// ---- NEXT-1 backward (backward.cu): gradients of the teacher-forced path, one GPU, empty cache ----
+struct BwdArgs {
+  CUtensorMap tm_k, tm_v, tm_q, tm_do;  // K' fp16, V bf16, Q' fp16 (pre-scaled), dO bf16; box (64, 1, 128, 1)
+  const void* dout = nullptr;           // bf16 [B][n][H][D]
+  const void* out = nullptr;            // bf16 [B][n][H][D], the forward's output
+  const float* lse = nullptr;           // fp32 [B][H][n], the forward's natural-log LSE
+  float* delta = nullptr;               // workspace fp32 [B][H][n]
+  float* lse2 = nullptr;                // workspace fp32 [B][H][n]
+  float* dq_acc = nullptr;              // workspace fp32 [B][n][H][D] (zeroed by the caller): dL/dq'
+  float* dk = nullptr;                  // workspace fp32 [B][n][H][D]: dL/dk'
+  void* dv = nullptr;                   // bf16 [B][n][H][D] out
+  const void* q_raw = nullptr;
+  const void* k_raw = nullptr;
+  void* dq = nullptr;                   // bf16 [B][n][H][D] out
+  void* dk_raw = nullptr;               // bf16 [B][n][H][D] out
+  const float* gain[2] = {nullptr, nullptr};
+  float* dgain[2] = {nullptr, nullptr};  // fp32 [H][D] out (zeroed by the caller)
+  const int32_t* pos = nullptr;
+  const float2* tab = nullptr;
+  int32_t tab_len = 0;
+  float eps = 1e-6f;
+  int32_t B = 0, n = 0, H = 0, D = 0;
+  float scale_q = 1.f;                  // dq' = scale_q * (dS K')
+  float scale_k = 1.f;                  // dk' = scale_k * (dS^T Q'), Q' pre-scaled by scale * log2e
+  SpanTable spans;
+  double omega[kMaxHeadDim / 2];
+  int8_t axis[kMaxHeadDim / 2];
+};
+cudaError_t launch_attention_backward(const BwdArgs& a, cudaStream_t s);
+
 // ---- K5: Ulysses receive unpack [N][B][n_loc][Hl][D] -> [B][n_loc][H][D] ---
 cudaError_t launch_sp_unpack(const void* recv, void* out, int32_t N, int32_t B, int32_t n_loc, int32_t Hl,
                              int32_t D, cudaStream_t s);
