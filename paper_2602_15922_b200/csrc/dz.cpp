@@ -1011,17 +1011,6 @@ dz_status dz_attend_spans_backward(dz_ctx* c, const void* q_raw, const void* k_r
     a.axis[j] = c->pro.axis[j];
   }
   r = cuda_check(c, dz::launch_attention_backward(a, st), "backward launch");
-    for (int sec = 0; sec < 3; ++sec) {
-      struct timespec ts = {1, 0};
-      nanosleep(&ts, nullptr);
-    }
-    const int ctas = c->B * c->H * (int)((n + 127) / 128);
-    for (int i = 0; i < ctas && i < 4096; ++i)
-      fprintf(stderr, "cta %d: w0 %d w1 %d w2 %d w3 %d issuer %d w5 %d\n", i, hp[i * 8], hp[i * 8 + 1], hp[i * 8 + 2],
-              hp[i * 8 + 3], hp[i * 8 + 4], hp[i * 8 + 5]);
-    return r;
-  }
-  r = cuda_check(c, dz::launch_attention_backward(a, st), "backward launch");
   if (!r) g_launches.fetch_add(3, std::memory_order_relaxed);
   return r;
 }
