@@ -486,6 +486,33 @@ def secondary(dz, dev, steps, timer: Timer, cooldown=3.0):
                         "k2_ms": spread(prof["attention"]), "k2_tflops": flop / (k2 * 1e-3) / 1e12,
                         "k2_frac": flop / (k2 * 1e-3) / 1e12 / peak, "clocks": clk}
     cache.close()
+
+    # NEXT-1 backward of the Fig. 10(a) layout [C0 C1; Z1 Z2] x 1344 (40 heads): the forward's prologue
+    # recomputed, delta, the attention backward, the prologue backward; useful FLOP = 10 D per visible
+    # pair (S, dP, dV, dK, dQ: 2 D each) summed over heads
+    time.sleep(cooldown)
+    spans = synth.teacher_forcing_spans(2, w.chunk_tokens)
+    n_b = sum(s.n_tokens for s in spans)
+    cache = dz.ChunkKVCache(1, w.heads, w.head_dim, 0, n_b, w.rope_dims, gq.to(dev), gk.to(dev),
+                            flags=dz.FLAG_WRITE_LSE | dz.FLAG_BACKWARD, device=dev)
+    q, k, v = device_inputs(w, dev, 1, 70_000, n_local=n_b)
+    dout = device_inputs(w, dev, 1, 80_000, n_local=n_b)[0]
+    pos = torch.cat([synth.chunk_positions(w, s.chunk) for s in spans]).to(dev)
+    sl = [(s.chunk, s.kind, s.n_tokens) for s in spans]
+    o = cache.attend_spans(q, k, v, pos, sl)
+    lse = cache.lse(n_b)
+    bstep = lambda: cache.attend_spans_backward(q, k, v, pos, sl, o, lse, dout)
+    for _ in range(3):
+        bstep()
+    sm, _, launches, clk = timer.run(bstep, max(5, steps // 4), profiled=False, clock_dev=dev.index)
+    bflop = 10.0 * w.head_dim * w.heads * visible_pairs(spans)
+    out["tf_backward"] = {"workload": "C1 shape, [C0 C1; Z1 Z2] x 1344, 40 heads",
+                          "mode": "dz_attend_spans_backward (prologue recompute + delta + attention backward + "
+                                  "prologue backward)", "step_ms": spread(sm),
+                          "step_tflops": bflop / (statistics.median(sm) * 1e-3) / 1e12,
+                          "step_frac": bflop / (statistics.median(sm) * 1e-3) / 1e12 / peak,
+                          "useful_flop": bflop, "gpu_launches_per_step": launches / max(5, steps // 4), "clocks": clk}
+    cache.close()
     return out
 
 
