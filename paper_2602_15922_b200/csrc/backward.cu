@@ -30,18 +30,25 @@
 namespace dz {
 namespace {
 
-constexpr int kBwdTile = 128;        // keys per CTA, queries per step
-constexpr int kBwdThreads = 192;     // warps 0..3 compute (TMEM lane quadrants), warp 4 TMA + MMA, warp 5 idle
-constexpr int kTileBytes = 128 * 128 * 2;  // one [128][128] 16-bit tile as two [128][64] SW128 boxes
-constexpr int kBoxBytes = 128 * 128;       // one [128 rows][64 cols] box
+constexpr int kBwdTile = 128;        // keys per CTA
+constexpr int kQStep = 64;           // queries per step
+constexpr int kBwdThreads = 192;     // warps 0..3 compute (TMEM lane quadrants), 4 TMA producer, 5 MMA issuer
+constexpr int kKTile = 128 * 128 * 2;      // [128 keys][128 d] 16-bit as two [128][64] SW128 boxes
+constexpr int kKBox = 128 * 128;
+constexpr int kQTile = 64 * 128 * 2;       // [64 q][128 d] as two [64][64] boxes
+constexpr int kQBox = 64 * 128;
+constexpr int kPTile = 128 * 64 * 2;       // [128 keys][64 q]: one box
 
-// shared-memory map
-constexpr int kOffK = 0, kOffV = kTileBytes, kOffQ = 2 * kTileBytes, kOffDO = 3 * kTileBytes,
-              kOffPT = 4 * kTileBytes, kOffDST = 5 * kTileBytes, kOffVec = 6 * kTileBytes,  // lse2[128], delta[128]
-              kOffBar = kOffVec + 1024, kBwdSmem = kOffBar + 1024 + 1024;
+// shared-memory map: K', V (whole launch), Q'[2], dO[2] (per step, double-buffered), P^T, dS^T,
+// lse2 / delta of the step's queries [2][2][64]
+constexpr int kOffK = 0, kOffV = kKTile, kOffQ = 2 * kKTile, kOffDO = kOffQ + 2 * kQTile, kOffPT = kOffDO + 2 * kQTile,
+              kOffDST = kOffPT + kPTile, kOffVec = kOffDST + kPTile, kOffDQ = kOffVec + 1024,
+              kDQTile = kQStep * 128 * 4,                    // dQ staging [64 q][128 d] fp32, double-buffered
+              kOffBar = kOffDQ + 2 * kDQTile, kBwdSmem = kOffBar + 1024 + 1024;
+static_assert(kBwdSmem <= 232448, "backward shared memory");
 
 struct BwdBars {
-  uint64_t kv_full, q_full, s_full, p_ready, mma_done, dq_free;
+  uint64_t kv_full, q_full[2], q_empty[2], s_full[2], tm_free[2], p_ready, mma_done;
   uint32_t tmem_base;
 };
 
@@ -53,66 +60,67 @@ __device__ __forceinline__ int span_of(const SpanTable& st, int x) {
   while (i + 1 < st.n && st.start[i + 1] <= x) ++i;
   return i;
 }
-// any visible (query, key) pair between query tile [q0, q0+128) and key tile [k0, k0+128) (both < n)
-__device__ __forceinline__ bool tile_visible(const SpanTable& st, int q0, int k0, int n) {
-  const int q1 = min(q0 + kBwdTile, n), k1 = min(k0 + kBwdTile, n);
+// any visible (query, key) pair between queries [q0, q0 + kQStep) and keys [k0, k0 + 128) (both < n)
+__device__ __forceinline__ bool step_visible(const SpanTable& st, int q0, int k0, int n) {
+  const int q1 = min(q0 + kQStep, n), k1 = min(k0 + kBwdTile, n);
   for (int ks = span_of(st, k0); ks < st.n && st.start[ks] < k1; ++ks)
     for (int qs = span_of(st, q0); qs < st.n && st.start[qs] < q1; ++qs)
       if (span_vis(st, qs, ks)) return true;
   return false;
 }
-// visible queries of key span ks among [q0, q0 + 128): 128-bit mask
-__device__ __forceinline__ void visible_queries(const SpanTable& st, int ks, int q0, int n, uint32_t (&m)[4]) {
-  m[0] = m[1] = m[2] = m[3] = 0u;
-  const int q1 = min(q0 + kBwdTile, n);
+// visible queries of key span ks among [q0, q0 + 64): 64-bit mask (two words)
+__device__ __forceinline__ void visible_queries(const SpanTable& st, int ks, int q0, int n, uint32_t (&m)[2]) {
+  m[0] = m[1] = 0u;
+  const int q1 = min(q0 + kQStep, n);
   for (int qs = span_of(st, q0); qs < st.n && st.start[qs] < q1; ++qs) {
     if (!span_vis(st, qs, ks)) continue;
     const int a = max(st.start[qs], q0) - q0, b = min(st.start[qs + 1], q1) - q0;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < 2; ++w) {
       const int lo = min(max(a - 32 * w, 0), 32), hi = min(max(b - 32 * w, 0), 32);
       if (hi > lo) m[w] |= (hi == 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~(lo == 32 ? 0xffffffffu : ((1u << lo) - 1u));
     }
   }
 }
 
-// element (r, c) of a [128][128] 16-bit tile stored as two SW128 boxes: byte offset of its 16-byte chunk
-__device__ __forceinline__ uint32_t chunk_off(int r, int c8) {  // c8 = column / 8 (0..15)
-  return (c8 / 8) * kBoxBytes + r * 128 + (((c8 % 8) ^ (r & 7)) << 4);
+// descriptors: K-major view (rows = M or N, 16-element K-steps along the 128-byte rows, boxes of 64
+// columns box_bytes apart) and MN-major view (rows = K, 16-row K-steps, 64-column blocks box_bytes apart)
+__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int kk, uint32_t box_bytes) {
+  return ptx::sdesc_sw128(tile + (kk / 4) * box_bytes + (kk % 4) * 32, 16, 1024);
 }
-// descriptors: K-major (rows = M or N, K along the 128-byte rows) and MN-major (rows = K) views of a tile
-__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int kk) {  // K-step kk of 16 elements
-  return ptx::sdesc_sw128(tile + (kk / 4) * kBoxBytes + (kk % 4) * 32, 16, 1024);
-}
-__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int kk) {  // K-step kk = 16 rows; 64-col blocks at LBO
-  return ptx::sdesc_sw128(tile + kk * 16 * 128, kBoxBytes, 1024);
+__device__ __forceinline__ uint64_t desc_mn(uint32_t tile, int kk, uint32_t box_bytes) {
+  return ptx::sdesc_sw128(tile + kk * 16 * 128, box_bytes, 1024);
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_dq,
                     const float* __restrict__ lse2, const float* __restrict__ delta, float* __restrict__ dq_acc,
-                    float* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int B, int H, int n,
+                    float* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int B, int H, int n, int n_pad,
                     float scale_q, float scale_k, const __grid_constant__ SpanTable st) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw);
   BwdBars* bars = reinterpret_cast<BwdBars*>(smem + kOffBar);
-  float* vec = reinterpret_cast<float*>(smem + kOffVec);  // lse2[128], delta[128] of the current query tile
+  const float* vec = reinterpret_cast<const float*>(smem + kOffVec);  // [buffer][lse2 | delta][64]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n_tiles = (n + kBwdTile - 1) / kBwdTile;
-  const int kt = blockIdx.x % n_tiles, bh = blockIdx.x / n_tiles, h = bh % H, b = bh / H;
+  const int n_ktiles = (n + kBwdTile - 1) / kBwdTile, n_qsteps = (n + kQStep - 1) / kQStep;
+  const int kt = blockIdx.x % n_ktiles, bh = blockIdx.x / n_ktiles, h = bh % H, b = bh / H;
   const int k0 = kt * kBwdTile;
   auto bar = [&](uint64_t& x) { return ptx::smem_u32(&x); };
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(bar(bars->kv_full), 1);
-    ptx::mbar_init(bar(bars->q_full), 1);
-    ptx::mbar_init(bar(bars->s_full), 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(bar(bars->q_full[i]), 1);
+      ptx::mbar_init(bar(bars->q_empty[i]), 1);
+      ptx::mbar_init(bar(bars->s_full[i]), 1);
+      ptx::mbar_init(bar(bars->tm_free[i]), 4);
+    }
     ptx::mbar_init(bar(bars->p_ready), 4);
     ptx::mbar_init(bar(bars->mma_done), 1);
-    ptx::mbar_init(bar(bars->dq_free), 4);
     ptx::fence_mbar_init();
   }
   if (warp == 4) ptx::tmem_alloc<512>(ptx::smem_u32(&bars->tmem_base));
@@ -121,136 +129,198 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   ptx::tc_fence_after();
   ptx::pdl_wait();
   const uint32_t tmem = bars->tmem_base;
-  constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 384, kDQ = 0;
-
+  // TMEM: buffer i (i = step & 1) holds S^T at [128 i, 128 i + 64), dP^T at [128 i + 64, 128 i + 128);
+  // dQ^T of step s reuses S^T's columns of its buffer once S^T has been read; dV [256, 384), dK [384, 512)
+  constexpr uint32_t kDV = 256, kDK = 384;
+  const uint64_t pol = ptx::l2_policy_evict_last();
+  const int64_t vrow = ((int64_t)b * H + h) * n_pad;  // lse2 / delta row of (b, h)
 
   if (warp == 4) {
-    // ------------------------------------------------------ TMA + MMA (one thread) --
+    // ------------------------------------------------------------ TMA producer --
     if (lane == 0) {
-      const uint64_t pol = ptx::l2_policy_evict_last();
-      ptx::mbar_arrive_expect_tx(bar(bars->kv_full), 2 * kTileBytes);
+      ptx::mbar_arrive_expect_tx(bar(bars->kv_full), 2 * kKTile);
       for (int x = 0; x < 2; ++x) {
-        ptx::tma_load_4d(base + kOffK + x * kBoxBytes, &tm_k, bar(bars->kv_full), x * 64, h, k0, b, pol);
-        ptx::tma_load_4d(base + kOffV + x * kBoxBytes, &tm_v, bar(bars->kv_full), x * 64, h, k0, b, pol);
+        ptx::tma_load_4d(base + kOffK + x * kKBox, &tm_k, bar(bars->kv_full), x * 64, h, k0, b, pol);
+        ptx::tma_load_4d(base + kOffV + x * kKBox, &tm_v, bar(bars->kv_full), x * 64, h, k0, b, pol);
       }
-      ptx::mbar_wait(bar(bars->kv_full), 0);
-      constexpr uint32_t iS = ptx::idesc_f16(0, 0, 0, 0, 128, 128), iDP = ptx::idesc_f16(1, 1, 0, 0, 128, 128),
-                         iDV = ptx::idesc_f16(1, 1, 0, 1, 128, 128), iDK = ptx::idesc_f16(0, 0, 0, 1, 128, 128),
-                         iDQ = ptx::idesc_f16(0, 0, 1, 1, 128, 128);
-      uint32_t it = 0;
-      for (int qt = 0; qt < n_tiles; ++qt) {
-        if (!tile_visible(st, qt * kBwdTile, k0, n)) continue;
-        const uint32_t ph = it & 1;
-        if (it > 0) ptx::mbar_wait(bar(bars->dq_free), ph ^ 1);  // dQ^T (cols 0..127) has been read
-        ptx::mbar_arrive_expect_tx(bar(bars->q_full), 2 * kTileBytes);
+      uint32_t i = 0;
+      for (int qs = 0; qs < n_qsteps; ++qs) {
+        if (!step_visible(st, qs * kQStep, k0, n)) continue;
+        const uint32_t bi = i & 1, u = i >> 1;
+        ptx::mbar_wait(bar(bars->q_empty[bi]), (u & 1) ^ 1);
+        const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
+        ptx::mbar_arrive_expect_tx(bar(bars->q_full[bi]), 2 * kQTile + 2 * kQStep * 4);
         for (int x = 0; x < 2; ++x) {
-          ptx::tma_load_4d(base + kOffQ + x * kBoxBytes, &tm_q, bar(bars->q_full), x * 64, h, qt * kBwdTile, b, pol);
-          ptx::tma_load_4d(base + kOffDO + x * kBoxBytes, &tm_do, bar(bars->q_full), x * 64, h, qt * kBwdTile, b,
-                           pol);
+          ptx::tma_load_4d(qb + x * kQBox, &tm_q, bar(bars->q_full[bi]), x * 64, h, qs * kQStep, b, pol);
+          ptx::tma_load_4d(ob + x * kQBox, &tm_do, bar(bars->q_full[bi]), x * 64, h, qs * kQStep, b, pol);
         }
-        ptx::mbar_wait(bar(bars->q_full), ph);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) ptx::mma_ss(tmem + kS, desc_k(base + kOffK, kk), desc_k(base + kOffQ, kk), iS, kk > 0);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tmem + kDP, desc_k(base + kOffV, kk), desc_k(base + kOffDO, kk), iDP, kk > 0);
-        ptx::tc_commit(bar(bars->s_full));
-        ptx::mbar_wait(bar(bars->p_ready), ph);  // P^T and dS^T are in shared memory
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tmem + kDV, desc_k(base + kOffPT, kk), desc_mn(base + kOffDO, kk), iDV, (it > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tmem + kDK, desc_k(base + kOffDST, kk), desc_mn(base + kOffQ, kk), iDK, (it > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tmem + kDQ, desc_mn(base + kOffK, kk), desc_mn(base + kOffDST, kk), iDQ, kk > 0);
-        ptx::tc_commit(bar(bars->mma_done));
-        ++it;
+        const uint32_t vb = base + kOffVec + bi * 512;
+        ptx::bulk_load(vb, lse2 + vrow + qs * kQStep, kQStep * 4, bar(bars->q_full[bi]), pol);
+        ptx::bulk_load(vb + 256, delta + vrow + qs * kQStep, kQStep * 4, bar(bars->q_full[bi]), pol);
+        ++i;
       }
     }
     __syncwarp();
-  } else if (warp < 4) {
-    // ------------------------------------------ softmax-gradient and epilogue warps --
-    const int r = warp * 32 + lane;                         // TMEM lane: key row r (S^T, dP^T, dV, dK) / d (dQ^T)
+  } else if (warp == 5) {
+    // ------------------------------------------------------------- MMA issuer --
+    if (lane == 0) {
+      constexpr uint32_t iS = ptx::idesc_f16(0, 0, 0, 0, 128, 64), iDP = ptx::idesc_f16(1, 1, 0, 0, 128, 64),
+                         iDV = ptx::idesc_f16(1, 1, 0, 1, 128, 128), iDK = ptx::idesc_f16(0, 0, 0, 1, 128, 128),
+                         iDQ = ptx::idesc_f16(0, 0, 1, 1, 128, 64);
+      ptx::mbar_wait(bar(bars->kv_full), 0);
+      // Software-pipelined: S^T / dP^T of step i + 1 are issued before waiting for step i's P^T / dS^T,
+      // so the tensor pipe computes them while the softmax-gradient warps work on step i (and they
+      // complete before step i's dV / dK / dQ^T MMAs, which are issued after them).
+      auto issue_sdp = [&](uint32_t i, int qs) {
+        const uint32_t bi = i & 1, u = i >> 1;
+        const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
+        const uint32_t tS = tmem + bi * 128, tDP = tS + 64;
+        ptx::mbar_wait(bar(bars->q_full[bi]), u & 1);
+        if (i >= 2) ptx::mbar_wait(bar(bars->tm_free[bi]), (u - 1) & 1);  // dQ^T(i - 2) drained
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_ss(tS, desc_k(base + kOffK, kk, kKBox), desc_k(qb, kk, kQBox), iS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_ss(tDP, desc_k(base + kOffV, kk, kKBox), desc_k(ob, kk, kQBox), iDP, kk > 0);
+        ptx::tc_commit(bar(bars->s_full[bi]));
+      };
+      auto next_visible = [&](int qs) {
+        while (qs < n_qsteps && !step_visible(st, qs * kQStep, k0, n)) ++qs;
+        return qs;
+      };
+      int qs = next_visible(0);
+      if (qs < n_qsteps) issue_sdp(0, qs);
+      uint32_t i = 0;
+      while (qs < n_qsteps) {
+        const uint32_t bi = i & 1;
+        const int qn = next_visible(qs + 1);
+        if (qn < n_qsteps) issue_sdp(i + 1, qn);
+        const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
+        const uint32_t tS = tmem + bi * 128;
+        ptx::mbar_wait(bar(bars->p_ready), i & 1);  // P^T and dS^T of step i are in shared memory
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::mma_ss(tmem + kDV, desc_k(base + kOffPT, kk, kPTile), desc_mn(ob, kk, kQBox), iDV,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::mma_ss(tmem + kDK, desc_k(base + kOffDST, kk, kPTile), desc_mn(qb, kk, kQBox), iDK,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_ss(tS, desc_mn(base + kOffK, kk, kKBox), desc_mn(base + kOffDST, kk, kPTile), iDQ, kk > 0);
+        ptx::tc_commit(bar(bars->mma_done));
+        ptx::tc_commit(bar(bars->q_empty[bi]));
+        qs = qn;
+        ++i;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------- softmax-gradient, dQ drain and epilogue --
+    const int r = warp * 32 + lane;  // TMEM lane: key row r (S^T, dP^T, dV, dK) / d (dQ^T)
     const uint32_t lb = (uint32_t)(warp * 32) << 16;
     const int key = k0 + r;
     const int ks = span_of(st, min(key, n - 1));
-    uint32_t it = 0;
-    for (int qt = 0; qt < n_tiles; ++qt) {
-      const int q0 = qt * kBwdTile;
-      if (!tile_visible(st, q0, k0, n)) continue;
-      const uint32_t ph = it & 1;
-      {  // this tile's lse2 / delta into shared memory (the previous tile's reads ended with dq_free)
-        const int q = min(q0 + r, n - 1);
-        vec[r] = lse2[((int64_t)b * H + h) * n + q];
-        vec[128 + r] = delta[((int64_t)b * H + h) * n + q];
-      }
+    // dQ^T of a step (thread = d row r): transposed into the staging tile [64 q][128 d] fp32 (thread r
+    // writes column r: conflict-free), then one TMA bulk reduce-add into dQ'[b][q0 .. q0 + 63][h][:]
+    // (rows past n clipped).  The staging tile alternates; its previous reduce must have read it.
+    uint32_t n_drain = 0;
+    auto drain = [&](uint32_t bi, int q0) {
+      const uint32_t sb = base + kOffDQ + (n_drain & 1) * kDQTile;
+      if (threadIdx.x == 0) ptx::bulk_wait_read_all();  // (keeps at most one reduce in flight)
       ptx::named_bar_sync(1, 128);
-      uint32_t vm[4];
-      visible_queries(st, ks, q0, n, vm);
-      if (key >= n) vm[0] = vm[1] = vm[2] = vm[3] = 0u;
-      ptx::mbar_wait(bar(bars->s_full), ph);
-      ptx::tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {  // 32 queries at a time
-        uint32_t sr[32], dr[32];
-        ptx::tmem_ld32(tmem + lb + kS + c * 32, sr);
-        ptx::tmem_ld32(tmem + lb + kDP + c * 32, dr);
+      for (int c = 0; c < 2; ++c) {
+        uint32_t qr[32];
+        ptx::tmem_ld32(tmem + lb + bi * 128 + c * 32, qr);
         ptx::tmem_wait_ld();
-        uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int j = 0; j < 32; ++j)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((c * 32 + j) * 128 + r) * 4),
+                       "f"(__uint_as_float(qr[j]) * scale_q)
+                       : "memory");
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      if (threadIdx.x == 0) {
+        ptx::tma_reduce_add_4d(&tm_dq, sb, 0, h, q0, b);
+        ptx::bulk_commit_group();
+      }
+      ++n_drain;
+    };
+    uint32_t i = 0;
+    int prev_q0 = 0;
+    for (int qs = 0; qs < n_qsteps; ++qs) {
+      const int q0 = qs * kQStep;
+      if (!step_visible(st, q0, k0, n)) continue;
+      const uint32_t bi = i & 1, u = i >> 1;
+      uint32_t vm[2];
+      visible_queries(st, ks, q0, n, vm);
+      if (key >= n) vm[0] = vm[1] = 0u;
+      ptx::mbar_wait(bar(bars->q_full[bi]), u & 1);    // this step's lse2 / delta are in shared memory
+      ptx::mbar_wait(bar(bars->s_full[bi]), u & 1);
+      ptx::tc_fence_after();
+      const float* lv = vec + bi * 128;
+      uint32_t pk[32], dk[32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {  // 32 queries at a time
+        uint32_t sr[32], dr[32];
+        ptx::tmem_ld32(tmem + lb + bi * 128 + c * 32, sr);
+        ptx::tmem_ld32(tmem + lb + bi * 128 + 64 + c * 32, dr);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
           float p2[2], d2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int qi = c * 32 + 2 * i + e;
-            const bool vis = (vm[c] >> (2 * i + e)) & 1u;
-            const float p = vis ? ptx::ex2(__uint_as_float(sr[2 * i + e]) - vec[qi]) : 0.f;
+            const int qi = c * 32 + 2 * j + e;
+            const bool vis = (vm[c] >> (2 * j + e)) & 1u;
+            // (lse2 / delta past n are unwritten workspace: select, never multiply, masked entries)
+            const float p = vis ? ptx::ex2(__uint_as_float(sr[2 * j + e]) - lv[qi]) : 0.f;
             p2[e] = p;
-            d2[e] = p * (__uint_as_float(dr[2 * i + e]) - vec[128 + qi]);
+            d2[e] = vis ? p * (__uint_as_float(dr[2 * j + e]) - lv[64 + qi]) : 0.f;
           }
-          pk[i] = ptx::pack_bf16x2(p2[0], p2[1]);
+          pk[16 * c + j] = ptx::pack_bf16x2(p2[0], p2[1]);
           __half2 hh = __floats2half2_rn(d2[0], d2[1]);
-          dk[i] = *reinterpret_cast<uint32_t*>(&hh);
+          dk[16 * c + j] = *reinterpret_cast<uint32_t*>(&hh);
         }
+      }
+      ptx::tc_fence_before();
+      if (i >= 1) {  // the previous step's MMAs are done: P^T / dS^T may be rewritten, its dQ^T drained
+        ptx::mbar_wait(bar(bars->mma_done), (i - 1) & 1);
+        ptx::tc_fence_after();
+        drain((i - 1) & 1, prev_q0);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar(bars->tm_free[(i - 1) & 1]));
+      }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t o = chunk_off(r, c * 4 + j);
-          ptx::st_shared_v4(base + kOffPT + o, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          ptx::st_shared_v4(base + kOffDST + o, dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
-        }
+      for (int j = 0; j < 8; ++j) {  // row r of the [128][64] tiles: 8 chunks of 8 queries, SW128
+        const uint32_t o = r * 128 + ((j ^ (r & 7)) << 4);
+        ptx::st_shared_v4(base + kOffPT + o, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        ptx::st_shared_v4(base + kOffDST + o, dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
       }
       ptx::fence_proxy_async_smem();  // generic stores -> the tensor core's reads
-      ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar(bars->p_ready));
-      // dQ^T (thread = d row r) -> fp32 atomics into dQ'[b][q][h][r], coalesced over d
-      ptx::mbar_wait(bar(bars->mma_done), ph);
-      ptx::tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t qr[32];
-        ptx::tmem_ld32(tmem + lb + kDQ + c * 32, qr);
-        ptx::tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int q = q0 + c * 32 + i;
-          if (q < n) atomicAdd(dq_acc + (((int64_t)b * n + q) * H + h) * 128 + r, __uint_as_float(qr[i]) * scale_q);
-        }
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar(bars->dq_free));
-      ++it;
+      prev_q0 = q0;
+      ++i;
     }
+    if (i >= 1) {  // the last step's dQ^T (and the final dV / dK)
+      ptx::mbar_wait(bar(bars->mma_done), (i - 1) & 1);
+      ptx::tc_fence_after();
+      drain((i - 1) & 1, prev_q0);
+    }
+    if (threadIdx.x == 0) ptx::bulk_wait_all();  // the dQ reduces have completed
     // dV (bf16) and dK' (fp32) of this thread's key row (tcgen05.ld is warp-collective: every lane
     // loads, only rows < n store)
     const int64_t row = (((int64_t)b * n + min(key, n - 1)) * H + h) * 128;
     const bool store = key < n;
-    if (it == 0) {  // no query sees these keys: zero gradients
+    if (i == 0) {  // no query sees these keys: zero gradients
       if (store)
         for (int d = 0; d < 128; d += 8) {
           *reinterpret_cast<uint4*>(dv_out + row + d) = make_uint4(0, 0, 0, 0);
@@ -290,7 +360,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // B1: delta = <dO, O> per (b, h, s) row and lse2 = lse * log2(e); one warp per row of D = 128
 __global__ void delta_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
                              const float* __restrict__ lse, float* __restrict__ delta, float* __restrict__ lse2, int B,
-                             int n, int H) {
+                             int n, int H, int n_pad) {
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   if (wid >= (int64_t)B * n * H) return;
@@ -306,10 +376,10 @@ __global__ void delta_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_
   for (int e = 0; e < 4; ++e) acc = fmaf(o4[e], g4[e], acc);
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
-  if (lane == 0) {
-    const int64_t i = ((int64_t)b * H + h) * n + s;
+  if (lane == 0) {  // rows of n_pad (a multiple of 64: the attention backward reads whole 64-query steps)
+    const int64_t i = ((int64_t)b * H + h) * n_pad + s;
     delta[i] = acc;
-    lse2[i] = lse[i] * 1.4426950408889634f;
+    lse2[i] = lse[((int64_t)b * H + h) * n + s] * 1.4426950408889634f;
   }
 }
 
@@ -402,7 +472,7 @@ cudaError_t launch_attention_backward(const BwdArgs& a, cudaStream_t s) {
     const int threads = 256;
     delta_kernel<<<(unsigned)((warps * 32 + threads - 1) / threads), threads, 0, s>>>(
         static_cast<const __nv_bfloat16*>(a.dout), static_cast<const __nv_bfloat16*>(a.out), a.lse, a.delta, a.lse2,
-        a.B, a.n, a.H);
+        a.B, a.n, a.H, a.n_pad);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -412,8 +482,9 @@ cudaError_t launch_attention_backward(const BwdArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const int tiles = (a.n + kBwdTile - 1) / kBwdTile;
     e = launch_pdl(attn_bwd_kernel, dim3((unsigned)(a.B * a.H * tiles)), dim3(kBwdThreads), (size_t)kBwdSmem, s,
-                   a.tm_k, a.tm_v, a.tm_q, a.tm_do, a.lse2, a.delta, a.dq_acc, a.dk, static_cast<__nv_bfloat16*>(a.dv),
-                   a.B, a.H, a.n, a.scale_q, a.scale_k, a.spans);
+                   a.tm_k, a.tm_v, a.tm_q, a.tm_do, a.tm_dq, a.lse2, a.delta, a.dq_acc, a.dk,
+                   static_cast<__nv_bfloat16*>(a.dv),
+                   a.B, a.H, a.n, a.n_pad, a.scale_q, a.scale_k, a.spans);
     if (e != cudaSuccess) return e;
   }
   // B3

@@ -86,8 +86,8 @@ Layout make_layout(const dz_config* c) {
   if (c->flags & DZ_FLAG_BACKWARD) {                                  // NEXT-1 backward workspace
     L.bq_off = take((size_t)B * mc * Hl * D * 4);                     // dL/dq' fp32 (atomic accumulation)
     L.bk_off = take((size_t)B * mc * Hl * D * 4);                     // dL/dk' fp32
-    L.bd_off = take((size_t)B * Hl * mc * 4);                         // delta = <dO, O>
-    L.bl_off = take((size_t)B * Hl * mc * 4);                         // lse * log2(e)
+    L.bd_off = take((size_t)B * Hl * ((mc + 63) / 64 * 64) * 4);      // delta = <dO, O> (rows padded to 64)
+    L.bl_off = take((size_t)B * Hl * ((mc + 63) / 64 * 64) * 4);      // lse * log2(e)
   }
   if (N > 1) {
     const size_t sb = (size_t)B * (mc / N) * c->heads * D * 2;       // [N][B][n_loc][Hl][D]
@@ -980,9 +980,19 @@ dz_status dz_attend_spans_backward(dz_ctx* c, const void* q_raw, const void* k_r
   const int64_t bs = n * c->H * c->D;
   if (!make_tmap(&a.tm_k, c->base + c->L.kc_off, 0, c->D, c->H, n, c->B, bs, 64, 128) ||
       !make_tmap(&a.tm_v, v_raw, 1, c->D, c->H, n, c->B, bs, 64, 128) ||
-      !make_tmap(&a.tm_q, c->base + c->L.q_off, 0, c->D, c->H, n, c->B, bs, 64, 128) ||
-      !make_tmap(&a.tm_do, dout, 1, c->D, c->H, n, c->B, bs, 64, 128))
+      !make_tmap(&a.tm_q, c->base + c->L.q_off, 0, c->D, c->H, n, c->B, bs, 64, 64) ||
+      !make_tmap(&a.tm_do, dout, 1, c->D, c->H, n, c->B, bs, 64, 64))
     return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (backward) failed");
+  {  // dL/dq' accumulator: fp32, box (D, 1, 64, 1), no swizzle -- the target of TMA reduce-adds
+    auto fn = encode_fn();
+    cuuint64_t dims[4] = {(cuuint64_t)c->D, (cuuint64_t)c->H, (cuuint64_t)n, (cuuint64_t)c->B};
+    cuuint64_t strides[3] = {(cuuint64_t)c->D * 4, (cuuint64_t)c->H * c->D * 4, (cuuint64_t)bs * 4};
+    cuuint32_t box[4] = {(cuuint32_t)c->D, 1, 64, 1}, estr[4] = {1, 1, 1, 1};
+    if (!fn || fn(&a.tm_dq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.dq_acc, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(c, DZ_ECUDA, "cuTensorMapEncodeTiled (dq) failed");
+  }
   a.dout = dout;
   a.out = out;
   a.lse = lse;
@@ -1001,6 +1011,7 @@ dz_status dz_attend_spans_backward(dz_ctx* c, const void* q_raw, const void* k_r
   a.eps = c->eps;
   a.B = c->B;
   a.n = (int32_t)n;
+  a.n_pad = (int32_t)((n + 63) / 64 * 64);
   a.H = c->H;
   a.D = c->D;
   a.scale_q = c->scale;

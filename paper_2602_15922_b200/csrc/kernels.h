@@ -141,7 +141,8 @@ cudaError_t trace_control(int enable, uint32_t* host, size_t n);  // K2 cycle tr
 
 // ---- NEXT-1 backward (backward.cu): gradients of the teacher-forced path, one GPU, empty cache ----
 struct BwdArgs {
-  CUtensorMap tm_k, tm_v, tm_q, tm_do;  // K' fp16, V bf16, Q' fp16 (pre-scaled), dO bf16; box (64, 1, 128, 1)
+  CUtensorMap tm_k, tm_v, tm_q, tm_do;  // K' fp16, V bf16 (box (64, 1, 128, 1)); Q' fp16 (pre-scaled), dO bf16 (64 rows)
+  CUtensorMap tm_dq;                    // dL/dq' fp32 [B][n][H][D], box (128, 1, 64, 1), no swizzle (TMA reduce-add)
   const void* dout = nullptr;           // bf16 [B][n][H][D]
   const void* out = nullptr;            // bf16 [B][n][H][D], the forward's output
   const float* lse = nullptr;           // fp32 [B][H][n], the forward's natural-log LSE
@@ -161,6 +162,7 @@ struct BwdArgs {
   int32_t tab_len = 0;
   float eps = 1e-6f;
   int32_t B = 0, n = 0, H = 0, D = 0;
+  int32_t n_pad = 0;                    // row length of delta / lse2 (n rounded up to 64)
   float scale_q = 1.f;                  // dq' = scale_q * (dS K')
   float scale_k = 1.f;                  // dk' = scale_k * (dS^T Q'), Q' pre-scaled by scale * log2e
   SpanTable spans;

@@ -206,6 +206,14 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, uint32_t src, int
                "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
+// TMA tensor reduce-add shared -> global (fp32 elements; bulk async-group completion)
+__device__ __forceinline__ void tma_reduce_add_4d(const void* tmap, uint32_t src, int32_t c0, int32_t c1, int32_t c2,
+                                                  int32_t c3) {
+  asm volatile("cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // the shared-memory sources of every committed bulk store have been read (the buffer may be reused)
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
