@@ -48,7 +48,7 @@ constexpr int kOffK = 0, kOffV = kKTile, kOffQ = 2 * kKTile, kOffDO = kOffQ + 2 
 static_assert(kBwdSmem <= 232448, "backward shared memory");
 
 struct BwdBars {
-  uint64_t kv_full, q_full[2], q_empty[2], s_full[2], tm_free[2], p_ready, mma_done;
+  uint64_t kv_full, q_full[2], q_empty[2], s_full, s_read, dq_free[2], p_ready, mma_done;
   uint32_t tmem_base;
 };
 
@@ -116,9 +116,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(bar(bars->q_full[i]), 1);
       ptx::mbar_init(bar(bars->q_empty[i]), 1);
-      ptx::mbar_init(bar(bars->s_full[i]), 1);
-      ptx::mbar_init(bar(bars->tm_free[i]), 4);
+      ptx::mbar_init(bar(bars->dq_free[i]), 4);
     }
+    ptx::mbar_init(bar(bars->s_full), 1);
+    ptx::mbar_init(bar(bars->s_read), 4);
     ptx::mbar_init(bar(bars->p_ready), 4);
     ptx::mbar_init(bar(bars->mma_done), 1);
     ptx::fence_mbar_init();
@@ -129,9 +130,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   ptx::tc_fence_after();
   ptx::pdl_wait();
   const uint32_t tmem = bars->tmem_base;
-  // TMEM: buffer i (i = step & 1) holds S^T at [128 i, 128 i + 64), dP^T at [128 i + 64, 128 i + 128);
-  // dQ^T of step s reuses S^T's columns of its buffer once S^T has been read; dV [256, 384), dK [384, 512)
-  constexpr uint32_t kDV = 256, kDK = 384;
+  // TMEM: S^T [0, 64), dP^T [64, 128) (one step at a time: the next step's are computed once these are in
+  // registers), dQ^T of step i in [128 + 64 (i & 1), +64) (drained while later steps run), dV [256, 384),
+  // dK [384, 512)
+  constexpr uint32_t kS = 0, kDP = 64, kDQ = 128, kDV = 256, kDK = 384;
   const uint64_t pol = ptx::l2_policy_evict_last();
   const int64_t vrow = ((int64_t)b * H + h) * n_pad;  // lse2 / delta row of (b, h)
 
@@ -171,35 +173,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // Software-pipelined: S^T / dP^T of step i + 1 are issued before waiting for step i's P^T / dS^T,
       // so the tensor pipe computes them while the softmax-gradient warps work on step i (and they
       // complete before step i's dV / dK / dQ^T MMAs, which are issued after them).
-      auto issue_sdp = [&](uint32_t i, int qs) {
+      auto issue_sdp = [&](uint32_t i) {
         const uint32_t bi = i & 1, u = i >> 1;
         const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
-        const uint32_t tS = tmem + bi * 128, tDP = tS + 64;
         ptx::mbar_wait(bar(bars->q_full[bi]), u & 1);
-        if (i >= 2) ptx::mbar_wait(bar(bars->tm_free[bi]), (u - 1) & 1);  // dQ^T(i - 2) drained
+        if (i >= 1) ptx::mbar_wait(bar(bars->s_read), (i - 1) & 1);  // S^T / dP^T of step i - 1 are in registers
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tS, desc_k(base + kOffK, kk, kKBox), desc_k(qb, kk, kQBox), iS, kk > 0);
+          ptx::mma_ss(tmem + kS, desc_k(base + kOffK, kk, kKBox), desc_k(qb, kk, kQBox), iS, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tDP, desc_k(base + kOffV, kk, kKBox), desc_k(ob, kk, kQBox), iDP, kk > 0);
-        ptx::tc_commit(bar(bars->s_full[bi]));
+          ptx::mma_ss(tmem + kDP, desc_k(base + kOffV, kk, kKBox), desc_k(ob, kk, kQBox), iDP, kk > 0);
+        ptx::tc_commit(bar(bars->s_full));
       };
       auto next_visible = [&](int qs) {
         while (qs < n_qsteps && !step_visible(st, qs * kQStep, k0, n)) ++qs;
         return qs;
       };
       int qs = next_visible(0);
-      if (qs < n_qsteps) issue_sdp(0, qs);
+      if (qs < n_qsteps) issue_sdp(0);
       uint32_t i = 0;
       while (qs < n_qsteps) {
-        const uint32_t bi = i & 1;
+        const uint32_t bi = i & 1, u = i >> 1;
         const int qn = next_visible(qs + 1);
-        if (qn < n_qsteps) issue_sdp(i + 1, qn);
+        if (qn < n_qsteps) issue_sdp(i + 1);  // (waits until step i's S^T / dP^T have been read)
         const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
-        const uint32_t tS = tmem + bi * 128;
         ptx::mbar_wait(bar(bars->p_ready), i & 1);  // P^T and dS^T of step i are in shared memory
+        if (i >= 2) ptx::mbar_wait(bar(bars->dq_free[bi]), (u - 1) & 1);  // dQ^T(i - 2) drained
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
@@ -211,7 +212,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                       (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tS, desc_mn(base + kOffK, kk, kKBox), desc_mn(base + kOffDST, kk, kPTile), iDQ, kk > 0);
+          ptx::mma_ss(tmem + kDQ + bi * 64, desc_mn(base + kOffK, kk, kKBox), desc_mn(base + kOffDST, kk, kPTile),
+                      iDQ, kk > 0);
         ptx::tc_commit(bar(bars->mma_done));
         ptx::tc_commit(bar(bars->q_empty[bi]));
         qs = qn;
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t qr[32];
-        ptx::tmem_ld32(tmem + lb + bi * 128 + c * 32, qr);
+        ptx::tmem_ld32(tmem + lb + kDQ + bi * 64 + c * 32, qr);
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j)
@@ -262,41 +264,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       visible_queries(st, ks, q0, n, vm);
       if (key >= n) vm[0] = vm[1] = 0u;
       ptx::mbar_wait(bar(bars->q_full[bi]), u & 1);    // this step's lse2 / delta are in shared memory
-      ptx::mbar_wait(bar(bars->s_full[bi]), u & 1);
+      ptx::mbar_wait(bar(bars->s_full), i & 1);
       ptx::tc_fence_after();
+      uint32_t sr[64], dr[64];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        ptx::tmem_ld32(tmem + lb + kS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
+        ptx::tmem_ld32(tmem + lb + kDP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&dr[32 * c]));
+      }
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(bar(bars->s_read));  // the next step's S^T / dP^T may be computed
       const float* lv = vec + bi * 128;
       uint32_t pk[32], dk[32];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {  // 32 queries at a time
-        uint32_t sr[32], dr[32];
-        ptx::tmem_ld32(tmem + lb + bi * 128 + c * 32, sr);
-        ptx::tmem_ld32(tmem + lb + bi * 128 + 64 + c * 32, dr);
-        ptx::tmem_wait_ld();
+      for (int j = 0; j < 32; ++j) {
+        float p2[2], d2[2];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float p2[2], d2[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int qi = c * 32 + 2 * j + e;
-            const bool vis = (vm[c] >> (2 * j + e)) & 1u;
-            // (lse2 / delta past n are unwritten workspace: select, never multiply, masked entries)
-            const float p = vis ? ptx::ex2(__uint_as_float(sr[2 * j + e]) - lv[qi]) : 0.f;
-            p2[e] = p;
-            d2[e] = vis ? p * (__uint_as_float(dr[2 * j + e]) - lv[64 + qi]) : 0.f;
-          }
-          pk[16 * c + j] = ptx::pack_bf16x2(p2[0], p2[1]);
-          __half2 hh = __floats2half2_rn(d2[0], d2[1]);
-          dk[16 * c + j] = *reinterpret_cast<uint32_t*>(&hh);
+        for (int e = 0; e < 2; ++e) {
+          const int qi = 2 * j + e;
+          const bool vis = (vm[qi / 32] >> (qi % 32)) & 1u;
+          // (lse2 / delta past n are unwritten workspace: select, never multiply, masked entries)
+          const float p = vis ? ptx::ex2(__uint_as_float(sr[qi]) - lv[qi]) : 0.f;
+          p2[e] = p;
+          d2[e] = vis ? p * (__uint_as_float(dr[qi]) - lv[64 + qi]) : 0.f;
         }
+        pk[j] = ptx::pack_bf16x2(p2[0], p2[1]);
+        __half2 hh = __floats2half2_rn(d2[0], d2[1]);
+        dk[j] = *reinterpret_cast<uint32_t*>(&hh);
       }
-      ptx::tc_fence_before();
-      if (i >= 1) {  // the previous step's MMAs are done: P^T / dS^T may be rewritten, its dQ^T drained
+      if (i >= 1) {  // the previous step's MMAs have read P^T / dS^T
         ptx::mbar_wait(bar(bars->mma_done), (i - 1) & 1);
         ptx::tc_fence_after();
-        drain((i - 1) & 1, prev_q0);
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(bar(bars->tm_free[(i - 1) & 1]));
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {  // row r of the [128][64] tiles: 8 chunks of 8 queries, SW128
@@ -307,6 +307,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::fence_proxy_async_smem();  // generic stores -> the tensor core's reads
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar(bars->p_ready));
+      if (i >= 1) {  // dQ^T of step i - 1 leaves TMEM while step i's MMAs run
+        drain((i - 1) & 1, prev_q0);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar(bars->dq_free[(i - 1) & 1]));
+      }
       prev_q0 = q0;
       ++i;
     }
