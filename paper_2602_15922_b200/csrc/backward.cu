@@ -32,7 +32,8 @@ namespace {
 
 constexpr int kBwdTile = 128;        // keys per CTA
 constexpr int kQStep = 64;           // queries per step
-constexpr int kBwdThreads = 192;     // warps 0..3 compute (TMEM lane quadrants), 4 TMA producer, 5 MMA issuer
+constexpr int kBwdThreads = 320;     // warps 0..7 compute (quadrant w % 4, query half w / 4), 8 TMA producer, 9 MMA issuer
+constexpr int kWarpProd = 8, kWarpMma = 9;
 constexpr int kKTile = 128 * 128 * 2;      // [128 keys][128 d] 16-bit as two [128][64] SW128 boxes
 constexpr int kKBox = 128 * 128;
 constexpr int kQTile = 64 * 128 * 2;       // [64 q][128 d] as two [64][64] boxes
@@ -116,15 +117,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(bar(bars->q_full[i]), 1);
       ptx::mbar_init(bar(bars->q_empty[i]), 1);
-      ptx::mbar_init(bar(bars->dq_free[i]), 4);
+      ptx::mbar_init(bar(bars->dq_free[i]), 8);
     }
     ptx::mbar_init(bar(bars->s_full), 1);
-    ptx::mbar_init(bar(bars->s_read), 4);
-    ptx::mbar_init(bar(bars->p_ready), 4);
+    ptx::mbar_init(bar(bars->s_read), 8);
+    ptx::mbar_init(bar(bars->p_ready), 8);
     ptx::mbar_init(bar(bars->mma_done), 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 4) ptx::tmem_alloc<512>(ptx::smem_u32(&bars->tmem_base));
+  if (warp == kWarpProd) ptx::tmem_alloc<512>(ptx::smem_u32(&bars->tmem_base));
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint64_t pol = ptx::l2_policy_evict_last();
   const int64_t vrow = ((int64_t)b * H + h) * n_pad;  // lse2 / delta row of (b, h)
 
-  if (warp == 4) {
+  if (warp == kWarpProd) {
     // ------------------------------------------------------------ TMA producer --
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(bar(bars->kv_full), 2 * kKTile);
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == kWarpMma) {
     // ------------------------------------------------------------- MMA issuer --
     if (lane == 0) {
       constexpr uint32_t iS = ptx::idesc_f16(0, 0, 0, 0, 128, 64), iDP = ptx::idesc_f16(1, 1, 0, 0, 128, 64),
@@ -221,33 +222,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
     __syncwarp();
-  } else {
+  } else {  // warps 0..7
     // ------------------------------------- softmax-gradient, dQ drain and epilogue --
-    const int r = warp * 32 + lane;  // TMEM lane: key row r (S^T, dP^T, dV, dK) / d (dQ^T)
-    const uint32_t lb = (uint32_t)(warp * 32) << 16;
+    // warp w: TMEM lane quadrant w % 4 (key rows, or d rows for dQ^T), query half hq = w / 4 of each step
+    const int quad = warp % 4, hq = warp / 4;
+    const int r = quad * 32 + lane;
+    const uint32_t lb = (uint32_t)(quad * 32) << 16;
     const int key = k0 + r;
     const int ks = span_of(st, min(key, n - 1));
-    // dQ^T of a step (thread = d row r): transposed into the staging tile [64 q][128 d] fp32 (thread r
-    // writes column r: conflict-free), then one TMA bulk reduce-add into dQ'[b][q0 .. q0 + 63][h][:]
-    // (rows past n clipped).  The staging tile alternates; its previous reduce must have read it.
+    // dQ^T of a step (thread = d row r, its warp's 32 queries): transposed into the staging tile
+    // [64 q][128 d] fp32 (thread r writes column r: conflict-free), then one TMA bulk reduce-add into
+    // dQ'[b][q0 .. q0 + 63][h][:] (rows past n clipped).  Staging alternates; its previous reduce must
+    // have read it.
     uint32_t n_drain = 0;
     auto drain = [&](uint32_t bi, int q0) {
       const uint32_t sb = base + kOffDQ + (n_drain & 1) * kDQTile;
       if (threadIdx.x == 0) ptx::bulk_wait_read_all();  // (keeps at most one reduce in flight)
-      ptx::named_bar_sync(1, 128);
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t qr[32];
-        ptx::tmem_ld32(tmem + lb + kDQ + bi * 64 + c * 32, qr);
-        ptx::tmem_wait_ld();
+      ptx::named_bar_sync(1, 256);
+      uint32_t qr[32];
+      ptx::tmem_ld32(tmem + lb + kDQ + bi * 64 + hq * 32, qr);
+      ptx::tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((c * 32 + j) * 128 + r) * 4),
-                       "f"(__uint_as_float(qr[j]) * scale_q)
-                       : "memory");
-      }
+      for (int j = 0; j < 32; ++j)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((hq * 32 + j) * 128 + r) * 4),
+                     "f"(__uint_as_float(qr[j]) * scale_q)
+                     : "memory");
       ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1, 128);
+      ptx::named_bar_sync(1, 256);
       if (threadIdx.x == 0) {
         ptx::tma_reduce_add_4d(&tm_dq, sb, 0, h, q0, b);
         ptx::bulk_commit_group();
@@ -260,31 +261,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int q0 = qs * kQStep;
       if (!step_visible(st, q0, k0, n)) continue;
       const uint32_t bi = i & 1, u = i >> 1;
-      uint32_t vm[2];
-      visible_queries(st, ks, q0, n, vm);
-      if (key >= n) vm[0] = vm[1] = 0u;
+      uint32_t vm2[2];
+      visible_queries(st, ks, q0, n, vm2);
+      const uint32_t vm = key < n ? vm2[hq] : 0u;
       ptx::mbar_wait(bar(bars->q_full[bi]), u & 1);    // this step's lse2 / delta are in shared memory
       ptx::mbar_wait(bar(bars->s_full), i & 1);
       ptx::tc_fence_after();
-      uint32_t sr[64], dr[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        ptx::tmem_ld32(tmem + lb + kS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-        ptx::tmem_ld32(tmem + lb + kDP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&dr[32 * c]));
-      }
+      uint32_t sr[32], dr[32];
+      ptx::tmem_ld32(tmem + lb + kS + hq * 32, sr);
+      ptx::tmem_ld32(tmem + lb + kDP + hq * 32, dr);
       ptx::tmem_wait_ld();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar(bars->s_read));  // the next step's S^T / dP^T may be computed
-      const float* lv = vec + bi * 128;
-      uint32_t pk[32], dk[32];
+      const float* lv = vec + bi * 128 + hq * 32;
+      uint32_t pk[16], dk[16];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
+      for (int j = 0; j < 16; ++j) {
         float p2[2], d2[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int qi = 2 * j + e;
-          const bool vis = (vm[qi / 32] >> (qi % 32)) & 1u;
+          const bool vis = (vm >> qi) & 1u;
           // (lse2 / delta past n are unwritten workspace: select, never multiply, masked entries)
           const float p = vis ? ptx::ex2(__uint_as_float(sr[qi]) - lv[qi]) : 0.f;
           p2[e] = p;
@@ -299,8 +297,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tc_fence_after();
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {  // row r of the [128][64] tiles: 8 chunks of 8 queries, SW128
-        const uint32_t o = r * 128 + ((j ^ (r & 7)) << 4);
+      for (int j = 0; j < 4; ++j) {  // row r of the [128][64] tiles: this warp's 4 chunks of 8 queries, SW128
+        const uint32_t o = r * 128 + (((hq * 4 + j) ^ (r & 7)) << 4);
         ptx::st_shared_v4(base + kOffPT + o, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         ptx::st_shared_v4(base + kOffDST + o, dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
       }
@@ -322,20 +320,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       drain((i - 1) & 1, prev_q0);
     }
     if (threadIdx.x == 0) ptx::bulk_wait_all();  // the dQ reduces have completed
-    // dV (bf16) and dK' (fp32) of this thread's key row (tcgen05.ld is warp-collective: every lane
-    // loads, only rows < n store)
+    // dV (bf16) and dK' (fp32) of this thread's key row, columns [64 hq, 64 hq + 64) (tcgen05.ld is
+    // warp-collective: every lane loads, only rows < n store)
     const int64_t row = (((int64_t)b * n + min(key, n - 1)) * H + h) * 128;
     const bool store = key < n;
     if (i == 0) {  // no query sees these keys: zero gradients
       if (store)
-        for (int d = 0; d < 128; d += 8) {
+        for (int d = hq * 64; d < hq * 64 + 64; d += 8) {
           *reinterpret_cast<uint4*>(dv_out + row + d) = make_uint4(0, 0, 0, 0);
           *reinterpret_cast<float4*>(dk_out + row + d) = make_float4(0.f, 0.f, 0.f, 0.f);
           *reinterpret_cast<float4*>(dk_out + row + d + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     } else {
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 2 * hq; c < 2 * hq + 2; ++c) {
         uint32_t vr[32], kr[32];
         ptx::tmem_ld32(tmem + lb + kDV + c * 32, vr);
         ptx::tmem_ld32(tmem + lb + kDK + c * 32, kr);
@@ -360,7 +358,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  if (warp == 4) ptx::tmem_dealloc<512>(tmem);
+  if (warp == kWarpProd) ptx::tmem_dealloc<512>(tmem);
 }
 
 // B1: delta = <dO, O> per (b, h, s) row and lse2 = lse * log2(e); one warp per row of D = 128
