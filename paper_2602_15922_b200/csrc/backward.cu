@@ -40,18 +40,46 @@ constexpr int kQTile = 64 * 128 * 2;       // [64 q][128 d] as two [64][64] boxe
 constexpr int kQBox = 64 * 128;
 constexpr int kPTile = 128 * 64 * 2;       // [128 keys][64 q]: one box
 
-// shared-memory map: K', V (whole launch), Q'[2], dO[2] (per step, double-buffered), P^T, dS^T,
-// lse2 / delta of the step's queries [2][2][64]
-constexpr int kOffK = 0, kOffV = kKTile, kOffQ = 2 * kKTile, kOffDO = kOffQ + 2 * kQTile, kOffPT = kOffDO + 2 * kQTile,
-              kOffDST = kOffPT + kPTile, kOffVec = kOffDST + kPTile, kOffDQ = kOffVec + 1024,
-              kDQTile = kQStep * 128 * 4,                    // dQ staging [64 q][128 d] fp32, double-buffered
-              kOffBar = kOffDQ + 2 * kDQTile, kBwdSmem = kOffBar + 1024 + 1024;
+// shared-memory map: K', V (whole launch), Q' / dO / lse2 / delta of the step's queries (a ring of
+// kQStages: a step's tiles are loaded while the two before it run), P^T, dS^T, the dQ staging tile
+constexpr int kQStages = 3;          // Q' / dO / lse2 / delta ring
+constexpr int kOffK = 0, kOffV = kKTile, kOffQ = 2 * kKTile, kOffDO = kOffQ + kQStages * kQTile,
+              kOffPT = kOffDO + kQStages * kQTile, kOffDST = kOffPT + kPTile, kOffVec = kOffDST + kPTile,
+              kOffDQ = kOffVec + kQStages * 512,
+              kDQTile = kQStep * 128 * 4,                    // dQ staging [64 q][128 d] fp32
+              kOffBar = kOffDQ + kDQTile, kBwdSmem = kOffBar + 256 + 1024;
 static_assert(kBwdSmem <= 232448, "backward shared memory");
 
+#ifdef DZ_BWD_TRACE
+// diagnostics build only: clock() per step of one CTA ([step][24] words)
+__device__ uint32_t g_bwd_trace[128 * 24];
+__device__ int g_bwd_trace_cta = -1;
+__device__ uint32_t g_bwd_cta[4096 * 4];  // per CTA: globaltimer start / end (ns, low 32 bits), steps, SM id
+__device__ __forceinline__ uint32_t bt_gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (uint32_t)t;
+}
+__device__ __forceinline__ uint32_t bt_smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#define BT_CTA(slot, v) do { if (blockIdx.x < 4096) g_bwd_cta[blockIdx.x * 4 + (slot)] = (v); } while (0)
+#define BT(step, slot) do { if (bt_on && (step) < 128) g_bwd_trace[(step) * 24 + (slot)] = (uint32_t)clock(); } while (0)
+#else
+#define BT(step, slot) do { } while (0)
+#define BT_CTA(slot, v) do { } while (0)
+#endif
+
+constexpr int kMaxRanges = 12;  // visible query-step ranges kept per key tile (more: the StepWalk path)
 struct BwdBars {
-  uint64_t kv_full, q_full[2], q_empty[2], s_full, s_read, dq_free[2], p_ready, mma_done;
+  uint64_t kv_full, q_full[kQStages], q_empty[kQStages], s_full, s_read, dq_free[2], p_ready, mma_done;
   uint32_t tmem_base;
+  int32_t n_ranges;              // -1: more than kMaxRanges, walk the span table instead
+  int32_t rng[kMaxRanges][2];    // [first, end) query steps, increasing, disjoint
 };
+static_assert(sizeof(BwdBars) <= 256, "backward barrier block");
 
 __device__ __forceinline__ bool span_vis(const SpanTable& st, int qs, int ks) {
   return qs == ks || st.kc[ks] < st.qth[qs];
@@ -61,20 +89,106 @@ __device__ __forceinline__ int span_of(const SpanTable& st, int x) {
   while (i + 1 < st.n && st.start[i + 1] <= x) ++i;
   return i;
 }
-// any visible (query, key) pair between queries [q0, q0 + kQStep) and keys [k0, k0 + 128) (both < n)
-__device__ __forceinline__ bool step_visible(const SpanTable& st, int q0, int k0, int n) {
-  const int q1 = min(q0 + kQStep, n), k1 = min(k0 + kBwdTile, n);
-  for (int ks = span_of(st, k0); ks < st.n && st.start[ks] < k1; ++ks)
-    for (int qs = span_of(st, q0); qs < st.n && st.start[qs] < q1; ++qs)
-      if (span_vis(st, qs, ks)) return true;
-  return false;
+// The visible query steps of one key tile, walked in increasing order; each role keeps its own walk.
+// The query-span cursor qc only moves forward and invisible query spans are skipped whole, so a walk
+// costs O(steps + spans) reads of the (parameter-space) span table.
+struct StepWalk {
+  int qc = 0;         // query span holding the first query of the last step returned
+  int ks_lo, ks_hi;   // key spans intersecting the tile
+  __device__ __forceinline__ StepWalk(const SpanTable& st, int k0, int n)
+      : ks_lo(span_of(st, k0)), ks_hi(span_of(st, min(k0 + kBwdTile, n) - 1)) {}
+  // first step >= s with a visible (query, key) pair (n_qsteps if none)
+  __device__ __forceinline__ int next(const SpanTable& st, int s, int n_qsteps) {
+    if (s >= n_qsteps) return n_qsteps;
+    const int q0 = s * kQStep;
+    while (qc + 1 < st.n && st.start[qc + 1] <= q0) ++qc;
+    int r = n_qsteps;
+    for (int qs = qc; qs < st.n; ++qs) {
+      bool v = false;
+      for (int ks = ks_lo; ks <= ks_hi; ++ks) v |= span_vis(st, qs, ks);
+      if (v) {
+        r = max(s, st.start[qs] / kQStep);
+        break;
+      }
+    }
+    if (r < n_qsteps)
+      while (qc + 1 < st.n && st.start[qc + 1] <= r * kQStep) ++qc;
+    return r;
+  }
+};
+// The visible steps of the tile in increasing order, from the ranges in shared memory (or the walk).
+struct Steps {
+  const BwdBars* bars;
+  StepWalk walk;
+  int r = 0;
+  __device__ __forceinline__ Steps(const BwdBars* b_, const SpanTable& st, int k0, int n) : bars(b_), walk(st, k0, n) {}
+  __device__ __forceinline__ int first(const SpanTable& st, int n_qsteps) {
+    const int nr = bars->n_ranges;
+    if (nr < 0) return walk.next(st, 0, n_qsteps);
+    r = 0;
+    return nr > 0 ? bars->rng[0][0] : n_qsteps;
+  }
+  __device__ __forceinline__ int next(const SpanTable& st, int s, int n_qsteps) {
+    const int nr = bars->n_ranges;
+    if (nr < 0) return walk.next(st, s + 1, n_qsteps);
+    if (s + 1 < bars->rng[r][1]) return s + 1;
+    ++r;
+    return r < nr ? bars->rng[r][0] : n_qsteps;
+  }
+};
+// Fill bars->rng / n_ranges (one warp, lanes over query spans): the steps overlapping any query span
+// that sees a key span of the tile, merged into ranges.
+__device__ __forceinline__ void build_ranges(const SpanTable& st, int k0, int n, BwdBars* bars, int lane) {
+  const int ks_lo = span_of(st, k0), ks_hi = span_of(st, min(k0 + kBwdTile, n) - 1);
+  int nr = 0, cur_lo = -1, cur_hi = -1;
+  for (int q_base = 0; q_base < st.n; q_base += 32) {
+    const int qs = q_base + lane;
+    int lo = 0, hi = 0;
+    if (qs < st.n) {
+      bool v = false;
+      for (int ks = ks_lo; ks <= ks_hi; ++ks) v |= span_vis(st, qs, ks);
+      if (v && st.start[qs + 1] > st.start[qs]) {
+        lo = st.start[qs] / kQStep;
+        hi = (st.start[qs + 1] - 1) / kQStep + 1;
+      }
+    }
+    uint32_t m = __ballot_sync(0xffffffffu, hi > lo);
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      const int l = __shfl_sync(0xffffffffu, lo, j), h = __shfl_sync(0xffffffffu, hi, j);
+      if (cur_lo >= 0 && l <= cur_hi) {
+        cur_hi = max(cur_hi, h);
+      } else {
+        if (cur_lo >= 0) {
+          if (lane == 0 && nr < kMaxRanges) {
+            bars->rng[nr][0] = cur_lo;
+            bars->rng[nr][1] = cur_hi;
+          }
+          ++nr;
+        }
+        cur_lo = l;
+        cur_hi = h;
+      }
+    }
+  }
+  if (cur_lo >= 0) {
+    if (lane == 0 && nr < kMaxRanges) {
+      bars->rng[nr][0] = cur_lo;
+      bars->rng[nr][1] = cur_hi;
+    }
+    ++nr;
+  }
+  if (lane == 0) bars->n_ranges = nr <= kMaxRanges ? nr : -1;
 }
-// visible queries of key span ks among [q0, q0 + 64): 64-bit mask (two words)
-__device__ __forceinline__ void visible_queries(const SpanTable& st, int ks, int q0, int n, uint32_t (&m)[2]) {
+// queries of [q0, q0 + 64) visible to a key of span ks (kc_ks = st.kc[ks]) as a 64-bit mask (two
+// words); qc = the query span holding q0
+__device__ __forceinline__ void visible_queries(const SpanTable& st, int ks, int kc_ks, int qc, int q0, int n,
+                                                uint32_t (&m)[2]) {
   m[0] = m[1] = 0u;
   const int q1 = min(q0 + kQStep, n);
-  for (int qs = span_of(st, q0); qs < st.n && st.start[qs] < q1; ++qs) {
-    if (!span_vis(st, qs, ks)) continue;
+  for (int qs = qc; qs < st.n && st.start[qs] < q1; ++qs) {
+    if (!(qs == ks || kc_ks < st.qth[qs])) continue;
     const int a = max(st.start[qs], q0) - q0, b = min(st.start[qs + 1], q1) - q0;
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
@@ -101,6 +215,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     float* __restrict__ dk_out, __nv_bfloat16* __restrict__ dv_out, int B, int H, int n, int n_pad,
                     float scale_q, float scale_k, const __grid_constant__ SpanTable st) {
   extern __shared__ uint8_t smem_raw[];
+#ifdef DZ_BWD_TRACE
+  const bool bt_on = blockIdx.x == (unsigned)g_bwd_trace_cta;
+#endif
+  if (threadIdx.x == 0) BT(0, 15);
   const uint32_t raw = ptx::smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (base - raw);
@@ -114,11 +232,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(bar(bars->kv_full), 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kQStages; ++i) {
       ptx::mbar_init(bar(bars->q_full[i]), 1);
       ptx::mbar_init(bar(bars->q_empty[i]), 1);
-      ptx::mbar_init(bar(bars->dq_free[i]), 8);
     }
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(bar(bars->dq_free[i]), 8);
     ptx::mbar_init(bar(bars->s_full), 1);
     ptx::mbar_init(bar(bars->s_read), 8);
     ptx::mbar_init(bar(bars->p_ready), 8);
@@ -126,11 +244,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ptx::fence_mbar_init();
   }
   if (warp == kWarpProd) ptx::tmem_alloc<512>(ptx::smem_u32(&bars->tmem_base));
+  if (warp == 0) build_ranges(st, k0, n, bars, lane);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   ptx::pdl_wait();
   const uint32_t tmem = bars->tmem_base;
+#ifdef DZ_BWD_TRACE
+  if (threadIdx.x == 0) {
+    BT_CTA(0, bt_gtime());
+    BT_CTA(3, bt_smid());
+    BT(0, 13);
+  }
+#endif
   // TMEM: S^T [0, 64), dP^T [64, 128) (one step at a time: the next step's are computed once these are in
   // registers), dQ^T of step i in [128 + 64 (i & 1), +64) (drained while later steps run), dV [256, 384),
   // dK [384, 512)
@@ -147,11 +273,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tma_load_4d(base + kOffV + x * kKBox, &tm_v, bar(bars->kv_full), x * 64, h, k0, b, pol);
       }
       uint32_t i = 0;
-      for (int qs = 0; qs < n_qsteps; ++qs) {
-        if (!step_visible(st, qs * kQStep, k0, n)) continue;
-        const uint32_t bi = i & 1, u = i >> 1;
+      Steps steps(bars, st, k0, n);
+      for (int qs = steps.first(st, n_qsteps); qs < n_qsteps; qs = steps.next(st, qs, n_qsteps)) {
+        const uint32_t bi = i % kQStages, u = i / kQStages;
         ptx::mbar_wait(bar(bars->q_empty[bi]), (u & 1) ^ 1);
+        BT(i, 10);
         const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
+#ifdef DZ_BWD_NO_QLOAD
+        if (i >= kQStages) {
+          ptx::mbar_arrive(bar(bars->q_full[bi]));
+          ++i;
+          continue;
+        }
+#endif
         ptx::mbar_arrive_expect_tx(bar(bars->q_full[bi]), 2 * kQTile + 2 * kQStep * 4);
         for (int x = 0; x < 2; ++x) {
           ptx::tma_load_4d(qb + x * kQBox, &tm_q, bar(bars->q_full[bi]), x * 64, h, qs * kQStep, b, pol);
@@ -166,60 +300,71 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     __syncwarp();
   } else if (warp == kWarpMma) {
     // ------------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
-      constexpr uint32_t iS = ptx::idesc_f16(0, 0, 0, 0, 128, 64), iDP = ptx::idesc_f16(1, 1, 0, 0, 128, 64),
-                         iDV = ptx::idesc_f16(1, 1, 0, 1, 128, 128), iDK = ptx::idesc_f16(0, 0, 0, 1, 128, 128),
-                         iDQ = ptx::idesc_f16(0, 0, 1, 1, 128, 64);
-      ptx::mbar_wait(bar(bars->kv_full), 0);
-      // Software-pipelined: S^T / dP^T of step i + 1 are issued before waiting for step i's P^T / dS^T,
-      // so the tensor pipe computes them while the softmax-gradient warps work on step i (and they
-      // complete before step i's dV / dK / dQ^T MMAs, which are issued after them).
-      auto issue_sdp = [&](uint32_t i) {
-        const uint32_t bi = i & 1, u = i >> 1;
-        const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
-        ptx::mbar_wait(bar(bars->q_full[bi]), u & 1);
-        if (i >= 1) ptx::mbar_wait(bar(bars->s_read), (i - 1) & 1);  // S^T / dP^T of step i - 1 are in registers
-        ptx::tc_fence_after();
+    // The whole warp runs the loop; ptx::mma_ss_warp / tc_commit_warp elect the issuing lane inside the
+    // asm (a lane-0 branch costs a per-MMA elect loop: ~63 vs ~40 cycles per issued MMA, measured in
+    // tools/mma_bench.cu).  Software-pipelined: S^T / dP^T of step i + 1 are issued before waiting for
+    // step i's P^T / dS^T, so the tensor pipe computes them while the softmax-gradient warps work on
+    // step i, and they complete before step i's dV / dK / dQ^T, issued after them (one issuing thread:
+    // the pipe runs its MMAs in this order).  Descriptors are formed once; a K-step only moves the start
+    // address field (bits [0,14), address >> 4), which never carries for shared-memory addresses.
+    constexpr uint32_t iS = ptx::idesc_f16(0, 0, 0, 0, 128, 64), iDP = ptx::idesc_f16(1, 1, 0, 0, 128, 64),
+                       iDV = ptx::idesc_f16(1, 1, 0, 1, 128, 128), iDK = ptx::idesc_f16(0, 0, 0, 1, 128, 128),
+                       iDQ = ptx::idesc_f16(0, 0, 1, 1, 128, 64);
+    auto koff = [](int kk, uint32_t box) { return (uint64_t)(((kk / 4) * box + (kk % 4) * 32) >> 4); };
+    auto moff = [](int kk) { return (uint64_t)((kk * 16 * 128) >> 4); };
+    const uint64_t dK = desc_k(base + kOffK, 0, kKBox), dV = desc_k(base + kOffV, 0, kKBox),
+                   dPT = desc_k(base + kOffPT, 0, kPTile), dST = desc_k(base + kOffDST, 0, kPTile),
+                   dKm = desc_mn(base + kOffK, 0, kKBox), dSTm = desc_mn(base + kOffDST, 0, kPTile);
+    ptx::mbar_wait(bar(bars->kv_full), 0);
+    auto issue_sdp = [&](uint32_t i) {
+      const uint32_t bi = i % kQStages, u = i / kQStages;
+      const uint64_t dQ = desc_k(base + kOffQ + bi * kQTile, 0, kQBox), dO = desc_k(base + kOffDO + bi * kQTile, 0, kQBox);
+      if (lane == 0) BT(i, 0);
+      ptx::mbar_wait(bar(bars->q_full[bi]), u & 1);
+      if (lane == 0) BT(i, 11);
+      if (i >= 1) ptx::mbar_wait(bar(bars->s_read), (i - 1) & 1);  // S^T / dP^T of step i - 1 are in registers
+      if (lane == 0) BT(i, 1);
+      #ifndef DZ_BWD_NO_IFENCE
+      ptx::tc_fence_after();
+#endif
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tmem + kS, desc_k(base + kOffK, kk, kKBox), desc_k(qb, kk, kQBox), iS, kk > 0);
+      for (int kk = 0; kk < 8; ++kk) ptx::mma_ss_warp(tmem + kS, dK + koff(kk, kKBox), dQ + koff(kk, kQBox), iS, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tmem + kDP, desc_k(base + kOffV, kk, kKBox), desc_k(ob, kk, kQBox), iDP, kk > 0);
-        ptx::tc_commit(bar(bars->s_full));
-      };
-      auto next_visible = [&](int qs) {
-        while (qs < n_qsteps && !step_visible(st, qs * kQStep, k0, n)) ++qs;
-        return qs;
-      };
-      int qs = next_visible(0);
-      if (qs < n_qsteps) issue_sdp(0);
-      uint32_t i = 0;
-      while (qs < n_qsteps) {
-        const uint32_t bi = i & 1, u = i >> 1;
-        const int qn = next_visible(qs + 1);
-        if (qn < n_qsteps) issue_sdp(i + 1);  // (waits until step i's S^T / dP^T have been read)
-        const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
-        ptx::mbar_wait(bar(bars->p_ready), i & 1);  // P^T and dS^T of step i are in shared memory
-        if (i >= 2) ptx::mbar_wait(bar(bars->dq_free[bi]), (u - 1) & 1);  // dQ^T(i - 2) drained
-        ptx::tc_fence_after();
+      for (int kk = 0; kk < 8; ++kk) ptx::mma_ss_warp(tmem + kDP, dV + koff(kk, kKBox), dO + koff(kk, kQBox), iDP, kk > 0);
+      ptx::tc_commit_warp(bar(bars->s_full));
+      if (lane == 0) BT(i, 16);
+    };
+    // (the walk runs one step ahead: the step after next is found while this step's P^T / dS^T are
+    // being computed, off the issue path)
+    Steps steps(bars, st, k0, n);
+    int qs = steps.first(st, n_qsteps);
+    int qn = qs < n_qsteps ? steps.next(st, qs, n_qsteps) : n_qsteps;
+    if (qs < n_qsteps) issue_sdp(0);
+    for (uint32_t i = 0; qs < n_qsteps; ++i) {
+      const uint32_t bi = i & 1, u = i >> 1, qi = i % kQStages;
+      if (qn < n_qsteps) issue_sdp(i + 1);  // (waits until step i's S^T / dP^T have been read)
+      const int qnn = qn < n_qsteps ? steps.next(st, qn, n_qsteps) : n_qsteps;
+      const uint64_t dQm = desc_mn(base + kOffQ + qi * kQTile, 0, kQBox), dOm = desc_mn(base + kOffDO + qi * kQTile, 0, kQBox);
+      ptx::mbar_wait(bar(bars->p_ready), i & 1);  // P^T and dS^T of step i are in shared memory
+      if (lane == 0) BT(i, 12);
+      if (i >= 2) ptx::mbar_wait(bar(bars->dq_free[bi]), (u - 1) & 1);  // dQ^T(i - 2) drained
+      if (lane == 0) BT(i, 2);
+      #ifndef DZ_BWD_NO_IFENCE
+      ptx::tc_fence_after();
+#endif
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          ptx::mma_ss(tmem + kDV, desc_k(base + kOffPT, kk, kPTile), desc_mn(ob, kk, kQBox), iDV,
-                      (i > 0 || kk > 0) ? 1u : 0u);
+      for (int kk = 0; kk < 4; ++kk)
+        ptx::mma_ss_warp(tmem + kDV, dPT + koff(kk, kPTile), dOm + moff(kk), iDV, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          ptx::mma_ss(tmem + kDK, desc_k(base + kOffDST, kk, kPTile), desc_mn(qb, kk, kQBox), iDK,
-                      (i > 0 || kk > 0) ? 1u : 0u);
+      for (int kk = 0; kk < 4; ++kk)
+        ptx::mma_ss_warp(tmem + kDK, dST + koff(kk, kPTile), dQm + moff(kk), iDK, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          ptx::mma_ss(tmem + kDQ + bi * 64, desc_mn(base + kOffK, kk, kKBox), desc_mn(base + kOffDST, kk, kPTile),
-                      iDQ, kk > 0);
-        ptx::tc_commit(bar(bars->mma_done));
-        ptx::tc_commit(bar(bars->q_empty[bi]));
-        qs = qn;
-        ++i;
-      }
+      for (int kk = 0; kk < 8; ++kk) ptx::mma_ss_warp(tmem + kDQ + bi * 64, dKm + moff(kk), dSTm + moff(kk), iDQ, kk > 0);
+      ptx::tc_commit_warp(bar(bars->mma_done));
+      ptx::tc_commit_warp(bar(bars->q_empty[qi]));
+      if (lane == 0) BT(i, 17);
+      qs = qn;
+      qn = qnn;
     }
     __syncwarp();
   } else {  // warps 0..7
@@ -229,16 +374,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int r = quad * 32 + lane;
     const uint32_t lb = (uint32_t)(quad * 32) << 16;
     const int key = k0 + r;
-    const int ks = span_of(st, min(key, n - 1));
+    const int ks = span_of(st, min(key, n - 1)), kc_ks = st.kc[ks];
     // dQ^T of a step (thread = d row r, its warp's 32 queries): transposed into the staging tile
     // [64 q][128 d] fp32 (thread r writes column r: conflict-free), then one TMA bulk reduce-add into
-    // dQ'[b][q0 .. q0 + 63][h][:] (rows past n clipped).  Staging alternates; its previous reduce must
-    // have read it.
+    // dQ'[b][q0 .. q0 + 63][h][:] (rows past n clipped), once the previous reduce has read the tile.
     uint32_t n_drain = 0;
     auto drain = [&](uint32_t bi, int q0) {
-      const uint32_t sb = base + kOffDQ + (n_drain & 1) * kDQTile;
-      if (threadIdx.x == 0) ptx::bulk_wait_read_all();  // (keeps at most one reduce in flight)
+      const uint32_t sb = base + kOffDQ;
+      if (threadIdx.x == 0) ptx::bulk_wait_read_all();  // the previous reduce has read the staging tile
       ptx::named_bar_sync(1, 256);
+      if (threadIdx.x == 0) BT(n_drain + 1, 8);
+#ifndef DZ_BWD_NO_DRAIN
       uint32_t qr[32];
       ptx::tmem_ld32(tmem + lb + kDQ + bi * 64 + hq * 32, qr);
       ptx::tmem_wait_ld();
@@ -247,35 +393,58 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((hq * 32 + j) * 128 + r) * 4),
                      "f"(__uint_as_float(qr[j]) * scale_q)
                      : "memory");
+#endif
       ptx::fence_proxy_async_smem();
       ptx::named_bar_sync(1, 256);
       if (threadIdx.x == 0) {
+#ifndef DZ_BWD_NO_REDUCE
         ptx::tma_reduce_add_4d(&tm_dq, sb, 0, h, q0, b);
+#endif
         ptx::bulk_commit_group();
       }
       ++n_drain;
     };
     uint32_t i = 0;
     int prev_q0 = 0;
-    for (int qs = 0; qs < n_qsteps; ++qs) {
+    // (the walk and the visibility mask run one step ahead, while the step's math hides their
+    // parameter-space loads)
+    Steps steps(bars, st, k0, n);
+    int qc = 0;  // query span holding the step's first query (only moves forward)
+    auto step_mask = [&](int s) {
+      const int q0 = s * kQStep;
+      while (qc + 1 < st.n && st.start[qc + 1] <= q0) ++qc;
+      uint32_t m[2];
+      visible_queries(st, ks, kc_ks, qc, q0, n, m);
+      return key < n ? m[hq] : 0u;
+    };
+    int qs = steps.first(st, n_qsteps);
+    uint32_t vm = qs < n_qsteps ? step_mask(qs) : 0u;
+    while (qs < n_qsteps) {
       const int q0 = qs * kQStep;
-      if (!step_visible(st, q0, k0, n)) continue;
-      const uint32_t bi = i & 1, u = i >> 1;
-      uint32_t vm2[2];
-      visible_queries(st, ks, q0, n, vm2);
-      const uint32_t vm = key < n ? vm2[hq] : 0u;
-      ptx::mbar_wait(bar(bars->q_full[bi]), u & 1);    // this step's lse2 / delta are in shared memory
+      const uint32_t qi = i % kQStages, uq = i / kQStages;
+      ptx::mbar_wait(bar(bars->q_full[qi]), uq & 1);    // this step's lse2 / delta are in shared memory
       ptx::mbar_wait(bar(bars->s_full), i & 1);
+      if (threadIdx.x == 0) BT(i, 3);
       ptx::tc_fence_after();
       uint32_t sr[32], dr[32];
+#ifndef DZ_BWD_NO_LDS
       ptx::tmem_ld32(tmem + lb + kS + hq * 32, sr);
       ptx::tmem_ld32(tmem + lb + kDP + hq * 32, dr);
       ptx::tmem_wait_ld();
+#else
+      for (int j = 0; j < 32; ++j) sr[j] = dr[j] = __float_as_uint(-100.f + j);
+#endif
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar(bars->s_read));  // the next step's S^T / dP^T may be computed
-      const float* lv = vec + bi * 128 + hq * 32;
+      if (threadIdx.x == 0) BT(i, 4);
+      const int qs_next = steps.next(st, qs, n_qsteps);
+      const uint32_t vm_next = qs_next < n_qsteps ? step_mask(qs_next) : 0u;
+      const float* lv = vec + qi * 128 + hq * 32;
       uint32_t pk[16], dk[16];
+#ifdef DZ_BWD_NO_MATH
+      for (int j = 0; j < 16; ++j) pk[j] = dk[j] = sr[j] ^ dr[j] ^ vm;
+#else
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         float p2[2], d2[2];
@@ -292,27 +461,35 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __half2 hh = __floats2half2_rn(d2[0], d2[1]);
         dk[j] = *reinterpret_cast<uint32_t*>(&hh);
       }
+#endif
+      if (threadIdx.x == 0) BT(i, 5);
       if (i >= 1) {  // the previous step's MMAs have read P^T / dS^T
         ptx::mbar_wait(bar(bars->mma_done), (i - 1) & 1);
         ptx::tc_fence_after();
       }
+#ifndef DZ_BWD_NO_MATH
 #pragma unroll
       for (int j = 0; j < 4; ++j) {  // row r of the [128][64] tiles: this warp's 4 chunks of 8 queries, SW128
         const uint32_t o = r * 128 + (((hq * 4 + j) ^ (r & 7)) << 4);
         ptx::st_shared_v4(base + kOffPT + o, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         ptx::st_shared_v4(base + kOffDST + o, dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
       }
+#endif
       ptx::fence_proxy_async_smem();  // generic stores -> the tensor core's reads
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar(bars->p_ready));
+      if (threadIdx.x == 0) BT(i, 6);
       if (i >= 1) {  // dQ^T of step i - 1 leaves TMEM while step i's MMAs run
         drain((i - 1) & 1, prev_q0);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(bar(bars->dq_free[(i - 1) & 1]));
+        if (threadIdx.x == 0) BT(i, 7);
       }
       prev_q0 = q0;
       ++i;
+      qs = qs_next;
+      vm = vm_next;
     }
     if (i >= 1) {  // the last step's dQ^T (and the final dV / dK)
       ptx::mbar_wait(bar(bars->mma_done), (i - 1) & 1);
@@ -320,6 +497,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       drain((i - 1) & 1, prev_q0);
     }
     if (threadIdx.x == 0) ptx::bulk_wait_all();  // the dQ reduces have completed
+#ifdef DZ_BWD_TRACE
+    if (threadIdx.x == 0) {
+      BT_CTA(2, i);
+      BT(1, 13);
+    }
+#endif
     // dV (bf16) and dK' (fp32) of this thread's key row, columns [64 hq, 64 hq + 64) (tcgen05.ld is
     // warp-collective: every lane loads, only rows < n store)
     const int64_t row = (((int64_t)b * n + min(key, n - 1)) * H + h) * 128;
@@ -359,6 +542,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == kWarpProd) ptx::tmem_dealloc<512>(tmem);
+#ifdef DZ_BWD_TRACE
+  if (threadIdx.x == 0) {
+    BT_CTA(1, bt_gtime());
+    BT(0, 14);
+  }
+#endif
 }
 
 // B1: delta = <dO, O> per (b, h, s) row and lse2 = lse * log2(e); one warp per row of D = 128
@@ -522,3 +711,16 @@ cudaError_t launch_attention_backward(const BwdArgs& a, cudaStream_t s) {
 }
 
 }  // namespace dz
+
+#ifdef DZ_BWD_TRACE
+// diagnostics build only: cta >= 0 arms the trace for that CTA; cta < 0 reads it ([128][24] words)
+extern "C" __attribute__((visibility("default"))) int dz_debug_bwd_trace(int cta, uint32_t* host) {
+  if (cta >= 0) {
+    static uint32_t z[128 * 24];
+    cudaMemcpyToSymbol(dz::g_bwd_trace, z, sizeof z);
+    return (int)cudaMemcpyToSymbol(dz::g_bwd_trace_cta, &cta, sizeof(int));
+  }
+  if (cta == -2) return (int)cudaMemcpyFromSymbol(host, dz::g_bwd_cta, sizeof(uint32_t) * 4096 * 4);
+  return (int)cudaMemcpyFromSymbol(host, dz::g_bwd_trace, sizeof(uint32_t) * 128 * 24);
+}
+#endif
