@@ -32,8 +32,9 @@ namespace {
 
 constexpr int kBwdTile = 128;        // keys per CTA
 constexpr int kQStep = 64;           // queries per step
-constexpr int kBwdThreads = 320;     // warps 0..7 compute (quadrant w % 4, query half w / 4), 8 TMA producer, 9 MMA issuer
-constexpr int kWarpProd = 8, kWarpMma = 9;
+constexpr int kBwdThreads = 448;     // warps 0..7 softmax gradient (quadrant w % 4, query half w / 4), 8 TMA
+                                     // producer, 9 MMA issuer, 10..13 dQ drain (quadrant w % 4)
+constexpr int kWarpProd = 8, kWarpMma = 9, kWarpDrain = 10;
 constexpr int kKTile = 128 * 128 * 2;      // [128 keys][128 d] 16-bit as two [128][64] SW128 boxes
 constexpr int kKBox = 128 * 128;
 constexpr int kQTile = 64 * 128 * 2;       // [64 q][128 d] as two [64][64] boxes
@@ -74,7 +75,7 @@ __device__ __forceinline__ uint32_t bt_smid() {
 
 constexpr int kMaxRanges = 12;  // visible query-step ranges kept per key tile (more: the StepWalk path)
 struct BwdBars {
-  uint64_t kv_full, q_full[kQStages], q_empty[kQStages], s_full, s_read, dq_free[2], p_ready, mma_done;
+  uint64_t kv_full, q_full[kQStages], q_empty[kQStages], s_full, s_read, dq_full[2], dq_free[2], p_ready, mma_done;
   uint32_t tmem_base;
   int32_t n_ranges;              // -1: more than kMaxRanges, walk the span table instead
   int32_t rng[kMaxRanges][2];    // [first, end) query steps, increasing, disjoint
@@ -236,7 +237,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::mbar_init(bar(bars->q_full[i]), 1);
       ptx::mbar_init(bar(bars->q_empty[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) ptx::mbar_init(bar(bars->dq_free[i]), 8);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(bar(bars->dq_full[i]), 1);
+      ptx::mbar_init(bar(bars->dq_free[i]), 4);
+    }
     ptx::mbar_init(bar(bars->s_full), 1);
     ptx::mbar_init(bar(bars->s_read), 8);
     ptx::mbar_init(bar(bars->p_ready), 8);
@@ -361,51 +365,69 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) ptx::mma_ss_warp(tmem + kDQ + bi * 64, dKm + moff(kk), dSTm + moff(kk), iDQ, kk > 0);
       ptx::tc_commit_warp(bar(bars->mma_done));
+      ptx::tc_commit_warp(bar(bars->dq_full[bi]));
       ptx::tc_commit_warp(bar(bars->q_empty[qi]));
       if (lane == 0) BT(i, 17);
       qs = qn;
       qn = qnn;
     }
     __syncwarp();
+  } else if (warp >= kWarpDrain) {
+    // ---------------------------------------------------------------- dQ drain --
+    // dQ^T of step i (thread = d row r, all 64 queries) leaves TMEM once its MMAs complete (dq_full,
+    // one barrier per TMEM buffer, so a drain can never fall a phase behind): transposed into the
+    // staging tile [64 q][128 d] fp32 (thread r writes column r: conflict-free) once the previous
+    // reduce has read it, then one TMA bulk reduce-add into dQ'[b][q0 .. q0 + 63][h][:] (rows past n
+    // clipped) while the next steps run.
+    const int quad = warp % 4;
+    const int r = quad * 32 + lane;
+    const uint32_t lb = (uint32_t)(quad * 32) << 16;
+    const uint32_t sb = base + kOffDQ;
+    const bool leader = warp == kWarpDrain && lane == 0;
+    Steps steps(bars, st, k0, n);
+    uint32_t i = 0;
+    for (int qs = steps.first(st, n_qsteps); qs < n_qsteps; qs = steps.next(st, qs, n_qsteps), ++i) {
+      const uint32_t bi = i & 1, u = i >> 1;
+      ptx::mbar_wait(bar(bars->dq_full[bi]), u & 1);
+      ptx::tc_fence_after();
+      if (leader) ptx::bulk_wait_read_all();  // the previous reduce has read the staging tile
+      ptx::named_bar_sync(1, 128);
+      if (leader) BT(i, 8);
+#ifndef DZ_BWD_NO_DRAIN
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t qr[32];
+        ptx::tmem_ld32(tmem + lb + kDQ + bi * 64 + half * 32, qr);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((half * 32 + j) * 128 + r) * 4),
+                       "f"(__uint_as_float(qr[j]) * scale_q)
+                       : "memory");
+      }
+#endif
+      ptx::tc_fence_before();
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      if (lane == 0) ptx::mbar_arrive(bar(bars->dq_free[bi]));  // the TMEM buffer may take dQ^T(i + 2)
+      if (leader) {
+#ifndef DZ_BWD_NO_REDUCE
+        ptx::tma_reduce_add_4d(&tm_dq, sb, 0, h, qs * kQStep, b);
+#endif
+        ptx::bulk_commit_group();
+        BT(i, 7);
+      }
+    }
+    if (leader) ptx::bulk_wait_all();  // the dQ reduces have completed
   } else {  // warps 0..7
-    // ------------------------------------- softmax-gradient, dQ drain and epilogue --
-    // warp w: TMEM lane quadrant w % 4 (key rows, or d rows for dQ^T), query half hq = w / 4 of each step
+    // ------------------------------------------ softmax gradient and epilogue --
+    // warp w: TMEM lane quadrant w % 4 (key rows), query half hq = w / 4 of each step
     const int quad = warp % 4, hq = warp / 4;
     const int r = quad * 32 + lane;
     const uint32_t lb = (uint32_t)(quad * 32) << 16;
     const int key = k0 + r;
     const int ks = span_of(st, min(key, n - 1)), kc_ks = st.kc[ks];
-    // dQ^T of a step (thread = d row r, its warp's 32 queries): transposed into the staging tile
-    // [64 q][128 d] fp32 (thread r writes column r: conflict-free), then one TMA bulk reduce-add into
-    // dQ'[b][q0 .. q0 + 63][h][:] (rows past n clipped), once the previous reduce has read the tile.
-    uint32_t n_drain = 0;
-    auto drain = [&](uint32_t bi, int q0) {
-      const uint32_t sb = base + kOffDQ;
-      if (threadIdx.x == 0) ptx::bulk_wait_read_all();  // the previous reduce has read the staging tile
-      ptx::named_bar_sync(1, 256);
-      if (threadIdx.x == 0) BT(n_drain + 1, 8);
-#ifndef DZ_BWD_NO_DRAIN
-      uint32_t qr[32];
-      ptx::tmem_ld32(tmem + lb + kDQ + bi * 64 + hq * 32, qr);
-      ptx::tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((hq * 32 + j) * 128 + r) * 4),
-                     "f"(__uint_as_float(qr[j]) * scale_q)
-                     : "memory");
-#endif
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1, 256);
-      if (threadIdx.x == 0) {
-#ifndef DZ_BWD_NO_REDUCE
-        ptx::tma_reduce_add_4d(&tm_dq, sb, 0, h, q0, b);
-#endif
-        ptx::bulk_commit_group();
-      }
-      ++n_drain;
-    };
     uint32_t i = 0;
-    int prev_q0 = 0;
     // (the walk and the visibility mask run one step ahead, while the step's math hides their
     // parameter-space loads)
     Steps steps(bars, st, k0, n);
@@ -438,28 +460,42 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar(bars->s_read));  // the next step's S^T / dP^T may be computed
       if (threadIdx.x == 0) BT(i, 4);
-      const int qs_next = steps.next(st, qs, n_qsteps);
-      const uint32_t vm_next = qs_next < n_qsteps ? step_mask(qs_next) : 0u;
-      const float* lv = vec + qi * 128 + hq * 32;
+      const float4* lv = reinterpret_cast<const float4*>(vec + qi * 128 + hq * 32);  // lse2 [64] | delta [64]
       uint32_t pk[16], dk[16];
 #ifdef DZ_BWD_NO_MATH
       for (int j = 0; j < 16; ++j) pk[j] = dk[j] = sr[j] ^ dr[j] ^ vm;
 #else
+      // pairs of queries in packed fp32x2 arithmetic; 2^x on MUFU for 5 pairs in 8 and by the FMA-pipe
+      // polynomial (ptx::f2_exp2_poly, rel. error ~1e-4, below bf16 P's rounding) for the other 3
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float p2[2], d2[2];
+      for (int j4 = 0; j4 < 8; ++j4) {
+        const float4 l4 = lv[j4], d4 = lv[16 + j4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int qi = 2 * j + e;
-          const bool vis = (vm >> qi) & 1u;
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int j = 2 * j4 + h2, q = 2 * j;
+          const float la = h2 ? l4.z : l4.x, lb2 = h2 ? l4.w : l4.y, da = h2 ? d4.z : d4.x, db = h2 ? d4.w : d4.y;
+          const uint64_t x = ptx::f2_add(ptx::f2_pack(__uint_as_float(sr[q]), __uint_as_float(sr[q + 1])),
+                                         ptx::f2_pack(-la, -lb2));
+          uint64_t p;
+          if (j % 8 == 2 || j % 8 == 5 || j % 8 == 7) {
+            p = ptx::f2_exp2_poly<true>(x);
+          } else {
+            float x0, x1;
+            ptx::f2_unpack(x, x0, x1);
+            p = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
+          }
+          const uint64_t dd = ptx::f2_add(ptx::f2_pack(__uint_as_float(dr[q]), __uint_as_float(dr[q + 1])),
+                                          ptx::f2_pack(-da, -db));
+          const uint64_t ds = ptx::f2_mul(p, dd);
+          float p0, p1, s0, s1;
+          ptx::f2_unpack(p, p0, p1);
+          ptx::f2_unpack(ds, s0, s1);
           // (lse2 / delta past n are unwritten workspace: select, never multiply, masked entries)
-          const float p = vis ? ptx::ex2(__uint_as_float(sr[qi]) - lv[qi]) : 0.f;
-          p2[e] = p;
-          d2[e] = vis ? p * (__uint_as_float(dr[qi]) - lv[64 + qi]) : 0.f;
+          const bool v0 = (vm >> q) & 1u, v1 = (vm >> (q + 1)) & 1u;
+          pk[j] = ptx::pack_bf16x2(v0 ? p0 : 0.f, v1 ? p1 : 0.f);
+          __half2 hh = __floats2half2_rn(v0 ? s0 : 0.f, v1 ? s1 : 0.f);
+          dk[j] = *reinterpret_cast<uint32_t*>(&hh);
         }
-        pk[j] = ptx::pack_bf16x2(p2[0], p2[1]);
-        __half2 hh = __floats2half2_rn(d2[0], d2[1]);
-        dk[j] = *reinterpret_cast<uint32_t*>(&hh);
       }
 #endif
       if (threadIdx.x == 0) BT(i, 5);
@@ -479,24 +515,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar(bars->p_ready));
       if (threadIdx.x == 0) BT(i, 6);
-      if (i >= 1) {  // dQ^T of step i - 1 leaves TMEM while step i's MMAs run
-        drain((i - 1) & 1, prev_q0);
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(bar(bars->dq_free[(i - 1) & 1]));
-        if (threadIdx.x == 0) BT(i, 7);
-      }
-      prev_q0 = q0;
+      // the next step and its visibility mask (parameter-space loads) while the MMAs run
+      const int qs_next = steps.next(st, qs, n_qsteps);
+      const uint32_t vm_next = qs_next < n_qsteps ? step_mask(qs_next) : 0u;
       ++i;
       qs = qs_next;
       vm = vm_next;
     }
-    if (i >= 1) {  // the last step's dQ^T (and the final dV / dK)
+    if (i >= 1) {  // the final dV / dK
       ptx::mbar_wait(bar(bars->mma_done), (i - 1) & 1);
       ptx::tc_fence_after();
-      drain((i - 1) & 1, prev_q0);
     }
-    if (threadIdx.x == 0) ptx::bulk_wait_all();  // the dQ reduces have completed
 #ifdef DZ_BWD_TRACE
     if (threadIdx.x == 0) {
       BT_CTA(2, i);
@@ -551,28 +580,45 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // B1: delta = <dO, O> per (b, h, s) row and lse2 = lse * log2(e); one warp per row of D = 128
-__global__ void delta_kernel(const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
-                             const float* __restrict__ lse, float* __restrict__ delta, float* __restrict__ lse2, int B,
-                             int n, int H, int n_pad) {
-  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  if (wid >= (int64_t)B * n * H) return;
-  const int h = (int)(wid % H), s = (int)((wid / H) % n), b = (int)(wid / ((int64_t)H * n));
-  const int64_t row = wid * 128 + lane * 4;  // [b][s][h][d], 4 elements per lane
-  const uint2 o = *reinterpret_cast<const uint2*>(out + row), g = *reinterpret_cast<const uint2*>(dout + row);
-  const float o4[4] = {__uint_as_float(o.x << 16), __uint_as_float(o.x & 0xFFFF0000u), __uint_as_float(o.y << 16),
-                       __uint_as_float(o.y & 0xFFFF0000u)};
-  const float g4[4] = {__uint_as_float(g.x << 16), __uint_as_float(g.x & 0xFFFF0000u), __uint_as_float(g.y << 16),
-                       __uint_as_float(g.y & 0xFFFF0000u)};
-  float acc = 0.f;
+// B1: 16 lanes per (b, s, h) row of D = 128 (8 elements, one 16-byte load of O and of dO each), two
+// rows per warp instruction, kDeltaRows rows per warp with all loads issued before the reductions.
+constexpr int kDeltaRows = 8;
+__global__ void __launch_bounds__(256) delta_kernel(const __nv_bfloat16* __restrict__ dout,
+                                                   const __nv_bfloat16* __restrict__ out, const float* __restrict__ lse,
+                                                   float* __restrict__ delta, float* __restrict__ lse2, int B, int n,
+                                                   int H, int n_pad) {
+  const int64_t rows = (int64_t)B * n * H;
+  const int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32) * kDeltaRows;
+  const int lane = threadIdx.x % 32, half = lane / 16, l16 = lane % 16;
+  uint4 o[kDeltaRows / 2], g[kDeltaRows / 2];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) acc = fmaf(o4[e], g4[e], acc);
+  for (int k = 0; k < kDeltaRows / 2; ++k) {
+    const int64_t wid = w0 + 2 * k + half;
+    if (wid < rows) {
+      o[k] = __ldg(reinterpret_cast<const uint4*>(out + wid * 128) + l16);
+      g[k] = __ldg(reinterpret_cast<const uint4*>(dout + wid * 128) + l16);
+    } else {
+      o[k] = g[k] = make_uint4(0, 0, 0, 0);
+    }
+  }
 #pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
-  if (lane == 0) {  // rows of n_pad (a multiple of 64: the attention backward reads whole 64-query steps)
-    const int64_t i = ((int64_t)b * H + h) * n_pad + s;
-    delta[i] = acc;
-    lse2[i] = lse[((int64_t)b * H + h) * n + s] * 1.4426950408889634f;
+  for (int k = 0; k < kDeltaRows / 2; ++k) {
+    const uint32_t ov[4] = {o[k].x, o[k].y, o[k].z, o[k].w}, gv[4] = {g[k].x, g[k].y, g[k].z, g[k].w};
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc = fmaf(__uint_as_float(ov[e] << 16), __uint_as_float(gv[e] << 16), acc);
+      acc = fmaf(__uint_as_float(ov[e] & 0xFFFF0000u), __uint_as_float(gv[e] & 0xFFFF0000u), acc);
+    }
+#pragma unroll
+    for (int m = 8; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    const int64_t wid = w0 + 2 * k + half;
+    if (l16 == 0 && wid < rows) {  // rows of n_pad (a multiple of 64: the attention backward reads whole steps)
+      const int h = (int)(wid % H), s = (int)((wid / H) % n), b = (int)(wid / ((int64_t)H * n));
+      const int64_t i = ((int64_t)b * H + h) * n_pad + s;
+      delta[i] = acc;
+      lse2[i] = lse[((int64_t)b * H + h) * n + s] * 1.4426950408889634f;
+    }
   }
 }
 
@@ -597,52 +643,77 @@ struct ProBwdArgs {
 };
 constexpr int kProBwdTokens = 64;
 
-__global__ void __launch_bounds__(256) prologue_bwd_kernel(const __grid_constant__ ProBwdArgs a) {
-  constexpr int D = 128;
-  const int w = blockIdx.z, h = blockIdx.y;
+#ifndef DZ_PB_R  // rows per warp pass / CTAs per SM: 2 / 4 measured best (64 registers, no spills)
+#define DZ_PB_R 2
+#define DZ_PB_MIN 4
+#endif
+__global__ void __launch_bounds__(256, DZ_PB_MIN) prologue_bwd_kernel(const __grid_constant__ ProBwdArgs a) {
+  constexpr int D = 128, R = DZ_PB_R;  // R rows per warp pass: all their loads are issued before the math
+  // blockIdx.x = head (fastest: CTAs running together read the neighbouring heads of the same tokens,
+  // whole [H][D] rows of the token-major tensors), blockIdx.y = run of tokens, blockIdx.z = q / k
+  const int w = blockIdx.z, h = blockIdx.x, tb = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int j0 = 2 * lane;  // this lane's rotation pairs j0, j0 + 1 (elements 4 lane .. 4 lane + 3)
   const float* gp = a.gain[w] + h * D + 4 * lane;
   const float g4[4] = {gp[0], gp[1], gp[2], gp[3]};
   float dg[4] = {0.f, 0.f, 0.f, 0.f};
   const int ax0 = a.axis[j0], ax1 = a.axis[j0 + 1];
-  const int items = a.B * a.n;
-  for (int it = blockIdx.x * kProBwdTokens + warp; it < min(items, (int)(blockIdx.x + 1) * kProBwdTokens); it += 8) {
-    const int b = it / a.n, t = it - b * a.n;
-    const int64_t row = (((int64_t)b * a.n + t) * a.H + h) * D + 4 * lane;
-    const uint2 xr = *reinterpret_cast<const uint2*>(a.x[w] + row);
-    const float x4[4] = {__uint_as_float(xr.x << 16), __uint_as_float(xr.x & 0xFFFF0000u),
-                         __uint_as_float(xr.y << 16), __uint_as_float(xr.y & 0xFFFF0000u)};
-    float ss = 0.f;
+  const int items = a.B * a.n, it_end = min(items, (tb + 1) * kProBwdTokens);
+  for (int it0 = tb * kProBwdTokens + warp * R; it0 < it_end; it0 += 8 * R) {
+    uint2 xr[R];
+    float4 d4[R];
+    int p0[R], p1[R];
+    int64_t row[R];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) ss = fmaf(x4[e], x4[e], ss);
+    for (int k = 0; k < R; ++k) {
+      const int it = min(it0 + k, it_end - 1);
+      const int b = it / a.n, t = it - b * a.n;
+      row[k] = (((int64_t)b * a.n + t) * a.H + h) * D + 4 * lane;
+      xr[k] = __ldg(reinterpret_cast<const uint2*>(a.x[w] + row[k]));
+      d4[k] = __ldcs(reinterpret_cast<const float4*>(a.dxp[w] + row[k]));
+      p0[k] = __ldg(a.pos + 3 * t + ax0);
+      p1[k] = __ldg(a.pos + 3 * t + ax1);
+    }
+    float2 c0[R], c1[R];
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
-    const float inv = rsqrtf(ss * (1.0f / D) + a.eps);
-    const float4 d4 = *reinterpret_cast<const float4*>(a.dxp[w] + row);
-    const int p0 = a.pos[3 * t + ax0], p1 = a.pos[3 * t + ax1];
-    const float2 c0 = (unsigned)p0 < (unsigned)a.tab_len ? a.tab[(size_t)p0 * (D / 2) + j0]
-                                                         : make_float2((float)cos(p0 * a.omega[j0]), (float)sin(p0 * a.omega[j0]));
-    const float2 c1 = (unsigned)p1 < (unsigned)a.tab_len ? a.tab[(size_t)p1 * (D / 2) + j0 + 1]
-                                                         : make_float2((float)cos(p1 * a.omega[j0 + 1]), (float)sin(p1 * a.omega[j0 + 1]));
-    // dy = R(-phi) dx' per pair
-    const float dy[4] = {d4.x * c0.x + d4.y * c0.y, -d4.x * c0.y + d4.y * c0.x,
-                         d4.z * c1.x + d4.w * c1.y, -d4.z * c1.y + d4.w * c1.x};
-    float xh[4], dxh[4], dot = 0.f;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      xh[e] = x4[e] * inv;
-      dg[e] = fmaf(dy[e], xh[e], dg[e]);
-      dxh[e] = dy[e] * g4[e];
-      dot = fmaf(dxh[e], xh[e], dot);
+    for (int k = 0; k < R; ++k) {
+      c0[k] = (unsigned)p0[k] < (unsigned)a.tab_len ? __ldg(a.tab + (size_t)p0[k] * (D / 2) + j0)
+                                                  : make_float2((float)cos(p0[k] * a.omega[j0]), (float)sin(p0[k] * a.omega[j0]));
+      c1[k] = (unsigned)p1[k] < (unsigned)a.tab_len
+                  ? __ldg(a.tab + (size_t)p1[k] * (D / 2) + j0 + 1)
+                  : make_float2((float)cos(p1[k] * a.omega[j0 + 1]), (float)sin(p1[k] * a.omega[j0 + 1]));
     }
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, m);
-    const float mdot = dot * (1.0f / D);
-    float dx[4];
+    for (int k = 0; k < R; ++k) {
+      if (it0 + k >= it_end) break;
+      const float x4[4] = {__uint_as_float(xr[k].x << 16), __uint_as_float(xr[k].x & 0xFFFF0000u),
+                           __uint_as_float(xr[k].y << 16), __uint_as_float(xr[k].y & 0xFFFF0000u)};
+      float ss = 0.f;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) dx[e] = (dxh[e] - xh[e] * mdot) * inv;
-    *reinterpret_cast<uint2*>(a.dx[w] + row) = make_uint2(ptx::pack_bf16x2(dx[0], dx[1]), ptx::pack_bf16x2(dx[2], dx[3]));
+      for (int e = 0; e < 4; ++e) ss = fmaf(x4[e], x4[e], ss);
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+      const float inv = rsqrtf(ss * (1.0f / D) + a.eps);
+      // dy = R(-phi) dx' per pair
+      const float dy[4] = {d4[k].x * c0[k].x + d4[k].y * c0[k].y, -d4[k].x * c0[k].y + d4[k].y * c0[k].x,
+                           d4[k].z * c1[k].x + d4[k].w * c1[k].y, -d4[k].z * c1[k].y + d4[k].w * c1[k].x};
+      float xh[4], dxh[4], dot = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        xh[e] = x4[e] * inv;
+        dg[e] = fmaf(dy[e], xh[e], dg[e]);
+        dxh[e] = dy[e] * g4[e];
+        dot = fmaf(dxh[e], xh[e], dot);
+      }
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, m);
+      const float mdot = dot * (1.0f / D);
+      float dx[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dx[e] = (dxh[e] - xh[e] * mdot) * inv;
+      __stcs(reinterpret_cast<uint2*>(a.dx[w] + row[k]),
+             make_uint2(ptx::pack_bf16x2(dx[0], dx[1]), ptx::pack_bf16x2(dx[2], dx[3])));
+    }
   }
   __shared__ float red[8][D];
 #pragma unroll
@@ -661,7 +732,7 @@ cudaError_t launch_attention_backward(const BwdArgs& a, cudaStream_t s) {
   if (a.D != 128) return cudaErrorInvalidValue;
   // B1
   {
-    const int64_t warps = (int64_t)a.B * a.n * a.H;
+    const int64_t warps = ((int64_t)a.B * a.n * a.H + kDeltaRows - 1) / kDeltaRows;
     const int threads = 256;
     delta_kernel<<<(unsigned)((warps * 32 + threads - 1) / threads), threads, 0, s>>>(
         static_cast<const __nv_bfloat16*>(a.dout), static_cast<const __nv_bfloat16*>(a.out), a.lse, a.delta, a.lse2,
@@ -705,7 +776,7 @@ cudaError_t launch_attention_backward(const BwdArgs& a, cudaStream_t s) {
       p.axis[j] = a.axis[j];
     }
     const unsigned blocks = (unsigned)((a.B * a.n + kProBwdTokens - 1) / kProBwdTokens);
-    prologue_bwd_kernel<<<dim3(blocks, (unsigned)a.H, 2), 256, 0, s>>>(p);
+    prologue_bwd_kernel<<<dim3((unsigned)a.H, blocks, 2), 256, 0, s>>>(p);
     return cudaGetLastError();
   }
 }
