@@ -401,9 +401,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((half * 32 + j) * 128 + r) * 4),
-                       "f"(__uint_as_float(qr[j]) * scale_q)
-                       : "memory");
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((half * 32 + j) * 128 + r) * 4), "r"(qr[j]) : "memory");
       }
 #endif
       ptx::tc_fence_before();
@@ -442,7 +440,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     int qs = steps.first(st, n_qsteps);
     uint32_t vm = qs < n_qsteps ? step_mask(qs) : 0u;
     while (qs < n_qsteps) {
-      const int q0 = qs * kQStep;
       const uint32_t qi = i % kQStages, uq = i / kQStages;
       ptx::mbar_wait(bar(bars->q_full[qi]), uq & 1);    // this step's lse2 / delta are in shared memory
       ptx::mbar_wait(bar(bars->s_full), i & 1);
@@ -474,8 +471,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int h2 = 0; h2 < 2; ++h2) {
           const int j = 2 * j4 + h2, q = 2 * j;
           const float la = h2 ? l4.z : l4.x, lb2 = h2 ? l4.w : l4.y, da = h2 ? d4.z : d4.x, db = h2 ? d4.w : d4.y;
-          const uint64_t x = ptx::f2_add(ptx::f2_pack(__uint_as_float(sr[q]), __uint_as_float(sr[q + 1])),
-                                         ptx::f2_pack(-la, -lb2));
+          // masked pairs (Fig. 10, queries or keys past n) get s = -inf: p = 2^-inf = 0 and dS = 0 x
+          // (dP - delta) = 0 (dP and delta are finite: dO rows past n load as zeros, delta is padded)
+          const float s0m = ((vm >> q) & 1u) ? __uint_as_float(sr[q]) : -INFINITY,
+                      s1m = ((vm >> (q + 1)) & 1u) ? __uint_as_float(sr[q + 1]) : -INFINITY;
+          const uint64_t x = ptx::f2_add(ptx::f2_pack(s0m, s1m), ptx::f2_pack(-la, -lb2));
           uint64_t p;
           if (j % 8 == 2 || j % 8 == 5 || j % 8 == 7) {
             p = ptx::f2_exp2_poly<true>(x);
@@ -490,10 +490,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           float p0, p1, s0, s1;
           ptx::f2_unpack(p, p0, p1);
           ptx::f2_unpack(ds, s0, s1);
-          // (lse2 / delta past n are unwritten workspace: select, never multiply, masked entries)
-          const bool v0 = (vm >> q) & 1u, v1 = (vm >> (q + 1)) & 1u;
-          pk[j] = ptx::pack_bf16x2(v0 ? p0 : 0.f, v1 ? p1 : 0.f);
-          __half2 hh = __floats2half2_rn(v0 ? s0 : 0.f, v1 ? s1 : 0.f);
+          pk[j] = ptx::pack_bf16x2(p0, p1);
+          __half2 hh = __floats2half2_rn(s0, s1);
           dk[j] = *reinterpret_cast<uint32_t*>(&hh);
         }
       }
@@ -618,6 +616,8 @@ __global__ void __launch_bounds__(256) delta_kernel(const __nv_bfloat16* __restr
       const int64_t i = ((int64_t)b * H + h) * n_pad + s;
       delta[i] = acc;
       lse2[i] = lse[((int64_t)b * H + h) * n + s] * 1.4426950408889634f;
+      if (s == n - 1)  // queries [n, n_pad): finite values, so masked scores (-inf) give p = 0 and dS = 0
+        for (int e = 1; s + e < n_pad; ++e) delta[i + e] = lse2[i + e] = 0.f;
     }
   }
 }
@@ -629,7 +629,8 @@ __global__ void __launch_bounds__(256) delta_kernel(const __nv_bfloat16* __restr
 // added once (fp32 atomics).
 struct ProBwdArgs {
   const __nv_bfloat16* x[2];  // raw q, k [B][n][H][D]
-  const float* dxp[2];        // dq', dk' fp32 [B][n][H][D]
+  const float* dxp[2];        // dq', dk' fp32 [B][n][H][D], times dscale[w]
+  float dscale[2];
   const float* gain[2];       // [H][D]
   __nv_bfloat16* dx[2];       // dq, dk bf16 [B][n][H][D]
   float* dgain[2];            // [H][D], accumulated
@@ -695,8 +696,10 @@ __global__ void __launch_bounds__(256, DZ_PB_MIN) prologue_bwd_kernel(const __gr
       for (int m = 16; m >= 1; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
       const float inv = rsqrtf(ss * (1.0f / D) + a.eps);
       // dy = R(-phi) dx' per pair
-      const float dy[4] = {d4[k].x * c0[k].x + d4[k].y * c0[k].y, -d4[k].x * c0[k].y + d4[k].y * c0[k].x,
-                           d4[k].z * c1[k].x + d4[k].w * c1[k].y, -d4[k].z * c1[k].y + d4[k].w * c1[k].x};
+      const float sc = a.dscale[w];
+      const float4 dd = make_float4(d4[k].x * sc, d4[k].y * sc, d4[k].z * sc, d4[k].w * sc);
+      const float dy[4] = {dd.x * c0[k].x + dd.y * c0[k].y, -dd.x * c0[k].y + dd.y * c0[k].x,
+                           dd.z * c1[k].x + dd.w * c1[k].y, -dd.z * c1[k].y + dd.w * c1[k].x};
       float xh[4], dxh[4], dot = 0.f;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -758,6 +761,8 @@ cudaError_t launch_attention_backward(const BwdArgs& a, cudaStream_t s) {
     p.x[1] = static_cast<const __nv_bfloat16*>(a.k_raw);
     p.dxp[0] = a.dq_acc;
     p.dxp[1] = a.dk;
+    p.dscale[0] = a.scale_q;  // dQ' accumulates K'^T dS^T unscaled
+    p.dscale[1] = 1.f;        // dK' is scaled in the attention epilogue
     p.gain[0] = a.gain[0];
     p.gain[1] = a.gain[1];
     p.dx[0] = static_cast<__nv_bfloat16*>(a.dq);

@@ -376,13 +376,14 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
           uint8_t* dst = static_cast<uint8_t*>(PEER ? pbase[w][i] : o.base) + base + ooff[w][i];
           *reinterpret_cast<uint2*>(dst) = make_uint2((uint32_t)q8[0] | ((uint32_t)q8[1] << 16),
                                                       (uint32_t)q8[2] | ((uint32_t)q8[3] << 16));
-          continue;
-        }
-        uint32_t pk[4];
+        } else {
+          uint32_t pk[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
-        reinterpret_cast<uint4*>(static_cast<__half*>(PEER ? pbase[w][i] : o.base) + base + ooff[w][i])[0] =
-            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          for (int e = 0; e < 4; ++e)
+            pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
+          reinterpret_cast<uint4*>(static_cast<__half*>(PEER ? pbase[w][i] : o.base) + base + ooff[w][i])[0] =
+              make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
       }
     }
 #pragma unroll
