@@ -443,7 +443,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   ptx::cluster_sync();  // both CTAs' barriers initialised and TMEM allocated before any remote traffic
   ptx::tc_fence_after();
-  ptx::pdl_wait();      // the prologue's Q' / K' / V (and everything before it) are complete
   const uint32_t tmem = bars->tmem_base;
   const int32_t* gpre = bars->gpre;
   // Hybrid schedule: all but the last ~1.x waves of units are dealt whole, round-robin (unit u
@@ -476,6 +475,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncthreads();
   }
 
+  // (the schedule above depends on the launch parameters only: it is computed while the
+  // predecessor finishes)
+  ptx::pdl_wait();      // the prologue's Q' / K' / V (and everything before it) are complete
   Sched sched0;
   sched0.streamk = streamk;
   sched0.P = ncl;
