@@ -32,9 +32,14 @@ namespace {
 
 constexpr int kBwdTile = 128;        // keys per CTA
 constexpr int kQStep = 64;           // queries per step
-constexpr int kBwdThreads = 448;     // warps 0..7 softmax gradient (quadrant w % 4, query half w / 4), 8 TMA
-                                     // producer, 9 MMA issuer, 10..13 dQ drain (quadrant w % 4)
-constexpr int kWarpProd = 8, kWarpMma = 9, kWarpDrain = 10;
+#ifndef DZ_BWD_QW
+#define DZ_BWD_QW 32
+#endif
+constexpr int kQW = DZ_BWD_QW;               // queries of a step per softmax-gradient warp
+constexpr int kQS = 64 / kQW;                // query slices of a step
+constexpr int kCompWarps = 4 * kQS;          // softmax-gradient warps: TMEM lane quadrant w % 4, slice w / 4
+constexpr int kWarpProd = kCompWarps, kWarpMma = kCompWarps + 1, kWarpDrain = kCompWarps + 2;  // + 4 drain warps
+constexpr int kBwdThreads = (kCompWarps + 6) * 32;
 constexpr int kKTile = 128 * 128 * 2;      // [128 keys][128 d] 16-bit as two [128][64] SW128 boxes
 constexpr int kKBox = 128 * 128;
 constexpr int kQTile = 64 * 128 * 2;       // [64 q][128 d] as two [64][64] boxes
@@ -242,8 +247,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::mbar_init(bar(bars->dq_free[i]), 4);
     }
     ptx::mbar_init(bar(bars->s_full), 1);
-    ptx::mbar_init(bar(bars->s_read), 8);
-    ptx::mbar_init(bar(bars->p_ready), 8);
+    ptx::mbar_init(bar(bars->s_read), kCompWarps);
+    ptx::mbar_init(bar(bars->p_ready), kCompWarps);
     ptx::mbar_init(bar(bars->mma_done), 1);
     ptx::fence_mbar_init();
   }
@@ -417,9 +422,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
     if (leader) ptx::bulk_wait_all();  // the dQ reduces have completed
-  } else {  // warps 0..7
+  } else {  // warps 0 .. kCompWarps - 1
     // ------------------------------------------ softmax gradient and epilogue --
-    // warp w: TMEM lane quadrant w % 4 (key rows), query half hq = w / 4 of each step
+    // warp w: TMEM lane quadrant w % 4 (key rows), query slice hq = w / 4 (kQW queries) of each step
     const int quad = warp % 4, hq = warp / 4;
     const int r = quad * 32 + lane;
     const uint32_t lb = (uint32_t)(quad * 32) << 16;
@@ -435,7 +440,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       while (qc + 1 < st.n && st.start[qc + 1] <= q0) ++qc;
       uint32_t m[2];
       visible_queries(st, ks, kc_ks, qc, q0, n, m);
-      return key < n ? m[hq] : 0u;
+      const uint32_t wbits = (m[(hq * kQW) / 32] >> ((hq * kQW) % 32)) & (kQW == 32 ? 0xffffffffu : ((1u << kQW) - 1u));
+      return key < n ? wbits : 0u;
     };
     int qs = steps.first(st, n_qsteps);
     uint32_t vm = qs < n_qsteps ? step_mask(qs) : 0u;
@@ -445,27 +451,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::mbar_wait(bar(bars->s_full), i & 1);
       if (threadIdx.x == 0) BT(i, 3);
       ptx::tc_fence_after();
-      uint32_t sr[32], dr[32];
-#ifndef DZ_BWD_NO_LDS
-      ptx::tmem_ld32(tmem + lb + kS + hq * 32, sr);
-      ptx::tmem_ld32(tmem + lb + kDP + hq * 32, dr);
+      uint32_t sr[kQW], dr[kQW];
+      if constexpr (kQW == 32) {
+        ptx::tmem_ld32(tmem + lb + kS + hq * kQW, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        ptx::tmem_ld32(tmem + lb + kDP + hq * kQW, *reinterpret_cast<uint32_t(*)[32]>(dr));
+      } else {
+        ptx::tmem_ld16(tmem + lb + kS + hq * kQW, *reinterpret_cast<uint32_t(*)[16]>(sr));
+        ptx::tmem_ld16(tmem + lb + kDP + hq * kQW, *reinterpret_cast<uint32_t(*)[16]>(dr));
+      }
       ptx::tmem_wait_ld();
-#else
-      for (int j = 0; j < 32; ++j) sr[j] = dr[j] = __float_as_uint(-100.f + j);
-#endif
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar(bars->s_read));  // the next step's S^T / dP^T may be computed
       if (threadIdx.x == 0) BT(i, 4);
-      const float4* lv = reinterpret_cast<const float4*>(vec + qi * 128 + hq * 32);  // lse2 [64] | delta [64]
-      uint32_t pk[16], dk[16];
+      const float4* lv = reinterpret_cast<const float4*>(vec + qi * 128 + hq * kQW);  // lse2 [64] | delta [64]
+      uint32_t pk[kQW / 2], dk[kQW / 2];
 #ifdef DZ_BWD_NO_MATH
-      for (int j = 0; j < 16; ++j) pk[j] = dk[j] = sr[j] ^ dr[j] ^ vm;
+      for (int j = 0; j < kQW / 2; ++j) pk[j] = dk[j] = sr[j] ^ dr[j] ^ vm;
 #else
-      // pairs of queries in packed fp32x2 arithmetic; 2^x on MUFU for 5 pairs in 8 and by the FMA-pipe
-      // polynomial (ptx::f2_exp2_poly, rel. error ~1e-4, below bf16 P's rounding) for the other 3
+      // pairs of queries in packed fp32x2 arithmetic, 2^x on MUFU (moving 1-4 pairs in 8 to the FMA-pipe
+      // polynomial measured slower: the warps are bound by their instruction count, not by MUFU)
 #pragma unroll
-      for (int j4 = 0; j4 < 8; ++j4) {
+      for (int j4 = 0; j4 < kQW / 4; ++j4) {
         const float4 l4 = lv[j4], d4 = lv[16 + j4];
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
@@ -476,14 +483,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const float s0m = ((vm >> q) & 1u) ? __uint_as_float(sr[q]) : -INFINITY,
                       s1m = ((vm >> (q + 1)) & 1u) ? __uint_as_float(sr[q + 1]) : -INFINITY;
           const uint64_t x = ptx::f2_add(ptx::f2_pack(s0m, s1m), ptx::f2_pack(-la, -lb2));
-          uint64_t p;
-          if (j % 8 == 2 || j % 8 == 5 || j % 8 == 7) {
-            p = ptx::f2_exp2_poly<true>(x);
-          } else {
-            float x0, x1;
-            ptx::f2_unpack(x, x0, x1);
-            p = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
-          }
+          float x0, x1;
+          ptx::f2_unpack(x, x0, x1);
+          const uint64_t p = ptx::f2_pack(ptx::ex2(x0), ptx::ex2(x1));
           const uint64_t dd = ptx::f2_add(ptx::f2_pack(__uint_as_float(dr[q]), __uint_as_float(dr[q + 1])),
                                           ptx::f2_pack(-da, -db));
           const uint64_t ds = ptx::f2_mul(p, dd);
@@ -503,8 +505,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
 #ifndef DZ_BWD_NO_MATH
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {  // row r of the [128][64] tiles: this warp's 4 chunks of 8 queries, SW128
-        const uint32_t o = r * 128 + (((hq * 4 + j) ^ (r & 7)) << 4);
+      for (int j = 0; j < kQW / 8; ++j) {  // row r of the [128][64] tiles: this warp's chunks of 8 queries, SW128
+        const uint32_t o = r * 128 + (((hq * (kQW / 8) + j) ^ (r & 7)) << 4);
         ptx::st_shared_v4(base + kOffPT + o, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         ptx::st_shared_v4(base + kOffDST + o, dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
       }
@@ -530,20 +532,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       BT(1, 13);
     }
 #endif
-    // dV (bf16) and dK' (fp32) of this thread's key row, columns [64 hq, 64 hq + 64) (tcgen05.ld is
-    // warp-collective: every lane loads, only rows < n store)
+    // dV (bf16) and dK' (fp32) of this thread's key row, columns [128 / kQS hq, + 128 / kQS) (tcgen05.ld
+    // is warp-collective: every lane loads, only rows < n store)
     const int64_t row = (((int64_t)b * n + min(key, n - 1)) * H + h) * 128;
     const bool store = key < n;
     if (i == 0) {  // no query sees these keys: zero gradients
       if (store)
-        for (int d = hq * 64; d < hq * 64 + 64; d += 8) {
+        for (int d = hq * (128 / kQS); d < (hq + 1) * (128 / kQS); d += 8) {
           *reinterpret_cast<uint4*>(dv_out + row + d) = make_uint4(0, 0, 0, 0);
           *reinterpret_cast<float4*>(dk_out + row + d) = make_float4(0.f, 0.f, 0.f, 0.f);
           *reinterpret_cast<float4*>(dk_out + row + d + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     } else {
 #pragma unroll 1
-      for (int c = 2 * hq; c < 2 * hq + 2; ++c) {
+      for (int c = hq * (4 / kQS); c < (hq + 1) * (4 / kQS); ++c) {
         uint32_t vr[32], kr[32];
         ptx::tmem_ld32(tmem + lb + kDV + c * 32, vr);
         ptx::tmem_ld32(tmem + lb + kDK + c * 32, kr);
