@@ -50,7 +50,7 @@ constexpr int kPTile = 128 * 64 * 2;       // [128 keys][64 q]: one box
 // kQStages: a step's tiles are loaded while the two before it run), P^T, dS^T, the dQ staging tile
 constexpr int kQStages = 3;          // Q' / dO / lse2 / delta ring
 constexpr int kOffK = 0, kOffV = kKTile, kOffQ = 2 * kKTile, kOffDO = kOffQ + kQStages * kQTile,
-              kOffPT = kOffDO + kQStages * kQTile, kOffDST = kOffPT + kPTile, kOffVec = kOffDST + kPTile,
+              kOffDST = kOffDO + kQStages * kQTile, kOffVec = kOffDST + 2 * kPTile,  // dS^T[2]
               kOffDQ = kOffVec + kQStages * 512,
               kDQTile = kQStep * 128 * 4,                    // dQ staging [64 q][128 d] fp32
               kOffBar = kOffDQ + kDQTile, kBwdSmem = kOffBar + 256 + 1024;
@@ -80,7 +80,7 @@ __device__ __forceinline__ uint32_t bt_smid() {
 
 constexpr int kMaxRanges = 12;  // visible query-step ranges kept per key tile (more: the StepWalk path)
 struct BwdBars {
-  uint64_t kv_full, q_full[kQStages], q_empty[kQStages], s_full, s_read, dq_full[2], dq_free[2], p_ready, mma_done;
+  uint64_t kv_full, q_full[kQStages], q_empty[kQStages], s_full, s_read, dq_full, dq_free, p_ready[2], mma_done[2];
   uint32_t tmem_base;
   int32_t n_ranges;              // -1: more than kMaxRanges, walk the span table instead
   int32_t rng[kMaxRanges][2];    // [first, end) query steps, increasing, disjoint
@@ -242,14 +242,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::mbar_init(bar(bars->q_full[i]), 1);
       ptx::mbar_init(bar(bars->q_empty[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(bar(bars->dq_full[i]), 1);
-      ptx::mbar_init(bar(bars->dq_free[i]), 4);
-    }
+    ptx::mbar_init(bar(bars->dq_full), 1);
+    ptx::mbar_init(bar(bars->dq_free), 4);
     ptx::mbar_init(bar(bars->s_full), 1);
     ptx::mbar_init(bar(bars->s_read), kCompWarps);
-    ptx::mbar_init(bar(bars->p_ready), kCompWarps);
-    ptx::mbar_init(bar(bars->mma_done), 1);
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(bar(bars->p_ready[i]), kCompWarps);
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(bar(bars->mma_done[i]), 1);
     ptx::fence_mbar_init();
   }
   if (warp == kWarpProd) ptx::tmem_alloc<512>(ptx::smem_u32(&bars->tmem_base));
@@ -269,7 +267,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // TMEM: S^T [0, 64), dP^T [64, 128) (one step at a time: the next step's are computed once these are in
   // registers), dQ^T of step i in [128 + 64 (i & 1), +64) (drained while later steps run), dV [256, 384),
   // dK [384, 512)
-  constexpr uint32_t kS = 0, kDP = 64, kDQ = 128, kDV = 256, kDK = 384;
+  constexpr uint32_t kS = 0, kDP = 64, kDQ = 128, kPT = 192, kDV = 256, kDK = 384;
   const uint64_t pol = ptx::l2_policy_evict_last();
   const int64_t vrow = ((int64_t)b * H + h) * n_pad;  // lse2 / delta row of (b, h)
 
@@ -288,13 +286,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::mbar_wait(bar(bars->q_empty[bi]), (u & 1) ^ 1);
         BT(i, 10);
         const uint32_t qb = base + kOffQ + bi * kQTile, ob = base + kOffDO + bi * kQTile;
-#ifdef DZ_BWD_NO_QLOAD
-        if (i >= kQStages) {
-          ptx::mbar_arrive(bar(bars->q_full[bi]));
-          ++i;
-          continue;
-        }
-#endif
         ptx::mbar_arrive_expect_tx(bar(bars->q_full[bi]), 2 * kQTile + 2 * kQStep * 4);
         for (int x = 0; x < 2; ++x) {
           ptx::tma_load_4d(qb + x * kQBox, &tm_q, bar(bars->q_full[bi]), x * 64, h, qs * kQStep, b, pol);
@@ -322,8 +313,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     auto koff = [](int kk, uint32_t box) { return (uint64_t)(((kk / 4) * box + (kk % 4) * 32) >> 4); };
     auto moff = [](int kk) { return (uint64_t)((kk * 16 * 128) >> 4); };
     const uint64_t dK = desc_k(base + kOffK, 0, kKBox), dV = desc_k(base + kOffV, 0, kKBox),
-                   dPT = desc_k(base + kOffPT, 0, kPTile), dST = desc_k(base + kOffDST, 0, kPTile),
-                   dKm = desc_mn(base + kOffK, 0, kKBox), dSTm = desc_mn(base + kOffDST, 0, kPTile);
+                   dKm = desc_mn(base + kOffK, 0, kKBox);
     ptx::mbar_wait(bar(bars->kv_full), 0);
     auto issue_sdp = [&](uint32_t i) {
       const uint32_t bi = i % kQStages, u = i / kQStages;
@@ -350,27 +340,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     int qn = qs < n_qsteps ? steps.next(st, qs, n_qsteps) : n_qsteps;
     if (qs < n_qsteps) issue_sdp(0);
     for (uint32_t i = 0; qs < n_qsteps; ++i) {
-      const uint32_t bi = i & 1, u = i >> 1, qi = i % kQStages;
+      const uint32_t bi = i & 1, qi = i % kQStages;
       if (qn < n_qsteps) issue_sdp(i + 1);  // (waits until step i's S^T / dP^T have been read)
       const int qnn = qn < n_qsteps ? steps.next(st, qn, n_qsteps) : n_qsteps;
       const uint64_t dQm = desc_mn(base + kOffQ + qi * kQTile, 0, kQBox), dOm = desc_mn(base + kOffDO + qi * kQTile, 0, kQBox);
-      ptx::mbar_wait(bar(bars->p_ready), i & 1);  // P^T and dS^T of step i are in shared memory
+      const uint64_t dST = desc_k(base + kOffDST + bi * kPTile, 0, kPTile), dSTm = desc_mn(base + kOffDST + bi * kPTile, 0, kPTile);
+      // P^T (TMEM) and dS^T (shared memory) of step i are written.  One barrier per buffer: the
+      // softmax-gradient warps may arrive for step i + 1 before this wait (they wait only for step i - 1's
+      // MMAs), never for step i + 2 (that needs step i's MMAs)
+      ptx::mbar_wait(bar(bars->p_ready[bi]), (i >> 1) & 1);
       if (lane == 0) BT(i, 12);
-      if (i >= 2) ptx::mbar_wait(bar(bars->dq_free[bi]), (u - 1) & 1);  // dQ^T(i - 2) drained
-      if (lane == 0) BT(i, 2);
-      #ifndef DZ_BWD_NO_IFENCE
       ptx::tc_fence_after();
-#endif
+      // dV += P^T dO with A = P^T from TMEM (lane = key, 16-bit pairs along the queries), dK += dS^T Q'
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        ptx::mma_ss_warp(tmem + kDV, dPT + koff(kk, kPTile), dOm + moff(kk), iDV, (i > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_ts_warp(tmem + kDV, tmem + kPT + bi * 32 + kk * 8, dOm + moff(kk), iDV, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
         ptx::mma_ss_warp(tmem + kDK, dST + koff(kk, kPTile), dQm + moff(kk), iDK, (i > 0 || kk > 0) ? 1u : 0u);
+      if (i >= 1) {
+        ptx::mbar_wait(bar(bars->dq_free), (i - 1) & 1);  // dQ^T(i - 1) has left TMEM
+        ptx::tc_fence_after();
+      }
+      if (lane == 0) BT(i, 2);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) ptx::mma_ss_warp(tmem + kDQ + bi * 64, dKm + moff(kk), dSTm + moff(kk), iDQ, kk > 0);
-      ptx::tc_commit_warp(bar(bars->mma_done));
-      ptx::tc_commit_warp(bar(bars->dq_full[bi]));
+      for (int kk = 0; kk < 8; ++kk) ptx::mma_ss_warp(tmem + kDQ, dKm + moff(kk), dSTm + moff(kk), iDQ, kk > 0);
+      ptx::tc_commit_warp(bar(bars->mma_done[bi]));
+      ptx::tc_commit_warp(bar(bars->dq_full));
       ptx::tc_commit_warp(bar(bars->q_empty[qi]));
       if (lane == 0) BT(i, 17);
       qs = qn;
@@ -379,11 +375,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     __syncwarp();
   } else if (warp >= kWarpDrain) {
     // ---------------------------------------------------------------- dQ drain --
-    // dQ^T of step i (thread = d row r, all 64 queries) leaves TMEM once its MMAs complete (dq_full,
-    // one barrier per TMEM buffer, so a drain can never fall a phase behind): transposed into the
-    // staging tile [64 q][128 d] fp32 (thread r writes column r: conflict-free) once the previous
-    // reduce has read it, then one TMA bulk reduce-add into dQ'[b][q0 .. q0 + 63][h][:] (rows past n
-    // clipped) while the next steps run.
+    // dQ^T of step i (thread = d row r, all 64 queries) leaves TMEM once its MMAs complete (dq_full; the
+    // next dQ^T MMAs wait for dq_free, so a drain can never fall a phase behind) and TMEM is released at
+    // once; then the values go transposed into the staging tile [64 q][128 d] fp32 (thread r writes
+    // column r: conflict-free) once the previous reduce has read it, and one TMA bulk reduce-add adds
+    // the tile into dQ'[b][q0 .. q0 + 63][h][:] (rows past n clipped) while the next steps run.
     const int quad = warp % 4;
     const int r = quad * 32 + lane;
     const uint32_t lb = (uint32_t)(quad * 32) << 16;
@@ -392,31 +388,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     Steps steps(bars, st, k0, n);
     uint32_t i = 0;
     for (int qs = steps.first(st, n_qsteps); qs < n_qsteps; qs = steps.next(st, qs, n_qsteps), ++i) {
-      const uint32_t bi = i & 1, u = i >> 1;
-      ptx::mbar_wait(bar(bars->dq_full[bi]), u & 1);
+      ptx::mbar_wait(bar(bars->dq_full), i & 1);
       ptx::tc_fence_after();
-      if (leader) ptx::bulk_wait_read_all();  // the previous reduce has read the staging tile
+      uint32_t qa[32], qb[32];
+      ptx::tmem_ld32(tmem + lb + kDQ, qa);
+      ptx::tmem_ld32(tmem + lb + kDQ + 32, qb);
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(bar(bars->dq_free));  // TMEM may take dQ^T(i + 1)
+      if (leader) ptx::bulk_wait_read_all();                // the previous reduce has read the staging tile
       ptx::named_bar_sync(1, 128);
       if (leader) BT(i, 8);
-#ifndef DZ_BWD_NO_DRAIN
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t qr[32];
-        ptx::tmem_ld32(tmem + lb + kDQ + bi * 64 + half * 32, qr);
-        ptx::tmem_wait_ld();
+      for (int j = 0; j < 32; ++j)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + (j * 128 + r) * 4), "r"(qa[j]) : "memory");
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((half * 32 + j) * 128 + r) * 4), "r"(qr[j]) : "memory");
-      }
-#endif
-      ptx::tc_fence_before();
+      for (int j = 0; j < 32; ++j)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + ((32 + j) * 128 + r) * 4), "r"(qb[j]) : "memory");
       ptx::fence_proxy_async_smem();
       ptx::named_bar_sync(1, 128);
-      if (lane == 0) ptx::mbar_arrive(bar(bars->dq_free[bi]));  // the TMEM buffer may take dQ^T(i + 2)
       if (leader) {
-#ifndef DZ_BWD_NO_REDUCE
         ptx::tma_reduce_add_4d(&tm_dq, sb, 0, h, qs * kQStep, b);
-#endif
         ptx::bulk_commit_group();
         BT(i, 7);
       }
@@ -466,9 +459,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (threadIdx.x == 0) BT(i, 4);
       const float4* lv = reinterpret_cast<const float4*>(vec + qi * 128 + hq * kQW);  // lse2 [64] | delta [64]
       uint32_t pk[kQW / 2], dk[kQW / 2];
-#ifdef DZ_BWD_NO_MATH
-      for (int j = 0; j < kQW / 2; ++j) pk[j] = dk[j] = sr[j] ^ dr[j] ^ vm;
-#else
       // pairs of queries in packed fp32x2 arithmetic, 2^x on MUFU (moving 1-4 pairs in 8 to the FMA-pipe
       // polynomial measured slower: the warps are bound by their instruction count, not by MUFU)
 #pragma unroll
@@ -497,23 +487,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dk[j] = *reinterpret_cast<uint32_t*>(&hh);
         }
       }
-#endif
       if (threadIdx.x == 0) BT(i, 5);
-      if (i >= 1) {  // the previous step's MMAs have read P^T / dS^T
-        ptx::mbar_wait(bar(bars->mma_done), (i - 1) & 1);
+      const uint32_t pb = i & 1;  // P^T / dS^T buffer: free once the MMAs of step i - 2 are done
+      if (i >= 2) {
+        ptx::mbar_wait(bar(bars->mma_done[pb]), ((i >> 1) - 1) & 1);
         ptx::tc_fence_after();
       }
-#ifndef DZ_BWD_NO_MATH
+      // P^T into TMEM (A of the dV MMA: 16-bit pairs, query 2c in the low half of column c), dS^T into
+      // shared memory (A of dK, K-major, and B of dQ^T, MN-major; SW128 rows of 64 queries)
+      if constexpr (kQW == 32)
+        ptx::tmem_st16(tmem + lb + kPT + pb * 32 + hq * (kQW / 2), *reinterpret_cast<uint32_t(*)[16]>(pk));
+      else
+        ptx::tmem_st8(tmem + lb + kPT + pb * 32 + hq * (kQW / 2), *reinterpret_cast<uint32_t(*)[8]>(pk));
 #pragma unroll
-      for (int j = 0; j < kQW / 8; ++j) {  // row r of the [128][64] tiles: this warp's chunks of 8 queries, SW128
+      for (int j = 0; j < kQW / 8; ++j) {  // row r of the [128][64] tile: this warp's chunks of 8 queries, SW128
         const uint32_t o = r * 128 + (((hq * (kQW / 8) + j) ^ (r & 7)) << 4);
-        ptx::st_shared_v4(base + kOffPT + o, pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        ptx::st_shared_v4(base + kOffDST + o, dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
+        ptx::st_shared_v4(base + kOffDST + pb * kPTile + o, dk[4 * j], dk[4 * j + 1], dk[4 * j + 2], dk[4 * j + 3]);
       }
-#endif
+      ptx::tmem_wait_st();
       ptx::fence_proxy_async_smem();  // generic stores -> the tensor core's reads
+      ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar(bars->p_ready));
+      if (lane == 0) ptx::mbar_arrive(bar(bars->p_ready[pb]));
       if (threadIdx.x == 0) BT(i, 6);
       // the next step and its visibility mask (parameter-space loads) while the MMAs run
       const int qs_next = steps.next(st, qs, n_qsteps);
@@ -522,8 +517,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       qs = qs_next;
       vm = vm_next;
     }
-    if (i >= 1) {  // the final dV / dK
-      ptx::mbar_wait(bar(bars->mma_done), (i - 1) & 1);
+    if (i >= 1) {  // the final dV / dK (the pipe completes the MMAs of step i - 1 last)
+      ptx::mbar_wait(bar(bars->mma_done[(i - 1) & 1]), ((i - 1) >> 1) & 1);
       ptx::tc_fence_after();
     }
 #ifdef DZ_BWD_TRACE
@@ -799,6 +794,7 @@ extern "C" __attribute__((visibility("default"))) int dz_debug_bwd_trace(int cta
     return (int)cudaMemcpyToSymbol(dz::g_bwd_trace_cta, &cta, sizeof(int));
   }
   if (cta == -2) return (int)cudaMemcpyFromSymbol(host, dz::g_bwd_cta, sizeof(uint32_t) * 4096 * 4);
+  if (cta == -3) return (int)cudaMemcpyFromSymbol(host, dz::ptx::g_dz_watchdog, sizeof(uint32_t) * 8);
   return (int)cudaMemcpyFromSymbol(host, dz::g_bwd_trace, sizeof(uint32_t) * 128 * 24);
 }
 #endif
