@@ -323,9 +323,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (lane == 0) BT(i, 11);
       if (i >= 1) ptx::mbar_wait(bar(bars->s_read), (i - 1) & 1);  // S^T / dP^T of step i - 1 are in registers
       if (lane == 0) BT(i, 1);
-      #ifndef DZ_BWD_NO_IFENCE
       ptx::tc_fence_after();
-#endif
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) ptx::mma_ss_warp(tmem + kS, dK + koff(kk, kKBox), dQ + koff(kk, kQBox), iS, kk > 0);
 #pragma unroll
