@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
         ptx::mma_ss_warp(tmem + kDK, dST + koff(kk, kPTile), dQm + moff(kk), iDK, (i > 0 || kk > 0) ? 1u : 0u);
+      ptx::tc_commit_warp(bar(bars->q_empty[qi]));  // the last reads of this Q' / dO stage (dQ^T does not use it)
       if (i >= 1) {
         ptx::mbar_wait(bar(bars->dq_free), (i - 1) & 1);  // dQ^T(i - 1) has left TMEM
         ptx::tc_fence_after();
@@ -365,7 +366,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int kk = 0; kk < 8; ++kk) ptx::mma_ss_warp(tmem + kDQ, dKm + moff(kk), dSTm + moff(kk), iDQ, kk > 0);
       ptx::tc_commit_warp(bar(bars->mma_done[bi]));
       ptx::tc_commit_warp(bar(bars->dq_full));
-      ptx::tc_commit_warp(bar(bars->q_empty[qi]));
       if (lane == 0) BT(i, 17);
       qs = qn;
       qn = qnn;
