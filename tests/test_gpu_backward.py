@@ -17,10 +17,10 @@ TOL_REL = 5e-3
 TOL_ABS = 2e-2
 
 
-def _case(M, n, heads, seed=0):
+def _case(M, n, heads, seed=0, spans=None):
     import paper_2602_15922_b200 as dz
     w = synth.scaled(synth.workload("C1"), heads=heads, cached_chunks=0)
-    spans = synth.teacher_forcing_spans(M, n)
+    spans = synth.teacher_forcing_spans(M, n) if spans is None else spans
     sl = [(s.chunk, s.kind, s.n_tokens) for s in spans]
     q, k, v, pos = synth.span_inputs(w, spans)
     ntot = q.shape[0]
@@ -76,3 +76,18 @@ def test_backward_deterministic_dv_dk():
     _, _, _, g1, _ = _case(2, 96, 4)
     _, _, _, g2, _ = _case(2, 96, 4)
     assert torch.equal(g1[2], g2[2])
+
+
+def test_backward_many_visible_ranges():
+    # 26 clean spans of 64 tokens in interleaved chunk order 25, 0, 24, 1, ..., 13, 12: a key of chunk c
+    # sees the spans of chunks >= c (every other step), so key tiles near the middle have more separate
+    # visible step ranges than the kernel keeps in shared memory (12) and take the span-walk path
+    order = [c for pair in zip(range(25, 12, -1), range(0, 13)) for c in pair]
+    spans = [synth.Span(c, synth.CLEAN, 64) for c in order]
+    w, sl, (q, k, v, pos, dout, gq, gk), (dq, dk, dv, dgq, dgk), _ = _case(0, 0, 1, spans=spans)
+    want = ob.spans_backward(gq, gk, q, k, v, pos, sl, dout, w.rope_dims)
+    _check("dq", dq[0].cpu().double().numpy(), want["dq"])
+    _check("dk", dk[0].cpu().double().numpy(), want["dk"])
+    _check("dv", dv[0].cpu().double().numpy(), want["dv"])
+    _check("dgq", dgq.cpu().double().numpy(), want["dgq"])
+    _check("dgk", dgk.cpu().double().numpy(), want["dgk"])
