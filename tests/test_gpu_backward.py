@@ -91,3 +91,34 @@ def test_backward_many_visible_ranges():
     _check("dv", dv[0].cpu().double().numpy(), want["dv"])
     _check("dgq", dgq.cpu().double().numpy(), want["dgq"])
     _check("dgk", dgk.cpu().double().numpy(), want["dgk"])
+
+
+def test_backward_batch_two():
+    # two batch elements with their own inputs in one call: per-element gradients, gain gradients summed
+    import paper_2602_15922_b200 as dz
+    heads, M, n = 2, 2, 160
+    w = synth.scaled(synth.workload("C1"), heads=heads, cached_chunks=0)
+    spans = synth.teacher_forcing_spans(M, n)
+    sl = [(s.chunk, s.kind, s.n_tokens) for s in spans]
+    ins = [synth.span_inputs(w, spans, b=b) for b in (0, 1)]
+    ntot = ins[0][0].shape[0]
+    gq, gk = synth.draw_gains(w)
+    g = torch.Generator().manual_seed(99)
+    dout = torch.randn(2, ntot, heads, 128, generator=g).to(torch.bfloat16)
+    dev = torch.device("cuda")
+    cache = dz.ChunkKVCache(2, heads, 128, 0, ntot, w.rope_dims, gq.to(dev), gk.to(dev),
+                            flags=dz.FLAG_WRITE_LSE | dz.FLAG_BACKWARD, device=dev)
+    Q, K, V = (torch.stack([x[i] for x in ins]).to(dev) for i in range(3))
+    P = ins[0][3].to(dev)
+    out = cache.attend_spans(Q, K, V, P, sl)
+    lse = cache.lse(ntot)
+    dq, dk, dv, dgq, dgk = cache.attend_spans_backward(Q, K, V, P, sl, out, lse, dout.to(dev))
+    torch.cuda.synchronize()
+    wants = [ob.spans_backward(gq, gk, q, k, v, pos, sl, dout[b], w.rope_dims)
+             for b, (q, k, v, pos) in enumerate(ins)]
+    for b in (0, 1):
+        _check(f"dq b{b}", dq[b].cpu().double().numpy(), wants[b]["dq"])
+        _check(f"dk b{b}", dk[b].cpu().double().numpy(), wants[b]["dk"])
+        _check(f"dv b{b}", dv[b].cpu().double().numpy(), wants[b]["dv"])
+    _check("dgq", dgq.cpu().double().numpy(), wants[0]["dgq"] + wants[1]["dgq"])
+    _check("dgk", dgk.cpu().double().numpy(), wants[0]["dgk"] + wants[1]["dgk"])
