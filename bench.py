@@ -329,15 +329,19 @@ class Timer:
             sampler.__enter__()
         for i in range(steps):
             self.flush()
+            torch.cuda.nvtx.range_push(f"dz step {i}")  # NVTX ranges: visible to nsys / ncu --nvtx
             ev[i][0].record()
             n0 = dz.kernel_launches()
             step()
             launches += dz.kernel_launches() - n0
             ev[i][1].record()
+            torch.cuda.nvtx.range_pop()
             if profiled:
                 cache.profile_enable(True)
                 self.flush()
+                torch.cuda.nvtx.range_push(f"dz profiled step {i}")
                 step()
+                torch.cuda.nvtx.range_pop()
                 p = cache.profile_last()         # host-syncs on the library's events (last call)
                 for k in prof:
                     prof[k].append(p[k])
