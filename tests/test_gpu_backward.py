@@ -47,7 +47,7 @@ def _check(name, got, want):
     assert rel <= TOL_REL and max_abs <= TOL_ABS * scale, (name, max_abs, rel)
 
 
-@pytest.mark.parametrize("M,n,heads", [(2, 96, 4), (3, 200, 2)])
+@pytest.mark.parametrize("M,n,heads", [(2, 96, 4), (3, 200, 2), (2, 37, 3), (1, 1, 2)])
 def test_backward_small_all_heads(M, n, heads):
     w, sl, (q, k, v, pos, dout, gq, gk), (dq, dk, dv, dgq, dgk), _ = _case(M, n, heads)
     want = ob.spans_backward(gq, gk, q, k, v, pos, sl, dout, w.rope_dims)
