@@ -5,20 +5,20 @@
 // Three kernels, run after the forward prologue (K1) has recomputed Q' (pre-scaled by
 // scale * log2e, fp16) and K' (fp16):
 //   B1 delta_kernel     delta_s = <dO_s, O_s> and lse2_s = lse_s * log2(e), per (b, h, query)
-//   B2 attn_bwd_kernel  one CTA per (b, h, 128-key tile), looping over the query tiles that see any of
-//                       its keys (SKIP tiles never loaded); five tcgen05 MMAs per query tile, all
-//                       operands in shared memory (SW128, 64-column TMA boxes), accumulators in TMEM:
-//                         S^T = K' Q'^T          (M = keys, N = queries, K = D)      cols [0,128)
-//                         dP^T = V dO^T          (M = keys, N = queries, K = D)      cols [128,256)
-//                         -- 4 warps (thread = key row): P^T = 2^(S^T - lse2), masked (Fig. 10);
-//                            dS^T = P^T (dP^T - delta), written bf16 / fp16 to shared memory --
-//                         dV += P^T dO           (B = dO read MN-major)              cols [256,384)
-//                         dK += dS^T Q'          (B = Q' read MN-major)              cols [384,512)
-//                         dQ^T = K'^T dS^T       (A = K', B = dS^T read MN-major)    cols [0,128)
-//                       dQ^T leaves TMEM (thread = d row) as fp32 atomics into dQ' (coalesced over d);
-//                       dV (bf16) and dK' (fp32) are written once per key tile.
+//   B2 attn_bwd_kernel  one CTA per (b, h, 128-key tile), looping over the 64-query steps that see any
+//                       of its keys (SKIP steps never loaded); five tcgen05 MMAs per step, accumulators
+//                       in TMEM (DESIGN.md §7 "Backward"):
+//                         S^T = K' Q'^T          (M = keys, N = queries, K = D)           cols [0,64)
+//                         dP^T = V dO^T          (M = keys, N = queries, K = D)           cols [64,128)
+//                         -- 8 warps (thread = key row, 32 queries each): P^T = 2^(S^T - lse2) into TMEM
+//                            (cols [192,256), two buffers), dS^T = P^T (dP^T - delta) into shared memory
+//                            (two buffers), masked (Fig. 10) --
+//                         dV += P^T dO           (A = P^T from TMEM, B = dO MN-major)     cols [256,384)
+//                         dK += dS^T Q'          (B = Q' read MN-major)                   cols [384,512)
+//                         dQ^T = K'^T dS^T       (A = K', B = dS^T, both MN-major)        cols [128,192)
+//                       4 drain warps move dQ^T (thread = d row) to a staging tile, one TMA reduce-add per
+//                       step into the fp32 dQ' workspace; dV (bf16) and dK' (fp32) are written once per CTA.
 //   B3 prologue_bwd_kernel  dx = RMSNorm/RoPE backward of dx' for q and k, and the gain gradients.
-// First version: correct by construction, not pipelined (each stage waits for the previous one).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
