@@ -773,7 +773,11 @@ def main():
                                 "step events / steps (no per-kernel events)"),
                      "k2_ms": spread(attn_ms),
                      "peak_source": peak_k2_src,
-                     "frac_vs_sustained": achieved / peak_sus, "flop_per_launch": flop_launch},
+                     "frac_vs_sustained": achieved / peak_sus, "flop_per_launch": flop_launch,
+                     # per-clock tensor efficiency: 148 SMs x 8192 dense bf16 FLOP/clk (tools/mma_bench.cu
+                     # measures 8110-8170 for N >= 128) at the median SM clock sampled in the timed region
+                     "frac_per_clock": (achieved * 1e12 / (148 * 8192 * clocks["sm_mhz"] * 1e6)
+                                        if clocks and clocks.get("sm_mhz") else None)},
         "kernels": {"prologue_ms": spread(prof["prologue"]) if profiled else None,
                     "prologue_gbs": pro_bytes / (pro_med * 1e-3) / 1e9 if profiled else None,
                     "append_ms": spread(prof["append"]) if profiled else None,
