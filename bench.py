@@ -115,16 +115,15 @@ def peaks():
 
 
 def lib_sha():
-    import paper_2602_15922_b200 as dz
-    h = hashlib.sha256()
-    with open(dz.LIB_PATH, "rb") as f:
-        h.update(f.read())
-    return h.hexdigest()[:16]
+    """Build identity: hash of the library's sources and build flags (paper_2602_15922_b200/build.py
+    source_sha; the linked .so itself is not byte-reproducible)."""
+    from paper_2602_15922_b200 import build as b
+    return b.source_sha()
 
 
 def stamped_traffic(workload: str):
     """DRAM bytes per K2 launch from the committed ncu capture, only if it was taken on this very
-    library build (sha of libdz.so stamped into the file) and workload; else None."""
+    library build (the sources' hash stamped into the file) and workload; else None."""
     tp = os.path.join(ROOT, "profiles", "ncu_attention_traffic.json")
     if not os.path.exists(tp):
         return None, "no capture"

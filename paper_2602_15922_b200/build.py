@@ -40,6 +40,19 @@ def deps():
         os.path.join(ROOT, "include", "dz.h")]
 
 
+def source_sha() -> str:
+    """Identity of a build: sha256 (16 hex) over every source the library compiles from and this build
+    script (its flags).  The linked libdz.so is not byte-reproducible (the device-link step embeds
+    nvcc's temporary file names), the objects and their SASS are."""
+    import hashlib
+    h = hashlib.sha256()
+    for p in sorted(deps()) + [os.path.abspath(__file__)]:
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
