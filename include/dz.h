@@ -232,7 +232,10 @@ DZ_API dz_status dz_append_attend(dz_ctx* ctx, const void* k_gt, const void* v_g
  * dq_gain, dk_gain = dL/dg (fp32 [heads*head_dim], overwritten), through the RMSNorm, the gains, the
  * 3D RoPE and the Fig. 10-masked attention.  Key tiles no query sees are never loaded against those
  * queries.  Needs DZ_FLAG_BACKWARD, one GPU, head_dim 128, the bf16 path (DZ_ESHAPE) and an empty
- * cache (DZ_ESTATE).  Tolerance against the fp64 oracle: DESIGN.md §4. */
+ * cache (DZ_ESTATE).  Tolerance against the fp64 oracle: DESIGN.md §4.  dv_raw and dk_raw are bitwise
+ * repeatable (one CTA per key tile); dq_raw and the gain gradients sum per-tile contributions with fp32
+ * reduce-adds in arrival order, so they repeat to fp32 rounding, not bitwise.  The fp32 dq accumulator
+ * lives in the context's workspace (sized at dz_create from max_chunk_tokens). */
 DZ_API dz_status dz_attend_spans_backward(dz_ctx* ctx, const void* q_raw, const void* k_raw, const void* v_raw,
                                           const int32_t* pos_thw, const dz_span* spans, int32_t n_spans,
                                           const void* out, const float* lse, const void* dout, void* dq_raw,
