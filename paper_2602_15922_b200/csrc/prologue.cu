@@ -395,6 +395,130 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
   }
 }
 
+// The fused append + attend prologue (one GPU, bf16) with two tensor slots per item instead of three:
+// an item of the attend set (j0) carries (q, k), an item of the appended set (j1) carries (k, v), so
+// slot 0 is q or k and slot 1 is k or v (v: a copy).  Same arithmetic and order as
+// prologue_loop_kernel; two thirds of its load registers (no spills at two CTAs per SM).
+template <int D>
+__global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_dual2_kernel(const PrologueArgs a) {
+  constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
+  ptx::pdl_launch_dependents();
+  const int tid = threadIdx.x, g = tid / G, li = tid % G;
+  const int H = a.H, items0 = a.B * a.n, items = items0 + a.B * a.j1.n;
+  auto locate = [&](int item, int& b, int& t) -> bool {
+    const bool s1 = item >= items0;
+    const int it = s1 ? item - items0 : item, nn = s1 ? a.j1.n : a.n;
+    b = it / nn;
+    t = it - b * nn;
+    return s1;
+  };
+  const int64_t tokD = (int64_t)H * D;
+  int64_t ooff[kPer];  // one GPU: every tensor's row of head h sits at h * D in the token's block
+  bool hv[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int h = g + kRows * i;
+    hv[i] = h < H;
+    ooff[i] = (int64_t)h * D + li * 8;
+  }
+  auto load = [&](int item, uint4 (&v)[2][kPer]) {
+    int b, t;
+    const bool s1 = locate(item, b, t);
+    const int64_t src = (int64_t)b * (s1 ? a.j1.x_bstride : a.x_bstride) + (int64_t)t * tokD + g * D + li * 8;
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+      const void* xw = s1 ? a.j1.x[sl + 1] : a.x[sl];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i)
+        if (hv[i])
+          v[sl][i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(xw) + src + (int64_t)kRows * i * D));
+    }
+  };
+  int ax[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) ax[e] = a.axis[li * 4 + e];
+  auto positions = [&](int item, int (&p)[4]) {
+    if (item >= items) return;
+    int b, t;
+    const int32_t* pos = locate(item, b, t) ? a.j1.pos : a.pos;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = __ldg(pos + 3 * t + ax[e]);
+  };
+  auto angles = [&](const int (&p)[4], float2 (&c)[4]) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      c[e] = (unsigned)p[e] < (unsigned)a.rope_len ? __ldg(a.rope_tab + (size_t)p[e] * (D / 2) + li * 4 + e)
+                                                   : rope_cs(p[e], a.omega[li * 4 + e]);
+  };
+  ptx::pdl_wait();  // before the first read of an input (its producer may be the previous kernel)
+  uint4 v[2][kPer], vn[2][kPer];
+  float2 csr[4], csn[4];
+  int pn[4] = {0, 0, 0, 0};
+  int item = blockIdx.x;
+  if (item < items) {
+    load(item, v);
+    positions(item, pn);
+    angles(pn, csr);
+    positions(item + gridDim.x, pn);
+  }
+  for (; item < items; item += gridDim.x) {
+    const int nxt = item + gridDim.x;
+    if (nxt < items) {  // in flight while this token is processed
+      load(nxt, vn);
+      angles(pn, csn);
+      positions(nxt + gridDim.x, pn);
+    }
+    int b, t;
+    const bool s1 = locate(item, b, t);
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+      const int w = s1 ? sl + 1 : sl;  // the tensor in this slot: 0 q, 1 k, 2 v (uniform per item)
+      const OutSlot& o = s1 ? a.j1.y[w] : a.y[w];
+      const int64_t base = (int64_t)b * o.bstride + (int64_t)t * o.tstride;
+      if (w == 2) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i)
+          if (hv[i]) reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(o.base) + base + ooff[i])[0] = v[sl][i];
+        continue;
+      }
+      float ss[kPer];
+      float f[kPer][8];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        bf16x8_to_f32(v[sl][i], f[i]);
+        ss[i] = rr::chunk_ss(f[i]);
+      }
+#pragma unroll
+      for (int m = G / 4; m >= 1; m >>= 1)
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) ss[i] = __fadd_rn(ss[i], __shfl_xor_sync(0xffffffffu, ss[i], m));
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) ss[i] = __fadd_rn(ss[i], __shfl_xor_sync(0xffffffffu, ss[i], G / 2));
+      const float sc = w == 0 ? a.q_scale : 1.f;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        if (!hv[i]) continue;
+        const int h = g + kRows * i;
+        const float inv = rr::inv_rms(ss[i], D, a.eps);
+        const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
+        const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
+        reinterpret_cast<uint4*>(static_cast<__half*>(o.base) + base + ooff[i])[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl)
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) v[sl][i] = vn[sl][i];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) csr[e] = csn[e];
+  }
+}
+
 template <int D>
 __global__ void rope_table_kernel(float2* __restrict__ tab, int32_t len, const PrologueArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -440,6 +564,19 @@ cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
   }
   if (a.j1.n > 0) {  // two token sets in one launch (one GPU, H within one pass of the token loop)
     if (a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
+    static const bool dual3 = getenv("DZ_PRO_DUAL3") != nullptr;  // A/B switch (diagnostics)
+    if (!dual3 && a.x[0] && a.x[1] && !a.x[2] && !a.j1.x[0] && a.j1.x[1] && a.j1.x[2]) {
+      static int grid_cap = 0;
+      if (grid_cap == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_dual2_kernel<D>, 256, 0);
+        grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
+      }
+      const int items = a.B * (a.n + a.j1.n);
+      return launch_pdl(prologue_dual2_kernel<D>, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s, a);
+    }
     return launch_loop<D, 7, true>(a, s);
   }
   static const bool force_ring = getenv("DZ_PRO_RING") != nullptr;  // diagnostics: the TMA-ring kernel
