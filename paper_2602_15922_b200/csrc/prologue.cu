@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
 // an item of the attend set (j0) carries (q, k), an item of the appended set (j1) carries (k, v), so
 // slot 0 is q or k and slot 1 is k or v (v: a copy).  Same arithmetic and order as
 // prologue_loop_kernel; two thirds of its load registers (no spills at two CTAs per SM).
-template <int D>
+template <int D, bool F8 = false>
 __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_dual2_kernel(const PrologueArgs a) {
   constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
   ptx::pdl_launch_dependents();
@@ -503,11 +503,21 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_dual2_kernel(c
         const float4* gp = reinterpret_cast<const float4*>(a.gain[w] + h * D + li * 8);
         const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1);
         const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-        uint32_t pk[4];
+        if constexpr (F8) {  // E4M3 rows of D bytes: this thread's 8 elements are 8 bytes
+          uint16_t q8[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
-        reinterpret_cast<uint4*>(static_cast<__half*>(o.base) + base + ooff[i])[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          for (int e = 0; e < 4; ++e)
+            q8[e] = rr::rot_pair_e4m3(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc,
+                                      a.f8_mul[w]);
+          *reinterpret_cast<uint2*>(static_cast<uint8_t*>(o.base) + base + ooff[i]) =
+              make_uint2((uint32_t)q8[0] | ((uint32_t)q8[1] << 16), (uint32_t)q8[2] | ((uint32_t)q8[3] << 16));
+        } else {
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            pk[e] = rr::rot_pair(f[i][2 * e], f[i][2 * e + 1], inv, gg[2 * e], gg[2 * e + 1], csr[e], sc);
+          reinterpret_cast<uint4*>(static_cast<__half*>(o.base) + base + ooff[i])[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
       }
     }
 #pragma unroll
@@ -544,11 +554,33 @@ cudaError_t launch_loop(const PrologueArgs& a, cudaStream_t s) {
                     dim3(256), 0, s, a);
 }
 
+// the two-slot fused prologue when the sets are (q, k) and (k, v); false: use the three-slot loop
+template <int D, bool F8>
+bool launch_dual2(const PrologueArgs& a, cudaStream_t s, cudaError_t& err) {
+  static const bool dual3 = getenv("DZ_PRO_DUAL3") != nullptr;  // A/B switch (diagnostics)
+  if (dual3 || !(a.x[0] && a.x[1] && !a.x[2] && !a.j1.x[0] && a.j1.x[1] && a.j1.x[2])) return false;
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_dual2_kernel<D, F8>, 256, 0);
+    grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
+  }
+  const int items = a.B * (a.n + a.j1.n);
+  err = launch_pdl(prologue_dual2_kernel<D, F8>, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s, a);
+  return true;
+}
+
 template <int D>
 cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
   if (a.fp8) {  // E4M3 Q'/K' (one GPU, token loop): attend (q, k [, v]), append (k, v), both in one launch
     if (a.peer || a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
-    if (a.j1.n > 0) return launch_loop<D, 7, true, false, true>(a, s);
+    if (a.j1.n > 0) {
+      cudaError_t e;
+      if (launch_dual2<D, true>(a, s, e)) return e;
+      return launch_loop<D, 7, true, false, true>(a, s);
+    }
     const int mask = (a.x[0] ? 1 : 0) | (a.x[1] ? 2 : 0) | (a.x[2] ? 4 : 0);
     switch (mask) {
       case 3: return launch_loop<D, 3, false, false, true>(a, s);
@@ -564,19 +596,8 @@ cudaError_t launch_pro(const PrologueArgs& a, cudaStream_t s) {
   }
   if (a.j1.n > 0) {  // two token sets in one launch (one GPU, H within one pass of the token loop)
     if (a.H > 3 * (256 / (D / 8))) return cudaErrorInvalidValue;
-    static const bool dual3 = getenv("DZ_PRO_DUAL3") != nullptr;  // A/B switch (diagnostics)
-    if (!dual3 && a.x[0] && a.x[1] && !a.x[2] && !a.j1.x[0] && a.j1.x[1] && a.j1.x[2]) {
-      static int grid_cap = 0;
-      if (grid_cap == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_dual2_kernel<D>, 256, 0);
-        grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
-      }
-      const int items = a.B * (a.n + a.j1.n);
-      return launch_pdl(prologue_dual2_kernel<D>, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s, a);
-    }
+    cudaError_t e;
+    if (launch_dual2<D, false>(a, s, e)) return e;
     return launch_loop<D, 7, true>(a, s);
   }
   static const bool force_ring = getenv("DZ_PRO_RING") != nullptr;  // diagnostics: the TMA-ring kernel
