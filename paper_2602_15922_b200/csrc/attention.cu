@@ -59,7 +59,8 @@ constexpr int kPolyPairs = DZ_POLY;
 constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr int kWarpMma = 11, kWarpTma = 10, kWarpPv = 9, kWarpTmem = 8;
 // setmaxnreg split, 128 * light + 256 * softmax = 384 * 168 (launch): ping-pong 104/200 (measured on
-// C1: 88/208 182.8 us, 104/200 178.0, 120/192 179.7), lock-step 88/208 (its softmax holds more state)
+// C1: 88/208 182.8 us, 104/200 178.0, 120/192 179.7), lock-step 72/216 (its softmax holds more state;
+// C1 forced online: 56/224 244.0 us, 72/216 234.0, 88/208 244.2; light must be 8 mod 16)
 template <bool PP> __host__ __device__ constexpr uint32_t regs_light() { return PP ? 104 : 88; }
 template <bool PP> __host__ __device__ constexpr uint32_t regs_softmax() { return PP ? 200 : 208; }
 

@@ -503,7 +503,7 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   // its rows and keys, not on the unit count (the same bits at every world size, reading A21)
   static const bool rr_forced = getenv("DZ_SCHED_RR") != nullptr;  // diagnostics: whole units round-robin
   const bool streamk = !rr_forced && !(c->cfg.flags & DZ_FLAG_WHOLE_UNITS) && n_groups <= 64 &&
-                       (int64_t)c->B * c->Hl * n_groups * n_steps * dz::kMaxPairs < (1ll << 31);
+                       (int64_t)c->B * c->Hl * n_groups * n_steps * dz::kMaxPairs * dz::kStepWeight < (1ll << 31);
   a.ws = streamk ? reinterpret_cast<float*>(c->base + c->L.ws_off) : nullptr;
   a.ws_cnt = reinterpret_cast<int32_t*>(c->base + c->L.cnt_off);
   if (!c->ws_zeroed) {  // piece counters start at zero; every combine resets its own

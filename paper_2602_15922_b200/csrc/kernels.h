@@ -129,6 +129,9 @@ cudaError_t launch_attention(const AttnArgs& a, cudaStream_t s);
 constexpr int kMaxPairs = 80;  // CTA pairs of the persistent grid (B200: 74)
 int attention_units(int32_t B, int32_t H, int32_t nq);
 constexpr int kTileQ = 256;  // skip / mask decision granularity: query rows of a CTA pair x the keys of a step
+// stream-K balances cost-weighted steps: a step of a full 256-row unit weighs kStepWeight, a step of a
+// half unit (a last query group of <= 128 rows, run as M = 128 pair MMAs) less (attention.cu)
+constexpr int kStepWeight = 8;
 // keys per K2 step: 128 with the fixed softmax base (ping-pong kernel), 256 with the online base
 int attention_step_keys(float m_static);
 // span layouts (several spans): the kernel's step-class table holds at most kMaxStepTiles
