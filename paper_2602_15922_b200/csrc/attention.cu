@@ -61,8 +61,11 @@ constexpr int kWarpMma = 11, kWarpTma = 10, kWarpPv = 9, kWarpTmem = 8;
 // setmaxnreg split, 128 * light + 256 * softmax = 384 * 168 (launch): ping-pong 104/200 (measured on
 // C1: 88/208 182.8 us, 104/200 178.0, 120/192 179.7), lock-step 72/216 (its softmax holds more state;
 // C1 forced online: 56/224 244.0 us, 72/216 234.0, 88/208 244.2; light must be 8 mod 16)
-template <bool PP> __host__ __device__ constexpr uint32_t regs_light() { return PP ? 104 : 88; }
-template <bool PP> __host__ __device__ constexpr uint32_t regs_softmax() { return PP ? 200 : 208; }
+#ifndef DZ_LS_LIGHT
+#define DZ_LS_LIGHT 72
+#endif
+template <bool PP> __host__ __device__ constexpr uint32_t regs_light() { return PP ? 104 : DZ_LS_LIGHT; }
+template <bool PP> __host__ __device__ constexpr uint32_t regs_softmax() { return PP ? 200 : (2016 - 4 * DZ_LS_LIGHT) / 8; }
 
 // Cycle trace of cluster 0's first unit (diagnostics, dz_debug_trace), per CTA
 // rank r at [r * 16 * kTraceSteps]: per step j [8j+0,1] QK wait/issue,
@@ -137,10 +140,26 @@ struct Cfg {
   static_assert(8 * 32 * D <= 32768 || !F8, "O staging");
   static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, 2 * BM, BN / 2);  // f16 x f16, K-major, per half
   static constexpr uint32_t kIdescPV = ptx::idesc_f16(1, 1, 0, 1, 2 * BM, D);   // P (TMEM) x V (MN-major)
+  // half units (M = 128 per pair, 64 rows per CTA): QK as above; PV takes P from shared memory (K-major)
+  static constexpr uint32_t kIdescQKh = ptx::idesc_f16(0, 0, 0, 0, BM, BN / 2);
+  static constexpr uint32_t kIdescPVh = ptx::idesc_f16(1, 1, 0, 1, BM, D);
   static constexpr int kVRowBytes = D;                      // V half row: D/2 bf16
 };
 
 constexpr int kMaxGroups = 64;    // stream-K schedule needs <= 64 query groups (16384 query rows)
+// Half units: with an odd number of 128-row query tiles the last query group holds <= 128 rows; the
+// ping-pong kernel runs it as M = 128 pair MMAs (64 rows per CTA: CTA r takes rows 256g + 64r ..
+// +63) instead of M = 256 with a wholly padded second tile.  The M = 128 accumulator layout
+// (tools/tmem_layout_probe.cu): lanes 0..63 hold the CTA's 64 rows for the columns n < N/2, lanes
+// 64..127 the same rows for n >= N/2, N/2 TMEM columns.  So softmax warp quadrant q sees rows
+// 32 (q & 1) .., keys 64 (q >> 1) .. of a step; P cannot be the TMEM A operand of PV (every lane would
+// need the whole row) and goes to shared memory instead (SS MMA), each warp writing its 32 rows x 64
+// keys -- exactly its own 4 KB epilogue staging slot, in the SW128 K-major layout.  A half-unit step
+// costs about kWHalf / kStepWeight of a full one (measured), the weight stream-K balances with.
+#ifndef DZ_WHALF
+#define DZ_WHALF 14
+#endif
+constexpr int kWHalf = DZ_WHALF;
 
 struct Bars {
   uint64_t q_full, q_empty, s_full[2], s_free[2], p_full[2], p_empty[2], o_full, o_empty;
@@ -274,7 +293,10 @@ struct Sched {
   int rr_end;          // hybrid: units [0, rr_end) are dealt whole, unit u to pair u % P
   int x0;              // ... and stream-K covers the executed steps [x0, W) of the remaining units
   const int32_t* plo;  // range boundaries [P + 1] (shared memory)
+  int half_g;          // the half-unit query group (-1: none)
 };
+// cost weight of one executed step of query group g (the linear step space of the schedule is weighted)
+__device__ __forceinline__ int step_wt(int half_g, int g) { return g == half_g ? kWHalf : kStepWeight; }
 // stream-K range boundary of pair p
 __device__ __forceinline__ int pair_lo(const Sched& sc, int p) { return sc.plo[p]; }
 __device__ __forceinline__ int pair_of(const Sched& sc, int x) {
@@ -295,7 +317,7 @@ __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_g
       sg.h = bh % H;
       sg.b = bh / H;
       sg.k0 = 0;
-      sg.k1 = sg.cnt = gpre[sg.g + 1] - gpre[sg.g];  // the group's executed steps
+      sg.k1 = sg.cnt = (gpre[sg.g + 1] - gpre[sg.g]) / step_wt(sc.half_g, sg.g);  // the group's executed steps
       return true;
     }
     if (sc.lo >= sc.hi) return false;
@@ -303,13 +325,14 @@ __device__ __forceinline__ bool next_seg(Sched& sc, const int32_t* gpre, int n_g
     const int r = sc.lo - bh * sc.wbh;
     int g = 0;
     while (gpre[g + 1] <= r) ++g;
+    const int w = step_wt(sc.half_g, g);
     sg.g = g;
     sg.h = bh % H;
     sg.b = bh / H;
-    sg.cnt = gpre[g + 1] - gpre[g];
-    sg.k0 = r - gpre[g];
-    sg.k1 = min(sg.cnt, sg.k0 + (sc.hi - sc.lo));
-    sc.lo += sg.k1 - sg.k0;
+    sg.cnt = (gpre[g + 1] - gpre[g]) / w;
+    sg.k0 = (r - gpre[g]) / w;  // (range boundaries are step boundaries)
+    sg.k1 = (min(sc.hi - bh * sc.wbh, gpre[g + 1]) - gpre[g] + w - 1) / w;
+    sc.lo += (sg.k1 - sg.k0) * w;
     return true;
   }
   if (sc.u >= n_units) return false;
@@ -369,6 +392,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int n_groups = (n_qtiles + 1) / 2;                 // 2 query tiles per cluster unit
   const int n_units = B * H * n_groups;
   const int nkv = (kv_len + BN - 1) / BN;                  // key steps
+  // the half-unit group (ping-pong kernel, D = 128, odd tile count); debug flag 2 turns half units off
+  const int half_g = (PP && D == 128 && (n_qtiles & 1) && !(dbg & 2)) ? n_groups - 1 : -1;
   const int cid = (int)ptx::cluster_id_x(), ncl = (int)ptx::nclusters_x();
   const bool trace_on = kTrace && g_dz_trace_on != 0 && cid == 0;
   uint32_t* const trace = g_dz_trace + rank * kTraceSteps * 16;
@@ -399,14 +424,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncthreads();
   }
   if (streamk) {
-    if (st.n == 1) {
-      for (int g = threadIdx.x; g <= n_groups; g += kThreads) bars->gpre[g] = g * nkv;
+    if (st.n == 1) {  // (only the last group can be the half group)
+      for (int g = threadIdx.x; g <= n_groups; g += kThreads)
+        bars->gpre[g] = nkv * (g * kStepWeight + (half_g >= 0 && g > half_g ? kWHalf - kStepWeight : 0));
     } else {
       for (int g = threadIdx.x; g <= n_groups; g += kThreads) bars->gpre[g] = 0;
       __syncthreads();
       for (int x = threadIdx.x; x < n_groups * nkv; x += kThreads)
         if (cls_get<BN, kTab>(st, x / nkv, x % nkv, nq, kv_len, nkv) != kSkip)
-          atomicAdd(&bars->gpre[x / nkv + 1], 1);
+          atomicAdd(&bars->gpre[x / nkv + 1], step_wt(half_g, x / nkv));
       __syncthreads();
       if (threadIdx.x == 0)
         for (int g = 1; g <= n_groups; ++g) bars->gpre[g] += bars->gpre[g - 1];
@@ -462,12 +488,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int32_t* plo = bars->plo;
     // linear index of the first executed step of unit u
     auto lin = [&](int u) { return (u / n_groups) * wbh + gpre[u % n_groups]; };
+    // nearest step boundary of the weighted step space (a range must start and end on one)
+    auto snap = [&](int x) {
+      if (x <= x0 || x >= W) return x;  // x0 and W are unit boundaries
+      const int bh = x / wbh, r = x - bh * wbh;
+      int g = 0;
+      while (gpre[g + 1] <= r) ++g;
+      const int w = step_wt(half_g, g);
+      return bh * wbh + gpre[g] + (r - gpre[g] + w / 2) / w * w;
+    };
     for (int p = threadIdx.x; p < ncl; p += kThreads) {
       // whole-unit steps of pairs 0..p: units w*P .. w*P + p of every round-robin wave w
       int rr = 0;
       for (int w0 = 0; w0 < rr_end; w0 += ncl) rr += lin(w0 + p + 1) - lin(w0);
       // pairs 0..p end where their whole-unit steps plus their ranges reach W (p + 1) / P
-      plo[p + 1] = p + 1 == ncl ? W : min(W, max(x0, x0 + W * (p + 1) / ncl - rr));  // (host: W * P < 2^31)
+      plo[p + 1] = p + 1 == ncl ? W : snap(min(W, max(x0, x0 + W * (p + 1) / ncl - rr)));  // (host: W * P < 2^31)
     }
     if (threadIdx.x == 0) plo[0] = x0;
     __syncthreads();
@@ -486,6 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   sched0.rr_end = rr_end;
   sched0.x0 = x0;
   sched0.plo = bars->plo;
+  sched0.half_g = half_g;
   if (streamk) {
     sched0.wbh = gpre[n_groups];
     sched0.W = B * H * sched0.wbh;
@@ -513,11 +549,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         q_phase ^= 1;
         const int qt = 2 * g + (int)rank;
         if (lane == 0) {
-          if (leader) ptx::mbar_arrive_expect_tx(bar(bars->q_full), min(2, n_qtiles - 2 * g) * C::kQTileBytes);
-          if (qt < n_qtiles)  // a tile wholly past nq is not loaded (its rows are never stored)
-            for (int x = 0; x < C::kQBoxes; ++x)
-              ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * C::kBoxElems, h, qt * BM, b,
-                                    pol_q);
+          if (g == half_g) {  // half unit: CTA r's 64 rows start at 256g + 64r (box rows past 64 unused)
+            const int r0 = g * kTileQ + 64 * (int)rank;
+            if (leader) ptx::mbar_arrive_expect_tx(bar(bars->q_full), (g * kTileQ + 64 < nq ? 2 : 1) * C::kQTileBytes);
+            if (r0 < nq)
+              for (int x = 0; x < C::kQBoxes; ++x)
+                ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * C::kBoxElems, h, r0, b, pol_q);
+          } else {
+            if (leader) ptx::mbar_arrive_expect_tx(bar(bars->q_full), min(2, n_qtiles - 2 * g) * C::kQTileBytes);
+            if (qt < n_qtiles)  // a tile wholly past nq is not loaded (its rows are never stored)
+              for (int x = 0; x < C::kQBoxes; ++x)
+                ptx::tma_load_4d_2cta(sQ + x * BM * 128, &tm_q, lbar(bars->q_full), x * C::kBoxElems, h, qt * BM, b,
+                                      pol_q);
+          }
         }
       }
       int j = step_of<BN, kTab>(st, g, sg.k0, nq, kv_len, nkv);
@@ -576,6 +620,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     bool first_seg = true;
     while (next_seg<BN, kTab>(sc, gpre, n_groups, n_units, H, st, nq, kv_len, nkv, sg)) {
       const int g = sg.g;
+      const bool hu = PP && g == half_g;  // half unit: M = 128 MMAs, P from shared memory
+      const uint32_t idq = hu ? C::kIdescQKh : C::kIdescQK;
       int j = step_of<BN, kTab>(st, g, sg.k0, nq, kv_len, nkv);
       for (int k = sg.k0; k < sg.k1; ++k, ++j) {
         if (st.n != 1)
@@ -615,10 +661,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const uint32_t koff = (kk / 4) * (64 * 128) + (kk % 4) * 32;   // K half: 64 rows per box
                 // descriptors: the start address field is addr >> 4 in the low bits, offsets add
                 if constexpr (F8)  // (the idesc's E4M3 format codes are the f16 kind's F16 codes: 0)
-                  ptx::mma_ss_2cta_f8(tmem + kColS + sb * 128, dq0 + (qoff >> 4), dk0 + (koff >> 4), C::kIdescQK,
-                                      kk > 0);
+                  ptx::mma_ss_2cta_f8(tmem + kColS + sb * 128, dq0 + (qoff >> 4), dk0 + (koff >> 4), idq, kk > 0);
                 else
-                  ptx::mma_ss_2cta(tmem + kColS + sb * 128, dq0 + (qoff >> 4), dk0 + (koff >> 4), C::kIdescQK, kk > 0);
+                  ptx::mma_ss_2cta(tmem + kColS + sb * 128, dq0 + (qoff >> 4), dk0 + (koff >> 4), idq, kk > 0);
                 if (tr && j == 9) trace[kTraceSteps * 8 + hh * 8 + kk] = (uint32_t)clock();
               }
               ptx::tc_commit_2cta(bar(bars->s_full[sb]), kBoth);
@@ -650,11 +695,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             const uint32_t va = sKV + v_st * C::kStageBytes;
             const uint64_t dv0 = D == 128 ? ptx::sdesc_sw128(va, 16, 1024) : ptx::sdesc_sw64(va, 16, 512);
+            if (hu) {  // P of warp group pb in shared memory: 64 rows x 128 keys, two 8 KB SW128 key columns
+              const uint64_t dp0 = ptx::sdesc_sw128(base + C::kOOff + pb * 16384, 16, 1024);
 #pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk) {
-              ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + pb * 64 + kk * 8, dv0 + ((kk * 16 * C::kVRowBytes) >> 4),
-                               C::kIdescPV, (!first || kk > 0) ? 1u : 0u);
-              if (tr && j == 9) trace[kTraceSteps * 8 + 16 + kk] = (uint32_t)clock();
+              for (int kk = 0; kk < BN / 16; ++kk)
+                ptx::mma_ss_2cta(tmem + kColO, dp0 + ((((kk / 4) * 8192) + (kk % 4) * 32) >> 4),
+                                 dv0 + ((kk * 16 * C::kVRowBytes) >> 4), C::kIdescPVh, (!first || kk > 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < BN / 16; ++kk) {
+                ptx::mma_ts_2cta(tmem + kColO, tmem + kColP + pb * 64 + kk * 8, dv0 + ((kk * 16 * C::kVRowBytes) >> 4),
+                                 C::kIdescPV, (!first || kk > 0) ? 1u : 0u);
+                if (tr && j == 9) trace[kTraceSteps * 8 + 16 + kk] = (uint32_t)clock();
+              }
             }
             ptx::tc_commit_2cta(bar(bars->p_empty[pb]), kBoth);              // P may be overwritten
             if (last) ptx::tc_commit_2cta(bar(bars->o_full), kBoth);
@@ -684,7 +737,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // through the warp's swizzled shared-memory staging tile and one TMA tensor store per warp
     // (32 rows x D bytes), so the output leaves in whole 128-byte lines; rows past nq are clipped.
     const uint32_t sOw = base + C::kOOff + warp * 32 * D;
-    auto store_o = [&](const uint32_t* pk, int b_, int h_, int qt_) {
+    auto store_o = [&](const uint32_t* pk, int b_, int h_, int r0, int ch) {
       constexpr int NC = D / 16;  // 16-byte chunks per staged row (D/2 bf16)
       if (lane == 0) ptx::bulk_wait_read_all();  // the previous store has read the staging tile
       __syncwarp();
@@ -695,9 +748,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        const int r0 = qt_ * BM + quad * 32;
         if (pm.n == 0) {
-          ptx::tma_store_4d(&tm_o, sOw, hc * (D / 2), h_, r0, b_);
+          ptx::tma_store_4d(&tm_o, sOw, ch * (D / 2), h_, r0, b_);
         } else {
           // peer stores: the 32 rows go to their owners' receive buffers as 4 boxes of 8 rows (owner
           // boundaries n_loc are multiples of 8, so a box never straddles two owners; an 8-row slice
@@ -707,7 +759,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int rr = r0 + 8 * i;
             if (rr < nq) {
               const int p = rr / pm.n_loc;
-              ptx::tma_store_4d(&pm.m[p], sOw + i * 8 * D, hc * (D / 2), h_, rr - p * pm.n_loc, b_);
+              ptx::tma_store_4d(&pm.m[p], sOw + i * 8 * D, ch * (D / 2), h_, rr - p * pm.n_loc, b_);
             }
           }
         }
@@ -732,7 +784,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (tl && n_seg < kTlSegs) tline[8 + 4 * n_seg] = (uint32_t)clock();
       float m_used = online ? -INFINITY : 0.f;   // softmax base, log2 units (fixed base: 0)
       float l = 0.f;                              // partial row sum over this warp's keys
-      const int s_row = qt * BM + row;            // this thread's query (row of the new tokens)
+      // Half unit (PP): this CTA's 64 rows start at 256g + 64 rank; warp quadrant q holds rows 32 (q & 1) ..
+      // for keys / O columns of half q >> 1.  Its epilogue: the group-0 warps, (rows, column half q >> 1).
+      const bool hu = PP && g == half_g;
+      const int e_row = hu ? (quad & 1) * 32 + lane : row;         // this thread's row of the CTA's tile
+      const int e_ch = hu ? (quad >> 1) : hc;                      // its O column half in the epilogue
+      const bool e_act = !hu || hc == 0;                           // takes part in the epilogue
+      const int qrow0 = hu ? g * kTileQ + 64 * (int)rank : qt * BM;  // first query row of the CTA's tile
+      const int r0e = qrow0 + e_row - lane;                        // first row of this warp's epilogue store
+      const uint32_t tOe = hu ? tmem + lane_bits + kColO : tO;
+      const int s_row = qrow0 + e_row;            // this thread's query (row of the new tokens)
       const int qs = st.n == 1 ? 0 : span_at(st, min(s_row, nq - 1));  // its span (rows past nq: never stored)
       const bool map_thread = tile_map != nullptr && b == 0 && h == 0 && rank == 0 && row == 0 && hc == 0;
       int j = step_of<BN, kTab>(st, g, sg.k0, nq, kv_len, nkv);
@@ -770,6 +831,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (tr) trace[j * 8 + 4] = (uint32_t)clock();
         SCHED_POINT();
         ptx::tc_fence_after();
+        if (PP && hu) {
+          // half-unit step: 64 scores of this row (keys 64 (quad >> 1) ..), P to the warp's staging slot
+          float sh[64];
+          {
+            uint32_t r[64];
+            ptx::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            ptx::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 64; ++i) sh[i] = __uint_as_float(r[i]);
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->s_free[hc]));
+          if (tr) trace[j * 8 + 6] = (uint32_t)clock();
+          if (masked) {
+            uint32_t vm[4];
+            visible_bits(st, qs, j * BN + 64 * (quad >> 1), kv_len, vm);
+#pragma unroll
+            for (int i = 0; i < 64; ++i)
+              if (!((vm[i / 32] >> (i % 32)) & 1u)) sh[i] = -INFINITY;
+          }
+          uint64_t acc[4] = {0, 0, 0, 0};
+          uint32_t pk[32];
+          const uint64_t nb0 = ptx::f2_pack(0.f, 0.f);
+          if (masked)
+            exp_half<false>(sh, nb0, pk, acc);
+          else
+            exp_half<true>(sh, nb0, pk, acc);
+          if (tr) trace[j * 8 + 7] = (uint32_t)clock();
+          if (lane == 0) ptx::bulk_wait_read_all();  // an epilogue store has read this warp's slot
+          ptx::mbar_wait(bar(bars->p_empty[hc]), (my_u & 1) ^ 1);  // PV(j-2) has read the slot
+          ptx::tc_fence_after();
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c)  // row e_row of key column quad >> 1: 128 bytes, SW128
+            ptx::st_shared_v4(sOw + lane * 128 + ((c ^ (lane & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                              pk[4 * c + 3]);
+          {
+            const uint64_t a = ptx::f2_add(ptx::f2_add(acc[0], acc[1]), ptx::f2_add(acc[2], acc[3]));
+            float a0, a1;
+            ptx::f2_unpack(a, a0, a1);
+            l += a0 + a1;
+          }
+          ptx::fence_proxy_async_smem();  // generic-proxy stores -> the MMA's async-proxy reads
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->p_full[hc]));
+          if (tr) trace[j * 8 + 5] = (uint32_t)clock();
+          continue;
+        }
         float s[128];
         {
           uint32_t r[128];
@@ -878,23 +990,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (fast) gsm = gsm0 + (sg.k1 - sg.k0);
       first_seg = false;
       if (tl && n_seg < kTlSegs) tline[9 + 4 * n_seg] = (uint32_t)clock();
-      // total row sum over both key halves
-      red[hc * BM + row] = l;
-      ptx::named_bar_sync(pair_bar, 64);
-      const float lt = l + red[(hc ^ 1) * BM + row];
-      ptx::named_bar_sync(pair_bar, 64);  // the buffer is reused by the next exchange
+      // total row sum over both key halves (half unit: over both step groups and both key halves)
+      float lt;
+      if (!hu) {
+        red[hc * BM + row] = l;
+        ptx::named_bar_sync(pair_bar, 64);
+        lt = l + red[(hc ^ 1) * BM + row];
+        ptx::named_bar_sync(pair_bar, 64);  // the buffer is reused by the next exchange
+      } else {
+        red[(hc * 2 + (quad >> 1)) * 64 + e_row] = l;
+        ptx::named_bar_sync(kSoftmaxBar, 256);
+        lt = (red[e_row] + red[64 + e_row]) + (red[128 + e_row] + red[192 + e_row]);
+        ptx::named_bar_sync(kSoftmaxBar, 256);
+      }
       ptx::mbar_wait(bar(bars->o_full), of_phase);
       of_phase ^= 1;
       ptx::tc_fence_after();
+      if (!e_act) {  // half unit, group 1: reads no O
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));
+      }
       if (tl && n_seg < kTlSegs) tline[10 + 4 * n_seg] = (uint32_t)clock();
-      const int s_idx = qt * BM + row;
+      const int s_idx = s_row;
+      if (sg.k0 == 0 && sg.k1 == sg.cnt && !e_act) {
+        ++n_seg;
+        continue;
+      }
       if (sg.k0 == 0 && sg.k1 == sg.cnt) {
         // whole unit: O / l -> bf16 -> HBM (this warp's D/2 columns).  O leaves TMEM first and is
         // released at once, so the next unit's first PV does not wait for the global stores.
         const float inv_l = lt > 0.f ? 1.f / lt : 0.f;
         uint32_t r[D / 2];
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) ptx::tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[c * 32]));
+        for (int c = 0; c < D / 64; ++c) ptx::tmem_ld32(tOe + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r[c * 32]));
         ptx::tmem_wait_ld();
         ptx::tc_fence_before();
         __syncwarp();
@@ -904,9 +1033,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < D / 4; ++i)
             pk[i] = ptx::pack_bf16x2(__uint_as_float(r[2 * i]) * inv_l, __uint_as_float(r[2 * i + 1]) * inv_l);
-          store_o(pk, b, h, qt);
+          store_o(pk, b, h, r0e, e_ch);
         }
-        if (lse != nullptr && hc == 0 && s_idx < nq)
+        if (lse != nullptr && e_ch == 0 && s_idx < nq)
           lse[((int64_t)b * H + h) * nq + s_idx] =
               (lt > 0.f) ? (m_used + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
         if (tl && n_seg < kTlSegs) tline[11 + 4 * n_seg] = (uint32_t)clock();
@@ -919,7 +1048,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       constexpr int kSlotFloats = (D + 2) * BM;
       float* mine = ws + ((size_t)(2 * cid + (sg.k0 > 0 ? 0 : 1)) * 2 + rank) * kSlotFloats;
       const int ustart = (b * H + h) * sched0.wbh + gpre[g];
-      const int pf = pair_of(sched0, ustart), pl = pair_of(sched0, ustart + sg.cnt - 1);
+      const int pf = pair_of(sched0, ustart), pl = pair_of(sched0, ustart + sg.cnt * step_wt(half_g, g) - 1);
       // pieces = pairs in [pf, pl] with a non-empty range (a pair's range may be empty when W < P)
       int n_pieces = 0;
       for (int q = pf; q <= pl; ++q) n_pieces += pair_lo(sched0, q) < pair_lo(sched0, q + 1);
@@ -930,21 +1059,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::named_bar_sync(kSoftmaxBar, 256);
       const bool direct = bars->last_piece == 2;  // (O leaves TMEM inside the combine loop below)
 #pragma unroll 1
-      for (int c = 0; c < D / 64 && !direct; ++c) {
+      for (int c = 0; c < D / 64 && !direct && e_act; ++c) {
         uint32_t r[32];
-        ptx::tmem_ld32(tO + c * 32, r);
+        ptx::tmem_ld32(tOe + c * 32, r);
         ptx::tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) __stcg(mine + (hc * (D / 2) + c * 32 + i) * BM + row, __uint_as_float(r[i]));
+        for (int i = 0; i < 32; ++i) __stcg(mine + (e_ch * (D / 2) + c * 32 + i) * BM + e_row, __uint_as_float(r[i]));
       }
       if (!direct) {
-        if (hc == 0) {
-          __stcg(mine + D * BM + row, lt);
-          __stcg(mine + (D + 1) * BM + row, m_used);
+        if (e_act && e_ch == 0) {
+          __stcg(mine + D * BM + e_row, lt);
+          __stcg(mine + (D + 1) * BM + e_row, m_used);
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(lbar(bars->o_empty));  // TMEM O has been read
+        if (lane == 0 && e_act) ptx::mbar_arrive_cluster(lbar(bars->o_empty));  // TMEM O has been read
         if (tl && n_part < 2) tline[50 + 5 * n_part] = (uint32_t)clock();
         // publish: every thread's stores precede the barrier; one thread fences (cumulative) and counts
         ptx::named_bar_sync(kSoftmaxBar, 256);
@@ -958,7 +1087,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::named_bar_sync(kSoftmaxBar, 256);
       }
       if (tl && n_part < 2) tline[51 + 5 * n_part] = (uint32_t)clock();
-      if (!bars->last_piece) {
+      if (!bars->last_piece || !e_act) {
         if (tl && n_seg < kTlSegs) tline[11 + 4 * n_seg] = (uint32_t)clock();
         ++n_seg;
         ++n_part;
@@ -975,7 +1104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int q = pf; q <= pl; ++q) {
         if (pair_lo(sched0, q) == pair_lo(sched0, q + 1)) continue;
         const float* pc = ws + ((size_t)(2 * q + (q == pf ? 1 : 0)) * 2 + rank) * kSlotFloats;
-        mmax = fmaxf(mmax, (direct && q == cid) ? m_own : __ldcg(pc + (D + 1) * BM + row));
+        mmax = fmaxf(mmax, (direct && q == cid) ? m_own : __ldcg(pc + (D + 1) * BM + e_row));
       }
       float wsum = 0.f;
       float acc[D / 2];
@@ -989,15 +1118,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         float mq, lq;
         if (direct && q == cid) {
 #pragma unroll
-          for (int c = 0; c < D / 64; ++c) ptx::tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[c * 32]));
+          for (int c = 0; c < D / 64; ++c) ptx::tmem_ld32(tOe + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[c * 32]));
           ptx::tmem_wait_ld();
           mq = m_own;
           lq = l_own;
         } else {
 #pragma unroll
-          for (int i = 0; i < D / 2; ++i) v[i] = __ldcg(pc + (hc * (D / 2) + i) * BM + row);
-          mq = __ldcg(pc + (D + 1) * BM + row);
-          lq = __ldcg(pc + D * BM + row);
+          for (int i = 0; i < D / 2; ++i) v[i] = __ldcg(pc + (e_ch * (D / 2) + i) * BM + e_row);
+          mq = __ldcg(pc + (D + 1) * BM + e_row);
+          lq = __ldcg(pc + D * BM + e_row);
         }
         const float wq = mq == -INFINITY ? 0.f : ptx::ex2(mq - mmax);  // fixed base: every mq = 0, wq = 1
         wsum += wq * lq;
@@ -1015,9 +1144,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t pk[D / 4];
 #pragma unroll
         for (int i = 0; i < D / 4; ++i) pk[i] = ptx::pack_bf16x2(acc[2 * i] * inv_l, acc[2 * i + 1] * inv_l);
-        store_o(pk, b, h, qt);
+        store_o(pk, b, h, r0e, e_ch);
       }
-      if (lse != nullptr && hc == 0 && s_idx < nq)
+      if (lse != nullptr && e_ch == 0 && s_idx < nq)
         lse[((int64_t)b * H + h) * nq + s_idx] =
             (wsum > 0.f) ? (mmax + __log2f(wsum)) * 0.69314718055994530942f : -INFINITY;
       if (threadIdx.x == 0) *cnt_ptr = 0;  // ready for the next launch

@@ -50,6 +50,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1) bench(long l
         for (int kk = 0; kk < 8; ++kk)
           ptx::mma_ts_2cta(tmem + 256, tmem + kk * 8, ptx::sdesc_sw128(b + kk * 2048, 16, 1024), idesc_ts, 1);
       }
+      if (MODE == 3 || MODE == 5) {  // half-unit QK: M = 128 per pair (64 rows per CTA)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t qoff = (kk / 4) * 16384 + (kk % 4) * 32, koff = (kk / 4) * 8192 + (kk % 4) * 32;
+          ptx::mma_ss_2cta(tmem + 128, ptx::sdesc_sw128(a + qoff, 16, 1024), ptx::sdesc_sw128(b + koff, 16, 1024),
+                           ptx::idesc_f16(0, 0, 0, 0, 128, 128), 1);
+        }
+      }
+      if (MODE == 4 || MODE == 5) {  // half-unit PV: P (K-major, 64 rows per CTA) x V (MN-major), M = 128
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_ss_2cta(tmem + 256, ptx::sdesc_sw128(a + (kk / 4) * 8192 + (kk % 4) * 32, 16, 1024),
+                           ptx::sdesc_sw128(b + kk * 2048, 16, 1024), ptx::idesc_f16(1, 1, 0, 1, 128, 128), 1);
+      }
       if (MODE == 0 || MODE == 2) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -231,6 +245,14 @@ void run(const char* name, double instr_per_iter) {
 }
 
 int main() {
+  if (getenv("ONLY_HALF")) {  // M = 128 pair MMAs (half units), per instruction against M = 256
+    run<0, true, false>("2CTA SS M256 N128 random", 8);
+    run<3, true, false>("2CTA SS M128 N128 (QK half)", 8);
+    run<4, true, false>("2CTA SS M128 N128 (PV half)", 8);
+    run<5, true, false>("2CTA QK+PV half", 16);
+    run<2, true, false>("2CTA TS+SS M256", 16);
+    return 0;
+  }
   if (getenv("ONLY_TMA")) {
     run<0, true, false, 1, 0, 41>("SS + TMA 16KB x1 in flight", 8);
     run<0, true, false, 1, 0, 42>("SS + TMA 16KB x2 in flight", 8);
