@@ -104,7 +104,7 @@ __device__ __forceinline__ uint32_t gtime() {
 // PP (ping-pong, fixed softmax base): 128-key steps, S and P double-buffered, the two
 // softmax warp groups take alternate steps.  !PP (online base): 256-key steps, each step
 // split in two key halves between the two warp groups.
-constexpr int kClsWords = kMaxStepTiles / 16;  // step-class table (several spans): 16 KB static shared memory
+constexpr int kClsWords = kMaxStepTiles / 16;  // step-class table (several spans): at most 16 KB of shared memory
 
 // F8 (DZ_FLAG_FP8_QK): Q' and K' are E4M3, one byte per element; QK^T by tcgen05.mma kind::f8f6f4
 // (K = 32 per instruction), PV unchanged (bf16).
@@ -136,6 +136,7 @@ struct Cfg {
   static constexpr bool kTab = PP || D == 64;                     // static step-class table fits beside
   static constexpr int kBarOff = kOOff + 8 * 32 * D;
   static constexpr int kSmem = kBarOff + 1024 + 1024;             // + barriers/schedule + alignment slack
+                                                                   // (+ the launch's step-class table)
   static_assert(kSmem + (kTab ? kClsWords * 4 : 0) <= 232448, "shared memory per CTA");
   static_assert(8 * 32 * D <= 32768 || !F8, "O staging");
   static constexpr uint32_t kIdescQK = ptx::idesc_f16(0, 0, 0, 0, 2 * BM, BN / 2);  // f16 x f16, K-major, per half
@@ -243,7 +244,13 @@ __device__ __forceinline__ uint8_t step_class(const SpanTable& st, int g, int j,
 // (the rows_in_bounds class: SKIP, PARTIAL = needs a mask, FULL), built once per CTA in static
 // shared memory so the single-thread roles (MMA issuers, TMA producers) never evaluate span loops
 // on their critical path.  With one span, or a table too large, the class is evaluated on the fly.
-__shared__ uint32_t s_cls_tab[kClsWords];
+// The table sits at the start of the dynamic shared memory, sized per launch (none with one span),
+// so a single-span launch keeps those bytes for the K/V rings; the kernel's tiles follow it.
+extern __shared__ __align__(16) uint32_t s_cls_tab[];
+// bytes of the table for a launch (multiple of 16)
+__host__ __device__ constexpr int cls_tab_bytes(bool tab, int n_spans, int n_groups, int nkv) {
+  return (tab && n_spans != 1) ? ((n_groups * nkv + 63) / 64) * 16 : 0;
+}
 template <int TK, bool kTab>
 __device__ __forceinline__ uint8_t cls_get(const SpanTable& st, int g, int j, int nq, int kv_len, int nkv) {
   if (kTab) {  // (the host rejects span layouts whose table would not fit: dz_attend_spans -> DZ_ESHAPE)
@@ -376,9 +383,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr int BN = C::kBN;  // keys per step (shadows the file-level 256)
   ptx::pdl_launch_dependents();  // the next kernel may take SMs as our CTAs finish (it waits for us)
   extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = ptx::smem_u32(smem_raw);
+  const uint32_t raw = ptx::smem_u32(smem_raw) + cls_tab_bytes(C::kTab, st.n, (((nq + BM - 1) / BM) + 1) / 2,
+                                                               (kv_len + BN - 1) / BN);
   const uint32_t base = (raw + 1023u) & ~1023u;           // SW128 tiles need 1024-byte alignment
-  uint8_t* smem = smem_raw + (base - raw);
+  uint8_t* smem = smem_raw + (base - ptx::smem_u32(smem_raw));
   Bars* bars = reinterpret_cast<Bars*>(smem + C::kBarOff);
   float* red = reinterpret_cast<float*>(smem + C::kRedOff);
   const uint32_t sQ = base + C::kQOff;
@@ -1175,9 +1183,12 @@ template <int D, bool PP, bool F8 = false>
 cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
   using C = Cfg<D, PP, F8>;
   auto k = attn_fwd_kernel<D, PP, F8>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       C::kSmem + (C::kTab ? kClsWords * 4 : 0));
   if (e != cudaSuccess) return e;
-  return launch_pdl(k, dim3(a.grid), dim3(kThreads), C::kSmem, s, a.tm_q, a.tm_k, a.tm_v, a.tm_k2, a.tm_v2, a.tm_o,
+  const int n_groups = ((a.nq + BM - 1) / BM + 1) / 2, nkv = (a.kv_len + C::kBN - 1) / C::kBN;
+  const int smem = C::kSmem + cls_tab_bytes(C::kTab, a.spans.n, n_groups, nkv);
+  return launch_pdl(k, dim3(a.grid), dim3(kThreads), (size_t)smem, s, a.tm_q, a.tm_k, a.tm_v, a.tm_k2, a.tm_v2, a.tm_o,
                     a.cur_step,
                     static_cast<__nv_bfloat16*>(a.out), a.o_bstride, a.o_tstride, a.lse, a.tile_map, a.B, a.H, a.nq,
                     a.kv_len, a.m_static, a.debug_flags, a.ws, a.ws_cnt, a.spans, a.pm);
