@@ -493,8 +493,7 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   a.kv_len = (int32_t)kv_len;
   a.scale_log2 = c->scale * 1.4426950408889634f;
   a.m_static = c->m_static;
-  // diagnostics: bit 0 no K/V TMA (results are garbage); bit 1 the last query group as a padded M = 256 unit
-  if (const char* e = getenv("DZ_DEBUG_KERNEL")) a.debug_flags = atoi(e);
+  if (const char* e = getenv("DZ_DEBUG_KERNEL")) a.debug_flags = atoi(e);  // diagnostics: results are garbage
   // persistent grid: one CTA pair per TPC; stream-K spreads the executed steps evenly over the pairs
   a.grid = 2 * std::min(c->num_sms / 2, dz::kMaxPairs);
   // stream-K needs <= 64 query groups and 32-bit step arithmetic (W * pairs < 2^31); else whole units round-robin

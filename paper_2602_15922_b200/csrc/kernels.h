@@ -119,8 +119,7 @@ struct AttnArgs {
   int32_t B = 0, H = 0, D = 0, nq = 0, kv_len = 0;
   float scale_log2 = 0.f;         // unused by the kernel: Q' is pre-scaled by softmax_scale * log2(e)
   float m_static = 0.f;           // > 0: fixed softmax base (log2 units) bounding every logit; 0: online max
-  int32_t debug_flags = 0;        // diagnostics only (DZ_DEBUG_KERNEL env): 1 no K/V TMA (results are garbage),
-                                  // 2 no half units (the last query group padded to M = 256)
+  int32_t debug_flags = 0;        // diagnostics only (DZ_DEBUG_KERNEL env): 1 no K/V TMA (results are garbage)
   int32_t grid = 0;               // persistent CTAs (<= #SMs)
   float* ws = nullptr;            // stream-K piece workspace: [2 * pairs][2 ranks][(D + 2) * 128] fp32 (nullptr: no split)
   int32_t* ws_cnt = nullptr;      // per (unit, rank) piece counters, zero between launches
@@ -132,7 +131,7 @@ int attention_units(int32_t B, int32_t H, int32_t nq);
 constexpr int kTileQ = 256;  // skip / mask decision granularity: query rows of a CTA pair x the keys of a step
 // stream-K balances cost-weighted steps: a step of a full 256-row unit weighs kStepWeight, a step of a
 // half unit (a last query group of <= 128 rows, run as M = 128 pair MMAs) less (attention.cu)
-constexpr int kStepWeight = 16;
+constexpr int kStepWeight = 8;
 // keys per K2 step: 128 with the fixed softmax base (ping-pong kernel), 256 with the online base
 int attention_step_keys(float m_static);
 // span layouts (several spans): the kernel's step-class table holds at most kMaxStepTiles

@@ -6,11 +6,7 @@ os.environ.setdefault("DZ_LIB_PATH", os.path.join(ROOT, "paper_2602_15922_b200",
 import numpy as np, torch, synth
 import paper_2602_15922_b200 as dz
 from helpers import GpuRun
-name = sys.argv[1] if len(sys.argv) > 1 else "C1"
-if name == "half128":  # every query group a half unit (tools/half_bench.py)
-    w = synth.scaled(synth.workload("C1"), frames=1, grid_h=4, grid_w=8, views=1, actions=96, cached_chunks=52)
-else:
-    w = synth.workload(name)
+w = synth.workload(sys.argv[1] if len(sys.argv) > 1 else "C1")
 run = GpuRun(w, flags=int(os.environ.get("DZ_FLAGS", "0"))); run.fill(); run.attend(); torch.cuda.synchronize()
 dz.debug_trace(True); run.attend(); torch.cuda.synchronize()
 tr = dz.debug_trace(False, read=True).astype(np.int64)
