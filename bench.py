@@ -302,8 +302,8 @@ def run_reference(args, w: synth.Workload, rank: int):
 class Timer:
     """Times K steps with CUDA events at step boundaries only (an event between two kernels
     would end their programmatic overlap), the L2 flushed before every step; the library's
-    per-kernel events are measured in a profiled step run after each timed one (same load and
-    clocks, not part of the sum)."""
+    per-kernel events are measured in K profiled steps run after the timed ones (not part of
+    the sum)."""
 
     def __init__(self, dev, flush=True, flush_read=False):
         self.flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if flush else None
@@ -326,6 +326,10 @@ class Timer:
         sampler = ClockSampler(clock_dev) if clock_dev is not None else None
         if sampler:
             sampler.__enter__()
+        # the timed steps are enqueued back to back with no host synchronisation, so the host runs
+        # ahead of the device and the events time device work only (host launch latency is part of
+        # the e2e measurement); the profiled steps (per-kernel library events, one host sync each)
+        # follow in a loop of their own
         for i in range(steps):
             self.flush()
             torch.cuda.nvtx.range_push(f"dz step {i}")  # NVTX ranges: visible to nsys / ncu --nvtx
@@ -335,19 +339,20 @@ class Timer:
             launches += dz.kernel_launches() - n0
             ev[i][1].record()
             torch.cuda.nvtx.range_pop()
-            if profiled:
-                cache.profile_enable(True)
-                self.flush()
-                torch.cuda.nvtx.range_push(f"dz profiled step {i}")
-                step()
-                torch.cuda.nvtx.range_pop()
-                p = cache.profile_last()         # host-syncs on the library's events (last call)
-                for k in prof:
-                    prof[k].append(p[k])
-                cache.profile_enable(False)
         torch.cuda.synchronize()
         if sampler:
             sampler.__exit__()
+        for i in range(steps if profiled else 0):
+            cache.profile_enable(True)
+            self.flush()
+            torch.cuda.nvtx.range_push(f"dz profiled step {i}")
+            step()
+            torch.cuda.nvtx.range_pop()
+            p = cache.profile_last()         # host-syncs on the library's events (last call)
+            for k in prof:
+                prof[k].append(p[k])
+            cache.profile_enable(False)
+        torch.cuda.synchronize()
         step_ms = [a.elapsed_time(b) for a, b in ev]
         return step_ms, prof, launches, (sampler.summary() if sampler else None)
 
