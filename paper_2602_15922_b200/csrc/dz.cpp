@@ -450,8 +450,9 @@ dz_status run_attention(dz_ctx* c, int64_t n, const dz::SpanTable& spans, void* 
   a.spans.valid = (int32_t)c->valid;
   const int64_t kv_len = c->valid + n;
   const int64_t bs = c->L.slots * c->Hl * c->D;
-  // Q: 128-row tiles per CTA; K: each CTA of a pair loads 2 x 64 of a step's 256 keys;
-  // V: each CTA loads D/2 of the columns of all 256 keys (see attention.cu).
+  // Q: 128-row tiles per CTA; a step is 128 keys (fixed softmax base) or 256 (online base,
+  // dz::attention_step_keys): each CTA of a pair loads 64-key boxes of K (half of the step's keys)
+  // and D/2 of the columns of all the step's V rows (see attention.cu).
   // FP8 QK: Q' / K' are E4M3 rows of D bytes: one 128-byte SW128 box per row
   const int qk_dt = c->f8 ? 2 : 0;
   const uint32_t qk_box = c->f8 ? (uint32_t)c->D : 64u;

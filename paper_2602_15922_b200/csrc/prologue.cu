@@ -399,18 +399,41 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(co
 // an item of the attend set (j0) carries (q, k), an item of the appended set (j1) carries (k, v), so
 // slot 0 is q or k and slot 1 is k or v (v: a copy).  Same arithmetic and order as
 // prologue_loop_kernel; two thirds of its load registers (no spills at two CTAs per SM).
-template <int D, bool F8 = false>
-__global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_dual2_kernel(const PrologueArgs a) {
-  constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
+// NT threads per CTA (NT / (D / 8) head rows per pass), KP passes: 256 x 3 covers 48 heads at D = 128,
+// 320 x 2 covers 40 with no idle head slots and two thirds of the load registers (two CTAs per SM
+// either way: 20 warps instead of 16)
+template <int D, bool F8 = false, int NT = 256, int KP = 3>
+__global__ void __launch_bounds__(NT, DZ_PRO_LOOP_MINB) prologue_dual2_kernel(const PrologueArgs a) {
+  constexpr int G = D / 8, kRows = NT / G, kPer = KP;
   ptx::pdl_launch_dependents();
   const int tid = threadIdx.x, g = tid / G, li = tid % G;
   const int H = a.H, items0 = a.B * a.n, items = items0 + a.B * a.j1.n;
-  auto locate = [&](int item, int& b, int& t) -> bool {
-    const bool s1 = item >= items0;
-    const int it = s1 ? item - items0 : item, nn = s1 ? a.j1.n : a.n;
-    b = it / nn;
-    t = it - b * nn;
-    return s1;
+  // item cursor (set, batch element, token), advanced by gridDim.x without a division except
+  // when it crosses into the appended set
+  struct Cur {
+    int item, b, t;
+    bool s1;
+  };
+  auto at = [&](int item) {
+    Cur c;
+    c.item = item;
+    c.s1 = item >= items0;
+    const int it = c.s1 ? item - items0 : item, nn = c.s1 ? a.j1.n : a.n;
+    c.b = it / nn;
+    c.t = it - c.b * nn;
+    return c;
+  };
+  auto adv = [&](const Cur& c) {
+    if (!c.s1 && c.item + (int)gridDim.x >= items0) return at(c.item + (int)gridDim.x);
+    Cur d = c;
+    const int nn = c.s1 ? a.j1.n : a.n;
+    d.item += gridDim.x;
+    d.t += gridDim.x;
+    while (d.t >= nn) {
+      d.t -= nn;
+      ++d.b;
+    }
+    return d;
   };
   const int64_t tokD = (int64_t)H * D;
   int64_t ooff[kPer];  // one GPU: every tensor's row of head h sits at h * D in the token's block
@@ -421,9 +444,9 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_dual2_kernel(c
     hv[i] = h < H;
     ooff[i] = (int64_t)h * D + li * 8;
   }
-  auto load = [&](int item, uint4 (&v)[2][kPer]) {
-    int b, t;
-    const bool s1 = locate(item, b, t);
+  auto load = [&](const Cur& c, uint4 (&v)[2][kPer]) {
+    const int b = c.b, t = c.t;
+    const bool s1 = c.s1;
     const int64_t src = (int64_t)b * (s1 ? a.j1.x_bstride : a.x_bstride) + (int64_t)t * tokD + g * D + li * 8;
 #pragma unroll
     for (int sl = 0; sl < 2; ++sl) {
@@ -437,12 +460,11 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_dual2_kernel(c
   int ax[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) ax[e] = a.axis[li * 4 + e];
-  auto positions = [&](int item, int (&p)[4]) {
-    if (item >= items) return;
-    int b, t;
-    const int32_t* pos = locate(item, b, t) ? a.j1.pos : a.pos;
+  auto positions = [&](const Cur& c, int (&p)[4]) {
+    if (c.item >= items) return;
+    const int32_t* pos = c.s1 ? a.j1.pos : a.pos;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) p[e] = __ldg(pos + 3 * t + ax[e]);
+    for (int e = 0; e < 4; ++e) p[e] = __ldg(pos + 3 * c.t + ax[e]);
   };
   auto angles = [&](const int (&p)[4], float2 (&c)[4]) {
 #pragma unroll
@@ -454,22 +476,21 @@ __global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_dual2_kernel(c
   uint4 v[2][kPer], vn[2][kPer];
   float2 csr[4], csn[4];
   int pn[4] = {0, 0, 0, 0};
-  int item = blockIdx.x;
-  if (item < items) {
-    load(item, v);
-    positions(item, pn);
+  Cur cur = at(blockIdx.x), nxt = adv(cur), nn2 = adv(nxt);  // this item, the next, the one after
+  if (cur.item < items) {
+    load(cur, v);
+    positions(cur, pn);
     angles(pn, csr);
-    positions(item + gridDim.x, pn);
+    positions(nxt, pn);
   }
-  for (; item < items; item += gridDim.x) {
-    const int nxt = item + gridDim.x;
-    if (nxt < items) {  // in flight while this token is processed
+  for (; cur.item < items; cur = nxt, nxt = nn2, nn2 = adv(nn2)) {
+    if (nxt.item < items) {  // in flight while this token is processed
       load(nxt, vn);
       angles(pn, csn);
-      positions(nxt + gridDim.x, pn);
+      positions(nn2, pn);
     }
-    int b, t;
-    const bool s1 = locate(item, b, t);
+    const int b = cur.b, t = cur.t;
+    const bool s1 = cur.s1;
 #pragma unroll
     for (int sl = 0; sl < 2; ++sl) {
       const int w = s1 ? sl + 1 : sl;  // the tensor in this slot: 0 q, 1 k, 2 v (uniform per item)
@@ -554,20 +575,33 @@ cudaError_t launch_loop(const PrologueArgs& a, cudaStream_t s) {
                     dim3(256), 0, s, a);
 }
 
+#ifndef DZ_PRO_NT320
+#define DZ_PRO_NT320 1
+#endif
+// persistent grid of a token-loop kernel: SMs x resident CTAs per SM x DZ_PRO_LOOP_WAVES
+template <typename K>
+int grid_of(K kernel, int threads) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  return sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
+}
+
 // the two-slot fused prologue when the sets are (q, k) and (k, v); false: use the three-slot loop
 template <int D, bool F8>
 bool launch_dual2(const PrologueArgs& a, cudaStream_t s, cudaError_t& err) {
   static const bool dual3 = getenv("DZ_PRO_DUAL3") != nullptr;  // A/B switch (diagnostics)
   if (dual3 || !(a.x[0] && a.x[1] && !a.x[2] && !a.j1.x[0] && a.j1.x[1] && a.j1.x[2])) return false;
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_dual2_kernel<D, F8>, 256, 0);
-    grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
-  }
   const int items = a.B * (a.n + a.j1.n);
+  if (DZ_PRO_NT320 && D == 128 && a.H <= 2 * (320 / (D / 8))) {
+    static int grid_cap = 0;
+    if (grid_cap == 0) grid_cap = grid_of(prologue_dual2_kernel<D, F8, 320, 2>, 320);
+    err = launch_pdl(prologue_dual2_kernel<D, F8, 320, 2>, dim3((unsigned)std::min(items, grid_cap)), dim3(320), 0, s, a);
+    return true;
+  }
+  static int grid_cap = 0;
+  if (grid_cap == 0) grid_cap = grid_of(prologue_dual2_kernel<D, F8>, 256);
   err = launch_pdl(prologue_dual2_kernel<D, F8>, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s, a);
   return true;
 }
