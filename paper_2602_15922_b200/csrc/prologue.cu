@@ -245,9 +245,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) prologue_kernel(const Pr
 // union of both sets' tensors and a tensor absent from an item's set (x[w] == nullptr) is skipped.
 // PEER: rows go straight to the destination ranks' buffers (a.peer_y, DZ_FLAG_PEER_STORE).
 // F8: Q' and K' are stored as E4M3 (DZ_FLAG_FP8_QK; one byte per element, rows of D bytes).
-template <int D, int MASK, bool DUAL, bool PEER = false, bool F8 = false>
-__global__ void __launch_bounds__(256, DZ_PRO_LOOP_MINB) prologue_loop_kernel(const PrologueArgs a) {
-  constexpr int G = D / 8, kRows = 256 / G, kPer = 3;
+// NT threads, KP head passes per CTA (as prologue_dual2_kernel: 256 x 3, or 320 x 2 for H <= 40 at D = 128)
+template <int D, int MASK, bool DUAL, bool PEER = false, bool F8 = false, int NT = 256, int KP = 3>
+__global__ void __launch_bounds__(NT, DZ_PRO_LOOP_MINB) prologue_loop_kernel(const PrologueArgs a) {
+  constexpr int G = D / 8, kRows = NT / G, kPer = KP;
   ptx::pdl_launch_dependents();
   const int tid = threadIdx.x, g = tid / G, li = tid % G;
   const int H = a.H, items0 = a.B * a.n, items = items0 + (DUAL ? a.B * a.j1.n : 0);
@@ -560,21 +561,6 @@ __global__ void rope_table_kernel(float2* __restrict__ tab, int32_t len, const P
 
 }  // namespace
 
-template <int D, int MASK, bool DUAL = false, bool PEER = false, bool F8 = false>
-cudaError_t launch_loop(const PrologueArgs& a, cudaStream_t s) {
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prologue_loop_kernel<D, MASK, DUAL, PEER, F8>, 256, 0);
-    grid_cap = sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
-  }
-  const int items = a.B * (a.n + (DUAL ? a.j1.n : 0));
-  return launch_pdl(prologue_loop_kernel<D, MASK, DUAL, PEER, F8>, dim3((unsigned)std::min(items, grid_cap)),
-                    dim3(256), 0, s, a);
-}
-
 #ifndef DZ_PRO_NT320
 #define DZ_PRO_NT320 1
 #endif
@@ -586,6 +572,21 @@ int grid_of(K kernel, int threads) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
   return sms * std::max(1, per_sm) * DZ_PRO_LOOP_WAVES;
+}
+
+template <int D, int MASK, bool DUAL = false, bool PEER = false, bool F8 = false>
+cudaError_t launch_loop(const PrologueArgs& a, cudaStream_t s) {
+  const int items = a.B * (a.n + (DUAL ? a.j1.n : 0));
+  if (DZ_PRO_NT320 && D == 128 && a.H <= 2 * (320 / (D / 8))) {
+    auto k = prologue_loop_kernel<D, MASK, DUAL, PEER, F8, 320, 2>;
+    static int grid_cap = 0;
+    if (grid_cap == 0) grid_cap = grid_of(k, 320);
+    return launch_pdl(k, dim3((unsigned)std::min(items, grid_cap)), dim3(320), 0, s, a);
+  }
+  auto k = prologue_loop_kernel<D, MASK, DUAL, PEER, F8>;
+  static int grid_cap = 0;
+  if (grid_cap == 0) grid_cap = grid_of(k, 256);
+  return launch_pdl(k, dim3((unsigned)std::min(items, grid_cap)), dim3(256), 0, s, a);
 }
 
 // the two-slot fused prologue when the sets are (q, k) and (k, v); false: use the three-slot loop
