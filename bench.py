@@ -78,6 +78,8 @@ def parse(argv=None):
     ap.add_argument("--fp8", action="store_true", help="FP8 (E4M3) QK^T variant (DZ_FLAG_FP8_QK; NEXT-2)")
     ap.add_argument("--cooldown", type=float, default=3.0,
                     help="idle seconds before each secondary workload (each starts at full clocks)")
+    ap.add_argument("--no-discard", action="store_true",
+                    help="keep the flush write's dirty lines in L2 (written back during the step)")
     ap.add_argument("--flush-read", action="store_true",
                     help="after the 512 MB flush write, read 256 MB of it so no dirty flush lines stay in L2")
     return ap.parse_args(argv)
@@ -305,15 +307,19 @@ class Timer:
     per-kernel events are measured in K profiled steps run after the timed ones (not part of
     the sum)."""
 
-    def __init__(self, dev, flush=True, flush_read=False):
+    def __init__(self, dev, flush=True, flush_read=False, discard=True):
         self.flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if flush else None
         self.flush_read = flush_read
+        self.discard = discard
 
     def flush(self):
         if self.flush_buf is not None:
             self.flush_buf.zero_()
             if self.flush_read:
                 self.flush_buf[: self.flush_buf.numel() // 2].sum()
+            if self.discard:  # the flush's dirty lines leave L2 without a write-back inside the step
+                import paper_2602_15922_b200 as dz
+                dz.l2_discard(self.flush_buf)
 
     def run(self, step, steps, cache=None, profiled=True, clock_dev=None):
         import paper_2602_15922_b200 as dz
@@ -357,12 +363,17 @@ class Timer:
         return step_ms, prof, launches, (sampler.summary() if sampler else None)
 
 
+# cache slack before a compaction, in chunks: the window slides by one chunk per step and the cache
+# is compacted (one device copy of the window) once per SLACK_CHUNKS steps; 64 chunks of C1 are 1.8 GB
+SLACK_CHUNKS = int(os.environ.get("DZ_BENCH_SLACK_CHUNKS", "64"))
+
+
 def make_cache(dz, w, dev, gq, gk, batch=None, world=1, rank=0, comm=0, flags=0, slack=None, max_chunk=None):
     n = w.chunk_tokens
     return dz.ChunkKVCache(w.batch if batch is None else batch, w.heads, w.head_dim, w.cache_tokens,
                            n if max_chunk is None else max_chunk, w.rope_dims, gq.to(dev), gk.to(dev),
                            rope_theta=w.rope_theta, rms_eps=w.rms_eps,
-                           window_slack=16 * n if slack is None else slack, world_size=world, rank=rank,
+                           window_slack=SLACK_CHUNKS * n if slack is None else slack, world_size=world, rank=rank,
                            nccl_comm=comm, flags=flags, device=dev)
 
 
@@ -649,7 +660,7 @@ def main():
     # ---------------- timed region
     flop_step = flop_one * S                         # global useful FLOP of one step (all ranks)
     profiled = graph is None and not args.no_profile
-    timer = Timer(dev, flush=not args.no_flush, flush_read=args.flush_read)
+    timer = Timer(dev, flush=not args.no_flush, flush_read=args.flush_read, discard=not args.no_discard)
     if pg:
         pg.barrier()
     step_ms, prof, launches, clocks = timer.run(step, args.steps, cache, profiled=profiled, clock_dev=local)
@@ -764,7 +775,8 @@ def main():
                             "one attend_spans (K1+K2, SKIP tiles never loaded)" if args.mode == "tf" else
                             f"{S} denoising steps of one chunk (K1+K2 each) over a fixed cache"
                             + (", one CUDA graph replay" if graph is not None else ", eager")),
-                   "l2": "flushed before every timed step (512 MB write)" if not args.no_flush else "warm",
+                   "l2": ("warm" if args.no_flush else "flushed before every timed step (512 MB write"
+                          + (")" if args.no_discard else ", then its L2 lines discarded without write-back)")),
                    "qk_storage": "e4m3 (FP8 variant)" if args.fp8 else "fp16 (post-RMSNorm)", "pv": "bf16",
                    "accumulate": "fp32"},
         "pct_peak": value / (world * peak), "pct_peak_sustained": value / (world * peak_sus),

@@ -375,6 +375,14 @@ DZ_API dz_status dz_debug_sp_unpack(const void* recv, void* out, int32_t world_s
  * is the number of the library's kernels in it (benchmark evidence). */
 DZ_API int64_t dz_kernel_launches(void);
 
+/* Benchmark helper, not part of the path: invalidates the L2 lines of the
+ * device buffer buf[0, bytes) without writing them back (PTX discard.global.L2;
+ * the buffer's contents become undefined).  bench.py runs it after the 512 MB
+ * L2-flush write so that the flush's dirty lines are not written back during the
+ * timed step.  bytes must be a multiple of 128 (DZ_EINVAL otherwise); enqueued
+ * on `stream`, not counted by dz_kernel_launches. */
+DZ_API dz_status dz_debug_l2_discard(void* buf, size_t bytes, void* stream);
+
 /* Number of attention work units (batch x heads/world_size x query-tile pairs)
  * for an n-token chunk; the persistent grid is min(units, SM count). */
 DZ_API int32_t dz_attention_units(const dz_ctx* ctx, int32_t n_tokens);

@@ -109,6 +109,7 @@ SIGNATURES = [
     ("dz_profile_enable", I32, [P, I32]),
     ("dz_debug_trace", I32, [I32, P, SZ]),
     ("dz_kernel_launches", I64, []),
+    ("dz_debug_l2_discard", I32, [P, SZ, P]),
 ]
 
 _lib = None
@@ -157,6 +158,16 @@ def _need(t: torch.Tensor, name: str, dtype: torch.dtype, shape: Sequence[int], 
 def kernel_launches() -> int:
     """Kernels the library has enqueued in this process (host-side count at launch)."""
     return int(lib().dz_kernel_launches())
+
+
+def l2_discard(buf) -> None:
+    """Benchmark helper: drop a device tensor's L2 lines without write-back (dz_debug_l2_discard)."""
+    import torch
+    nbytes = buf.numel() * buf.element_size() // 128 * 128
+    s = lib().dz_debug_l2_discard(ctypes.c_void_p(buf.data_ptr()), nbytes,
+                                  ctypes.c_void_p(torch.cuda.current_stream(buf.device).cuda_stream))
+    if s:
+        raise DzError(s, "dz_debug_l2_discard")
 
 
 def watchdog(reset: bool = True):

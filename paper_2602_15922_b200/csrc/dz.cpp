@@ -1238,6 +1238,11 @@ dz_status dz_debug_sp_unpack(const void* recv, void* out, int32_t world_size, in
              : DZ_ECUDA;
 }
 
+dz_status dz_debug_l2_discard(void* buf, size_t bytes, void* stream) {
+  if (!buf || bytes % 128) return DZ_EINVAL;
+  return dz::launch_l2_discard(buf, bytes, static_cast<cudaStream_t>(stream)) == cudaSuccess ? DZ_OK : DZ_ECUDA;
+}
+
 int64_t dz_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int32_t dz_attention_units(const dz_ctx* c, int32_t n) {

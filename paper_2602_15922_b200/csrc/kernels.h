@@ -178,4 +178,7 @@ cudaError_t launch_attention_backward(const BwdArgs& a, cudaStream_t s);
 cudaError_t launch_sp_unpack(const void* recv, void* out, int32_t N, int32_t B, int32_t n_loc, int32_t Hl,
                              int32_t D, cudaStream_t s);
 
+// ---- benchmark helper: invalidate a buffer's L2 lines without write-back (l2.cu) ---
+cudaError_t launch_l2_discard(void* p, size_t bytes, cudaStream_t s);
+
 }  // namespace dz

@@ -547,3 +547,18 @@ def test_append_attend_validation():
         run.cache.append_attend(k, v, pos, 2, q, k, v, pos, 3)
     assert e.value.status == -3
     assert run.cache.state()[1] == 2            # the failed call changed nothing
+
+
+def test_l2_discard_helper_leaves_no_launch_count_and_validates():
+    # bench helper (dz_debug_l2_discard): enqueues without error on a buffer larger than L2, is not
+    # counted as a path kernel, and rejects sizes that are not whole 128-byte lines
+    import ctypes
+    import paper_2602_15922_b200 as dz
+    buf = torch.ones(160 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    n0 = dz.kernel_launches()
+    dz.l2_discard(buf)
+    torch.cuda.synchronize()
+    assert dz.kernel_launches() == n0
+    s = dz.lib().dz_debug_l2_discard(ctypes.c_void_p(buf.data_ptr()), 100, None)
+    assert s != 0
+    assert dz.lib().dz_debug_l2_discard(None, 128, None) != 0
