@@ -595,6 +595,8 @@ def main():
                      streams[0].cache_pos[c][sl].contiguous().to(dev), c)
     q, k, v = (dev_chunk(stack(x, 0)) for x in ("cur_q", "cur_k", "cur_v"))
     kc, vc = dev_chunk(stack("cur_k", 1)), dev_chunk(stack("cur_v", 1))   # the ground-truth clean chunk
+    if os.environ.get("DZ_BENCH_DIAG_ZERO_VGT"):  # diagnostics only (operand-dependent clocks): V_gt = 0
+        vc.zero_()
     pos = streams[0].cur_pos[sl].contiguous().to(dev)
     out = torch.empty_like(q)
     # parity sample (outside the timed region): the first attention of this config, batch element 0
