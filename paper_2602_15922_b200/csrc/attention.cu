@@ -806,9 +806,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // exchanged maxima.  O may be rescaled only when no PV into it is in flight:
           // wait for PV(j-1) (p_empty) first.  tcgen05.ld/st are warp-collective, so
           // the decision is warp-uniform.
-          float mx = s[0];
+          // row max as 8 independent chains (the single 128-long chain was 64 dependent
+          // FMNMX3 on the critical path of every step); max is exact in any order
+          float m8[8];
 #pragma unroll
-          for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+          for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+          for (int i = 8; i < 128; i += 8)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[i + k]);
+          float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
           red[hc * BM + row] = mx;
           ptx::named_bar_sync(pair_bar, 64);
           mx = fmaxf(mx, red[(hc ^ 1) * BM + row]);
