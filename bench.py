@@ -329,6 +329,7 @@ class Timer:
         prof = {"prologue": [], "attention": [], "append": []}
         launches = 0
         torch.cuda.synchronize()
+        dz.k2_clock(reset=True)  # SM cycles / ns summed over the attention CTAs of the timed steps
         sampler = ClockSampler(clock_dev) if clock_dev is not None else None
         if sampler:
             sampler.__enter__()
@@ -346,6 +347,8 @@ class Timer:
             ev[i][1].record()
             torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
+        cyc, ns = dz.k2_clock()
+        self.k2_ghz = cyc / ns if ns else None
         if sampler:
             sampler.__exit__()
         for i in range(steps if profiled else 0):
@@ -438,7 +441,7 @@ def secondary(dz, dev, steps, timer: Timer, cooldown=3.0):
                      "k2_peak": pk,
                      "prologue_ms": spread(prof["prologue"]), "prologue_gbs": pro_bytes / (pro * 1e-3) / 1e9,
                      "prologue_frac_hbm": pro_bytes / (pro * 1e-3) / 1e9 / hbm,
-                     "gpu_launches_per_step": launches / steps, "clocks": clk}
+                     "gpu_launches_per_step": launches / steps, "clocks": clk, "k2_sm_ghz": timer.k2_ghz}
         cache.close()
 
     chunk_line(synth.workload("C1"), "C1_fp8_qk", dz.FLAG_FP8_QK)   # NEXT-2: E4M3 QK^T, bf16 PV
@@ -795,7 +798,12 @@ def main():
                      # per-clock tensor efficiency: 148 SMs x 8192 dense bf16 FLOP/clk (tools/mma_bench.cu
                      # measures 8110-8170 for N >= 128) at the median SM clock sampled in the timed region
                      "frac_per_clock": (achieved * 1e12 / (148 * 8192 * clocks["sm_mhz"] * 1e6)
-                                        if clocks and clocks.get("sm_mhz") else None)},
+                                        if clocks and clocks.get("sm_mhz") else None),
+                     # the SM clock K2 actually ran at in the timed steps (clock64 / globaltimer of every
+                     # K2 CTA, dz_debug_k2_clock; NVML's 1 ms samples mostly see the flush and idle gaps)
+                     "k2_sm_ghz": getattr(timer, "k2_ghz", None),
+                     "frac_per_clock_k2": (achieved * 1e12 / (148 * 8192 * timer.k2_ghz * 1e9)
+                                           if getattr(timer, "k2_ghz", None) else None)},
         "kernels": {"prologue_ms": spread(prof["prologue"]) if profiled else None,
                     "prologue_gbs": pro_bytes / (pro_med * 1e-3) / 1e9 if profiled else None,
                     "append_ms": spread(prof["append"]) if profiled else None,

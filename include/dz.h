@@ -313,6 +313,13 @@ DZ_API dz_status dz_nccl_comm_destroy(void* comm);
  * Synchronous. */
 DZ_API dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset);
 
+/* Effective SM clock under the attention kernel: every attention launch adds, per
+ * CTA, its SM's clock64() cycles and %globaltimer nanoseconds between the end of its
+ * wait on the predecessor and its exit.  Copies {cycles, ns} (summed over CTAs and
+ * launches since the last reset) to host2[2] when host2 != NULL; reset != 0 then
+ * zeroes them.  cycles / ns is the mean SM clock in GHz.  Synchronous (device-wide). */
+DZ_API dz_status dz_debug_k2_clock(uint64_t* host2, int32_t reset);
+
 /* Pipeline diagnostics: enable != 0 makes later attention launches record a
  * clock() trace of CTA 0's first work unit (MMA waits/issues, softmax S-ready /
  * P-done per KV step, up to 256 steps; layout documented in attention.cu),

@@ -110,6 +110,7 @@ SIGNATURES = [
     ("dz_debug_trace", I32, [I32, P, SZ]),
     ("dz_kernel_launches", I64, []),
     ("dz_debug_l2_discard", I32, [P, SZ, P]),
+    ("dz_debug_k2_clock", I32, [P, I32]),
 ]
 
 _lib = None
@@ -158,6 +159,15 @@ def _need(t: torch.Tensor, name: str, dtype: torch.dtype, shape: Sequence[int], 
 def kernel_launches() -> int:
     """Kernels the library has enqueued in this process (host-side count at launch)."""
     return int(lib().dz_kernel_launches())
+
+
+def k2_clock(reset: bool = False):
+    """(SM cycles, ns) summed over attention CTAs since the last reset (dz_debug_k2_clock)."""
+    buf = (ctypes.c_uint64 * 2)()
+    s = lib().dz_debug_k2_clock(ctypes.cast(buf, ctypes.c_void_p), 1 if reset else 0)
+    if s:
+        raise DzError(s, "dz_debug_k2_clock")
+    return int(buf[0]), int(buf[1])
 
 
 def l2_discard(buf) -> None:

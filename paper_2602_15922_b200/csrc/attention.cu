@@ -92,6 +92,14 @@ __device__ int g_dz_trace_on;
 // [8 + 4i] start, [9 + 4i] last step's P written, [10 + 4i] O complete (o_full), [11 + 4i] end (clock()).
 constexpr int kTimelineCtas = 160, kTimelineWords = 64, kTlSegs = 14;
 __device__ uint32_t g_dz_timeline[kTimelineCtas * kTimelineWords];
+// Effective SM clock under K2 (dz_debug_k2_clock): every CTA's thread 0 adds its SM's cycles and
+// globaltimer nanoseconds from the end of the predecessor wait to the last cluster barrier.
+__device__ unsigned long long g_dz_k2clk[2];
+__device__ __forceinline__ uint64_t gtime64() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t gtime() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -146,6 +154,7 @@ constexpr int kMaxGroups = 64;    // stream-K schedule needs <= 64 query groups 
 struct Bars {
   uint64_t q_full, q_empty, s_full[2], s_free[2], p_full[2], p_empty[2], o_full, o_empty;
   uint64_t kv_full[12], kv_empty[12];
+  uint64_t clk0, ns0;               // thread 0: SM clock64 / globaltimer after the predecessor wait
   uint32_t tmem_base;
   int32_t last_piece;               // combine election result (softmax warps)
   int32_t gpre[kMaxGroups + 1];     // prefix sums of executed steps per query group
@@ -487,6 +496,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // (the schedule above depends on the launch parameters only: it is computed while the
   // predecessor finishes)
   ptx::pdl_wait();      // the prologue's Q' / K' / V (and everything before it) are complete
+  if (threadIdx.x == 0) {
+    bars->clk0 = clock64();
+    bars->ns0 = gtime64();
+  }
   Sched sched0;
   sched0.streamk = streamk;
   sched0.P = ncl;
@@ -1055,6 +1068,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::cluster_sync();  // no remote arrives / multicast commits may target an exited CTA
   ptx::tc_fence_after();
   if (warp == kWarpTmem) ptx::tmem_dealloc_2cta<512>(tmem);
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_dz_k2clk[0], (unsigned long long)(clock64() - bars->clk0));
+    atomicAdd(&g_dz_k2clk[1], (unsigned long long)(gtime64() - bars->ns0));
+  }
 }
 
 template <int D, bool PP, bool F8 = false>
@@ -1074,6 +1091,12 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+cudaError_t k2_clock(uint64_t* host2, int reset) {
+  cudaError_t e = host2 ? cudaMemcpyFromSymbol(host2, g_dz_k2clk, sizeof(uint64_t) * 2) : cudaSuccess;
+  if (e != cudaSuccess || !reset) return e;
+  const unsigned long long z[2] = {0, 0};
+  return cudaMemcpyToSymbol(g_dz_k2clk, z, sizeof(z));
+}
 cudaError_t read_watchdog(uint32_t* host8) {
   return cudaMemcpyFromSymbol(host8, ptx::g_dz_watchdog, sizeof(uint32_t) * 8);
 }

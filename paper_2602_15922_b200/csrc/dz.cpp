@@ -1216,6 +1216,10 @@ dz_status dz_debug_watchdog(uint32_t* host8, int32_t reset) {
   return DZ_OK;
 }
 
+dz_status dz_debug_k2_clock(uint64_t* host2, int32_t reset) {
+  return dz::k2_clock(host2, reset) == cudaSuccess ? DZ_OK : DZ_ECUDA;
+}
+
 dz_status dz_debug_trace(int32_t enable, uint32_t* host, size_t n) {
   return dz::trace_control(enable, host, n) == cudaSuccess ? DZ_OK : DZ_ECUDA;
 }

@@ -138,6 +138,7 @@ int attention_step_keys(float m_static);
 // (256-row query group, key step) tiles when attention_has_step_table(D, m_static)
 constexpr int kMaxStepTiles = 65536;
 bool attention_has_step_table(int32_t D, float m_static);
+cudaError_t k2_clock(uint64_t* host2, int reset);  // {SM cycles, globaltimer ns} summed over K2 CTAs
 cudaError_t read_watchdog(uint32_t* host8);   // {fired, block, warp, bar addr, parity, smid, bars base, 0}
 cudaError_t reset_watchdog();
 cudaError_t trace_control(int enable, uint32_t* host, size_t n);  // K2 cycle trace (CTA 0, first unit)  // work units (b, h, q-tile pair)
