@@ -562,3 +562,19 @@ def test_l2_discard_helper_leaves_no_launch_count_and_validates():
     s = dz.lib().dz_debug_l2_discard(ctypes.c_void_p(buf.data_ptr()), 100, None)
     assert s != 0
     assert dz.lib().dz_debug_l2_discard(None, 128, None) != 0
+
+
+def test_k2_clock_counters():
+    # dz_debug_k2_clock: every attention launch adds its CTAs' SM cycles and globaltimer ns; the
+    # ratio is a plausible SM clock (B200: at most 1.965 GHz) and a reset zeroes both sums
+    import paper_2602_15922_b200 as dz
+    run = GpuRun(_small("C1", heads=4, cached_chunks=2))
+    run.fill()
+    torch.cuda.synchronize()
+    dz.k2_clock(reset=True)
+    run.attend()
+    torch.cuda.synchronize()
+    cyc, ns = dz.k2_clock(reset=True)
+    assert cyc > 0 and ns > 0
+    assert 0.3 < cyc / ns < 2.2, cyc / ns
+    assert dz.k2_clock() == (0, 0)
