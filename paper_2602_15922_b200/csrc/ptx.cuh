@@ -84,13 +84,44 @@ template <bool kCluster = false>
 __device__ __forceinline__ bool mbar_try_wait_s(uint32_t bar, uint32_t parity) {
   return kCluster ? mbar_try_wait_cluster(bar, parity) : mbar_try_wait(bar, parity);
 }
+// try_wait with a suspend-time hint (ns): the waiting thread sleeps until the phase completes or
+// the hint expires, instead of re-polling after the system's default window (waiting warps
+// otherwise take issue slots from the working warps on their sub-partition)
+#ifndef DZ_WAIT_HINT
+#define DZ_WAIT_HINT 20000  // ns (C1, same box, alternated: step median 195.8-197.0 -> 193.7 us; 1 ms measured the same)
+#endif
+template <bool kCluster = false>
+__device__ __forceinline__ bool mbar_try_wait_h(uint32_t bar, uint32_t parity) {
+  if constexpr (DZ_WAIT_HINT == 0) {
+    return mbar_try_wait_s<kCluster>(bar, parity);
+  } else {
+    uint32_t ok;
+    if constexpr (kCluster)
+      asm volatile(
+          "{\n\t.reg .pred P;\n\t"
+          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, P;\n\t}"
+          : "=r"(ok)
+          : "r"(bar), "r"(parity), "r"((uint32_t)DZ_WAIT_HINT)
+          : "memory");
+    else
+      asm volatile(
+          "{\n\t.reg .pred P;\n\t"
+          "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, P;\n\t}"
+          : "=r"(ok)
+          : "r"(bar), "r"(parity), "r"((uint32_t)DZ_WAIT_HINT)
+          : "memory");
+    return ok != 0;
+  }
+}
 template <bool kCluster = false>
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   if (mbar_try_wait_s<kCluster>(bar, parity)) return;
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   uint32_t polls = 0;
-  while (!mbar_try_wait_s<kCluster>(bar, parity)) {
+  while (!mbar_try_wait_h<kCluster>(bar, parity)) {
     if ((++polls & 1023u) == 0) {
 #ifdef DZ_TRACE
       if (*((volatile uint32_t*)&g_dz_watchdog[0]) != 0) return;
