@@ -84,9 +84,9 @@ template <bool kCluster = false>
 __device__ __forceinline__ bool mbar_try_wait_s(uint32_t bar, uint32_t parity) {
   return kCluster ? mbar_try_wait_cluster(bar, parity) : mbar_try_wait(bar, parity);
 }
-// try_wait with a suspend-time hint (ns): the waiting thread sleeps until the phase completes or
-// the hint expires, instead of re-polling after the system's default window (waiting warps
-// otherwise take issue slots from the working warps on their sub-partition)
+// try_wait with a suspend-time hint (ns): the waiting thread may sleep until the phase completes
+// or the hint expires (measured: C1 step 195.8-197.0 -> 193.7 us; the executed poll count did not
+// drop)
 #ifndef DZ_WAIT_HINT
 #define DZ_WAIT_HINT 20000  // ns (C1, same box, alternated: step median 195.8-197.0 -> 193.7 us; 1 ms measured the same)
 #endif
